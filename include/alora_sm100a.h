@@ -1,0 +1,181 @@
+/*
+ * libalora_sm100a.so — C ABI of the B200 (sm_100a) aLoRA hot path.
+ *
+ * Drop-in boundary for /root/reference/pkg/src/aloraserve (pure Python/numpy).
+ * The reference has no FFI; every entry point below replaces one Python
+ * function of its hot path (file:line into /root/reference/pkg/src/aloraserve):
+ *
+ *   alora_hash_block / alora_hash_chain  <- kv_cache.py:41-69 hash_block, and the chain
+ *                                           walks of kv_cache.py:166-182, 253-260
+ *   alora_qkv_proj                       <- model.py:117-146 project_qkv_masked
+ *   alora_kv_write                       <- model.py:217-222 _write_kv
+ *   alora_paged_prefill_attn             <- model.py:149-187 paged_attention
+ *   alora_model_* (native executor)      <- model.py:233-272 Model.forward_step /
+ *                                           _forward_one, batched over all spans of a step
+ *   alora_argmax                         <- model.py:190-195 greedy_next_token
+ *
+ * Conventions
+ *   - Plain pointers and sizes only. Device pointers are CUDA global memory owned
+ *     by the caller; no entry point allocates device memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Return 0 (ALORA_OK) or a negative status; the Python shim maps
+ *     ALORA_EINVAL to ValueError and the rest to RuntimeError (the reference
+ *     raises ValueError for bad shapes, model.py:134-135, 162-163, 250-258).
+ *   - dtype: ALORA_F32 = fp32 storage with fp64 accumulation (the reference's
+ *     numerics, model.py:95-98); ALORA_BF16 = bf16 storage, fp32 accumulation
+ *     on tcgen05 tensor cores.
+ *   - KV pool layout is the reference's block-major [NB, L, 2, B, kv_width]
+ *     (kv_cache.py:143); a slot is block_id * B + (pos % B).
+ */
+#ifndef ALORA_SM100A_H
+#define ALORA_SM100A_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ALORA_OK 0
+#define ALORA_EINVAL (-1)
+#define ALORA_ECUDA (-2)
+#define ALORA_EUNSUPPORTED (-3)
+
+#define ALORA_F32 0
+#define ALORA_BF16 1
+
+#define ALORA_ARCH_REF 0   /* aloraserve model.py: sinusoidal pos, no-gain RMSNorm, MHA, ReLU 4x MLP */
+#define ALORA_ARCH_LLAMA 1 /* RoPE, GQA, SwiGLU, weighted RMSNorm, tied lm_head */
+
+/* ---------------------------------------------------------------- host ---- */
+
+/* Version string of the build (architecture, nvcc). */
+const char* alora_version(void);
+
+/* One block digest: blake2b-128 over the kv_cache.py:41-69 encoding.
+ * parent: 16 bytes or NULL (first block). tokens: block_size u32 ids. */
+int alora_hash_block(const uint8_t* parent, const uint32_t* tokens, int32_t block_size,
+                     const char* key, int32_t key_len, uint8_t* out_digest);
+
+/* Chain of n_blocks digests; block i hashes tokens[i*B, (i+1)*B) with key
+ * key_blob[key_off[i], key_off[i+1]) and parent = digest i-1 (or `parent`
+ * for i = 0, NULL = chain start). out_digests: n_blocks * 16 bytes. */
+int alora_hash_chain(const uint8_t* parent, const uint32_t* tokens, int64_t n_blocks,
+                     int32_t block_size, const char* key_blob, const int64_t* key_off,
+                     uint8_t* out_digests);
+
+/* ------------------------------------------------------ hot-path kernels ---- */
+
+/* Masked multi-adapter aLoRA Q/K/V projection (model.py:117-146).
+ *   x          [M, K] (dtype), row stride K
+ *   w_qkv_t    [Nq + 2*Nkv, K] (dtype): Wq|Wk|Wv transposed (K contiguous)
+ *   row_slot   [M] int32 adapter slot of the row, -1 = no adapter
+ *   row_apply  [M] uint8 1 = add the delta (activated: pos >= inv_start; standard: all rows)
+ *   lora_down  [3, n_slots, rank, K] (dtype) zero padded beyond each adapter's rank
+ *   lora_up_t  [Nq + 2*Nkv, n_slots*rank] (dtype): up_t^T for the target owning the column
+ *   slot_targets [n_slots] uint8 bit0 q, bit1 k, bit2 v
+ *   s_ws       workspace, >= 3*M*n_slots*rank elements (dtype) (shrink output)
+ *   out        [M, ld_out] (dtype): q at col 0, k at Nq, v at Nq+Nkv
+ * Rows with row_apply = 0 (or slot -1, or untargeted projections) are exactly
+ * the base product — row select, not blend (model.py:145). */
+int alora_qkv_proj(int32_t dtype, const void* x, int32_t M, int32_t K, const void* w_qkv_t,
+                   int32_t Nq, int32_t Nkv, const int32_t* row_slot, const uint8_t* row_apply,
+                   const void* lora_down, const void* lora_up_t, int32_t n_slots, int32_t rank,
+                   const uint8_t* slot_targets, void* s_ws, void* out, int32_t ld_out, void* stream);
+
+/* Paged KV scatter (model.py:217-222): for m < M with slot_mapping[m] >= 0,
+ * kv[blk, layer, 0, row, :] = k[m, :], kv[blk, layer, 1, row, :] = v[m, :],
+ * blk = slot / block_size, row = slot % block_size. Vectorised 16-byte stores. */
+int alora_kv_write(int32_t dtype, const void* k, const void* v, int64_t ld_src,
+                   const int32_t* slot_mapping, int32_t M, int32_t kv_width, void* kv_pool,
+                   int32_t n_layers, int32_t layer, int32_t block_size, void* stream);
+
+/* Paged causal prefill attention over the cache (model.py:149-187, GQA):
+ * sequence s owns query rows [cu_q[s], cu_q[s+1]) at absolute positions
+ * start_pos[s] + i and attends keys [0, start_pos[s] + i] read through
+ * block_table[s, :] (their K/V must already be in the pool: alora_kv_write).
+ *   q [n_rows, ld_q] (dtype) heads contiguous, out [n_rows, ld_out] (dtype); n_rows == cu_q[n_seqs].
+ * Scale is 1/sqrt(head_dim) as in model.py:179. Keys are visited in a fixed
+ * order of absolute positions, so results do not depend on chunking. */
+int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t n_rows,
+                             int32_t n_seqs, const int32_t* cu_q, const int32_t* start_pos,
+                             const int32_t* block_table, int32_t max_blocks, int32_t max_q,
+                             int32_t max_ctx, const void* kv_pool, int32_t n_layers, int32_t layer,
+                             int32_t block_size, int32_t n_heads, int32_t n_kv_heads,
+                             int32_t head_dim, void* out, int64_t ld_out, void* workspace,
+                             int64_t workspace_bytes, void* stream);
+
+/* Device workspace alora_paged_prefill_attn needs (bf16 split-KV partials; 0 for fp32). */
+int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs, int32_t max_q,
+                                   int32_t max_ctx, int32_t n_heads, int32_t n_kv_heads,
+                                   int32_t head_dim);
+
+/* Greedy next token per row of logits [rows, V] fp32: argmax, ties -> lowest id (model.py:190-195). */
+int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream);
+
+/* ------------------------------------------------------ native executor ---- */
+
+/* Model description: shapes plus device pointers (caller-owned). Per-layer
+ * pointers are arrays of n_layers device pointers living in HOST memory. */
+typedef struct AloraModelDesc {
+  int32_t arch, dtype;
+  int32_t n_layers, d_model, n_heads, n_kv_heads, head_dim, ffn_dim, vocab, max_seq_len;
+  float rms_eps, rope_theta;
+  int32_t max_tokens;            /* workspace capacity in rows per step */
+  int32_t max_seqs;              /* workspace capacity in spans per step */
+  /* weights (dtype), transposed to [out, in] */
+  const void* embed;             /* [V, d] */
+  const void* unembed_t;         /* [V, d] (ref: unembed^T; llama: == embed when tied) */
+  const float* pos_table;        /* ref: [max_seq_len, d] fp32 sinusoidal */
+  const float* rope_cos;         /* llama: [max_seq_len, head_dim/2] fp32 */
+  const float* rope_sin;
+  const float* final_norm;       /* llama: [d] fp32, ref: NULL */
+  const void* const* w_qkv_t;    /* [L] -> [Nq+2Nkv, d] */
+  const void* const* w_o_t;      /* [L] -> [d, Nq] */
+  const void* const* w_in_t;     /* [L] -> ref [4d, d] (ReLU) / llama [2F, d] gate|up interleaved per 64 */
+  const void* const* w_out_t;    /* [L] -> [d, F] */
+  const float* const* attn_norm; /* [L] -> [d] fp32 or NULL */
+  const float* const* mlp_norm;  /* [L] -> [d] fp32 or NULL */
+  /* adapters */
+  int32_t n_slots, lora_rank;
+  const void* const* lora_down;  /* [L] -> [3, n_slots, rank, d] */
+  const void* const* lora_up_t;  /* [L] -> [Nq+2Nkv, n_slots*rank] */
+  const uint8_t* slot_targets;   /* [n_slots] device */
+  /* paged KV pool */
+  void* kv_pool;                 /* [NB, L, 2, B, Hkv*D] (dtype) */
+  int32_t total_blocks, block_size;
+  /* workspace (caller-owned device memory, >= alora_model_workspace_bytes) */
+  void* workspace;
+  int64_t workspace_bytes;
+} AloraModelDesc;
+
+/* One engine step: all spans packed back to back (varlen). Device arrays. */
+typedef struct AloraStepDesc {
+  int32_t n_tokens, n_seqs, max_blocks, max_q, max_ctx;
+  const int32_t* tokens;        /* [M] */
+  const int32_t* positions;     /* [M] absolute */
+  const int32_t* slot_mapping;  /* [M] */
+  const int32_t* row_slot;      /* [M] adapter slot or -1 */
+  const uint8_t* row_apply;     /* [M] */
+  const int32_t* cu_q;          /* [S+1] */
+  const int32_t* start_pos;     /* [S] */
+  const int32_t* block_table;   /* [S, max_blocks] */
+  const int32_t* last_row;      /* [S] row whose logits are produced */
+  float* logits;                /* [S, V] fp32 out */
+  int32_t* next_ids;            /* [S] argmax out */
+} AloraStepDesc;
+
+int64_t alora_model_workspace_bytes(const AloraModelDesc* desc);
+int alora_model_create(const AloraModelDesc* desc, void** out_handle);
+int alora_model_destroy(void* handle);
+/* Run every layer for one packed step: embed -> L x [norm, masked QKV (+LoRA),
+ * KV write, paged attention, O-proj, MLP] -> last-row logits -> argmax. */
+int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream);
+/* Count of kernel launches issued by the last alora_model_forward. */
+int32_t alora_model_last_launches(void* handle);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* ALORA_SM100A_H */

@@ -1,0 +1,121 @@
+"""ctypes binding of libalora_sm100a.so (include/alora_sm100a.h).
+
+The product path has no CPU fallback: if the library is missing this module
+raises at import, and device entry points raise if CUDA is unavailable.
+Statuses map like the reference's errors: ALORA_EINVAL -> ValueError,
+everything else -> RuntimeError.
+"""
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libalora_sm100a.so")
+
+ALORA_OK = 0
+ALORA_EINVAL = -1
+ALORA_ECUDA = -2
+ALORA_EUNSUPPORTED = -3
+ALORA_F32 = 0
+ALORA_BF16 = 1
+ALORA_ARCH_REF = 0
+ALORA_ARCH_LLAMA = 1
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(or `make -C paper_2512_17910_b200`). There is no CPU fallback."
+    )
+
+lib = ctypes.CDLL(LIB_PATH)
+
+c_void_p = ctypes.c_void_p
+c_i32 = ctypes.c_int32
+c_i64 = ctypes.c_int64
+c_f32 = ctypes.c_float
+c_u8p = ctypes.POINTER(ctypes.c_uint8)
+
+
+class AloraModelDesc(ctypes.Structure):
+    _fields_ = [
+        ("arch", c_i32), ("dtype", c_i32),
+        ("n_layers", c_i32), ("d_model", c_i32), ("n_heads", c_i32), ("n_kv_heads", c_i32),
+        ("head_dim", c_i32), ("ffn_dim", c_i32), ("vocab", c_i32), ("max_seq_len", c_i32),
+        ("rms_eps", c_f32), ("rope_theta", c_f32),
+        ("max_tokens", c_i32), ("max_seqs", c_i32),
+        ("embed", c_void_p), ("unembed_t", c_void_p), ("pos_table", c_void_p),
+        ("rope_cos", c_void_p), ("rope_sin", c_void_p), ("final_norm", c_void_p),
+        ("w_qkv_t", ctypes.POINTER(c_void_p)), ("w_o_t", ctypes.POINTER(c_void_p)),
+        ("w_in_t", ctypes.POINTER(c_void_p)), ("w_out_t", ctypes.POINTER(c_void_p)),
+        ("attn_norm", ctypes.POINTER(c_void_p)), ("mlp_norm", ctypes.POINTER(c_void_p)),
+        ("n_slots", c_i32), ("lora_rank", c_i32),
+        ("lora_down", ctypes.POINTER(c_void_p)), ("lora_up_t", ctypes.POINTER(c_void_p)),
+        ("slot_targets", c_void_p),
+        ("kv_pool", c_void_p), ("total_blocks", c_i32), ("block_size", c_i32),
+        ("workspace", c_void_p), ("workspace_bytes", c_i64),
+    ]
+
+
+class AloraStepDesc(ctypes.Structure):
+    _fields_ = [
+        ("n_tokens", c_i32), ("n_seqs", c_i32), ("max_blocks", c_i32), ("max_q", c_i32), ("max_ctx", c_i32),
+        ("tokens", c_void_p), ("positions", c_void_p), ("slot_mapping", c_void_p), ("row_slot", c_void_p),
+        ("row_apply", c_void_p), ("cu_q", c_void_p), ("start_pos", c_void_p), ("block_table", c_void_p),
+        ("last_row", c_void_p), ("logits", c_void_p), ("next_ids", c_void_p),
+    ]
+
+
+def _sig(name, restype, *argtypes):
+    fn = getattr(lib, name)
+    fn.restype = restype
+    fn.argtypes = list(argtypes)
+    return fn
+
+
+# Every symbol declared in include/alora_sm100a.h (tests check this list against the header).
+EXPORTS = {
+    "alora_version": _sig("alora_version", ctypes.c_char_p),
+    "alora_hash_block": _sig("alora_hash_block", c_i32, c_void_p, c_void_p, c_i32, ctypes.c_char_p, c_i32, c_void_p),
+    "alora_hash_chain": _sig("alora_hash_chain", c_i32, c_void_p, c_void_p, c_i64, c_i32, ctypes.c_char_p,
+                             c_void_p, c_void_p),
+    "alora_qkv_proj": _sig("alora_qkv_proj", c_i32, c_i32, c_void_p, c_i32, c_i32, c_void_p, c_i32, c_i32,
+                           c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
+                           c_i32, c_void_p),
+    "alora_kv_write": _sig("alora_kv_write", c_i32, c_i32, c_void_p, c_void_p, c_i64, c_void_p, c_i32, c_i32,
+                           c_void_p, c_i32, c_i32, c_i32, c_void_p),
+    "alora_paged_prefill_attn": _sig("alora_paged_prefill_attn", c_i32, c_i32, c_void_p, c_i64, c_i32, c_i32,
+                                     c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, c_i32, c_i32,
+                                     c_i32, c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p, c_i64, c_void_p),
+    "alora_attn_workspace_bytes": _sig("alora_attn_workspace_bytes", c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                       c_i32, c_i32, c_i32),
+    "alora_argmax": _sig("alora_argmax", c_i32, c_void_p, c_i32, c_i32, c_void_p, c_void_p),
+    "alora_model_workspace_bytes": _sig("alora_model_workspace_bytes", c_i64, ctypes.POINTER(AloraModelDesc)),
+    "alora_model_create": _sig("alora_model_create", c_i32, ctypes.POINTER(AloraModelDesc),
+                               ctypes.POINTER(c_void_p)),
+    "alora_model_destroy": _sig("alora_model_destroy", c_i32, c_void_p),
+    "alora_model_forward": _sig("alora_model_forward", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc), c_void_p),
+    "alora_model_last_launches": _sig("alora_model_last_launches", c_i32, c_void_p),
+}
+
+
+def check(rc: int, what: str) -> None:
+    if rc == ALORA_OK:
+        return
+    if rc == ALORA_EINVAL:
+        raise ValueError(f"{what}: invalid argument (ALORA_EINVAL)")
+    if rc == ALORA_EUNSUPPORTED:
+        raise RuntimeError(f"{what}: unsupported configuration (ALORA_EUNSUPPORTED)")
+    raise RuntimeError(f"{what}: CUDA error (status {rc})")
+
+
+def require_cuda():
+    """The device path is the only path: fail loudly without a GPU."""
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("libalora_sm100a needs a CUDA device (B200, sm_100a); no CPU fallback exists")
+    return torch
+
+
+def version() -> str:
+    return lib.alora_version().decode()

@@ -1,0 +1,178 @@
+// Native block-hash chain: blake2b-128 over the reference's exact byte encoding.
+//
+// Replaces the per-block Python hashlib loop of
+//   /root/reference/pkg/src/aloraserve/kv_cache.py:41-69   (hash_block)
+//   kv_cache.py:166-182  (find_cached_prefix chain walk)
+//   kv_cache.py:253-260  (commit_and_free re-hash)
+// Message per block (all integers little endian):
+//   "aloraserve.block.v1" | 0x00            (no parent)
+//                         | 0x01 parent[16] (chained)
+//   | u32(len(key)) key | u32(block_size) | u32(token) x block_size
+// BLAKE2b is RFC 7693 with digest length 16, no key, no salt/personal.
+
+#include <cstdint>
+#include <cstring>
+#include <vector>
+
+#include "../../include/alora_sm100a.h"
+
+namespace {
+
+constexpr uint64_t kIV[8] = {
+    0x6a09e667f3bcc908ULL, 0xbb67ae8584caa73bULL, 0x3c6ef372fe94f82bULL, 0xa54ff53a5f1d36f1ULL,
+    0x510e527fade682d1ULL, 0x9b05688c2b3e6c1fULL, 0x1f83d9abfb41bd6bULL, 0x5be0cd19137e2179ULL};
+
+constexpr uint8_t kSigma[12][16] = {
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3},
+    {11, 8, 12, 0, 5, 2, 15, 13, 10, 14, 3, 6, 7, 1, 9, 4},
+    {7, 9, 3, 1, 13, 12, 11, 14, 2, 6, 5, 10, 4, 0, 15, 8},
+    {9, 0, 5, 7, 2, 4, 10, 15, 14, 1, 11, 12, 6, 8, 3, 13},
+    {2, 12, 6, 10, 0, 11, 8, 3, 4, 13, 7, 5, 15, 14, 1, 9},
+    {12, 5, 1, 15, 14, 13, 4, 10, 0, 7, 6, 3, 9, 2, 8, 11},
+    {13, 11, 7, 14, 12, 1, 3, 9, 5, 0, 15, 4, 8, 6, 2, 10},
+    {6, 15, 14, 9, 11, 3, 0, 8, 12, 2, 13, 7, 1, 4, 10, 5},
+    {10, 2, 8, 4, 7, 6, 1, 5, 15, 11, 9, 14, 3, 12, 13, 0},
+    {0, 1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 11, 12, 13, 14, 15},
+    {14, 10, 4, 8, 9, 15, 13, 6, 1, 12, 0, 2, 11, 7, 5, 3}};
+
+inline uint64_t rotr(uint64_t x, int n) { return (x >> n) | (x << (64 - n)); }
+
+inline uint64_t load64(const uint8_t* p) {
+  uint64_t v;
+  std::memcpy(&v, p, 8);  // host is little endian (x86_64 / aarch64)
+  return v;
+}
+
+struct Blake2b {
+  uint64_t h[8];
+  uint64_t t0 = 0, t1 = 0;
+  uint8_t buf[128];
+  size_t fill = 0;
+  size_t outlen;
+
+  explicit Blake2b(size_t out) : outlen(out) {
+    for (int i = 0; i < 8; ++i) h[i] = kIV[i];
+    h[0] ^= 0x01010000ULL ^ static_cast<uint64_t>(out);
+  }
+
+  void compress(const uint8_t* block, bool last) {
+    uint64_t m[16], v[16];
+    for (int i = 0; i < 16; ++i) m[i] = load64(block + 8 * i);
+    for (int i = 0; i < 8; ++i) {
+      v[i] = h[i];
+      v[i + 8] = kIV[i];
+    }
+    v[12] ^= t0;
+    v[13] ^= t1;
+    if (last) v[14] = ~v[14];
+#define G(a, b, c, d, x, y)          \
+  do {                               \
+    v[a] = v[a] + v[b] + (x);        \
+    v[d] = rotr(v[d] ^ v[a], 32);    \
+    v[c] = v[c] + v[d];              \
+    v[b] = rotr(v[b] ^ v[c], 24);    \
+    v[a] = v[a] + v[b] + (y);        \
+    v[d] = rotr(v[d] ^ v[a], 16);    \
+    v[c] = v[c] + v[d];              \
+    v[b] = rotr(v[b] ^ v[c], 63);    \
+  } while (0)
+    for (int r = 0; r < 12; ++r) {
+      const uint8_t* s = kSigma[r];
+      G(0, 4, 8, 12, m[s[0]], m[s[1]]);
+      G(1, 5, 9, 13, m[s[2]], m[s[3]]);
+      G(2, 6, 10, 14, m[s[4]], m[s[5]]);
+      G(3, 7, 11, 15, m[s[6]], m[s[7]]);
+      G(0, 5, 10, 15, m[s[8]], m[s[9]]);
+      G(1, 6, 11, 12, m[s[10]], m[s[11]]);
+      G(2, 7, 8, 13, m[s[12]], m[s[13]]);
+      G(3, 4, 9, 14, m[s[14]], m[s[15]]);
+    }
+#undef G
+    for (int i = 0; i < 8; ++i) h[i] ^= v[i] ^ v[i + 8];
+  }
+
+  void update(const uint8_t* p, size_t n) {
+    while (n > 0) {
+      if (fill == 128) {  // only compress a full buffer once more input arrives
+        t0 += 128;
+        if (t0 < 128) ++t1;
+        compress(buf, false);
+        fill = 0;
+      }
+      size_t take = 128 - fill;
+      if (take > n) take = n;
+      std::memcpy(buf + fill, p, take);
+      fill += take;
+      p += take;
+      n -= take;
+    }
+  }
+
+  void u32(uint32_t x) {
+    uint8_t b[4] = {uint8_t(x), uint8_t(x >> 8), uint8_t(x >> 16), uint8_t(x >> 24)};
+    update(b, 4);
+  }
+
+  void final(uint8_t* out) {
+    t0 += fill;
+    if (t0 < fill) ++t1;
+    std::memset(buf + fill, 0, 128 - fill);
+    compress(buf, true);
+    uint8_t full[64];
+    std::memcpy(full, h, 64);
+    std::memcpy(out, full, outlen);
+  }
+};
+
+const char kDomain[] = "aloraserve.block.v1";
+
+void hash_one(const uint8_t* parent, const uint32_t* tokens, int32_t block_size, const char* key,
+              int32_t key_len, uint8_t* out) {
+  Blake2b b(16);
+  b.update(reinterpret_cast<const uint8_t*>(kDomain), sizeof(kDomain) - 1);
+  if (parent == nullptr) {
+    uint8_t z = 0;
+    b.update(&z, 1);
+  } else {
+    uint8_t one = 1;
+    b.update(&one, 1);
+    b.update(parent, 16);
+  }
+  b.u32(static_cast<uint32_t>(key_len));
+  if (key_len > 0) b.update(reinterpret_cast<const uint8_t*>(key), static_cast<size_t>(key_len));
+  b.u32(static_cast<uint32_t>(block_size));
+  // tokens are already u32 little-endian in memory on the host
+  b.update(reinterpret_cast<const uint8_t*>(tokens), static_cast<size_t>(block_size) * 4);
+  b.final(out);
+}
+
+}  // namespace
+
+extern "C" {
+
+int alora_hash_block(const uint8_t* parent, const uint32_t* tokens, int32_t block_size, const char* key,
+                     int32_t key_len, uint8_t* out_digest) {
+  if (tokens == nullptr || out_digest == nullptr || block_size < 1 || key_len < 0) return ALORA_EINVAL;
+  if (key_len > 0 && key == nullptr) return ALORA_EINVAL;
+  hash_one(parent, tokens, block_size, key, key_len, out_digest);
+  return ALORA_OK;
+}
+
+int alora_hash_chain(const uint8_t* parent, const uint32_t* tokens, int64_t n_blocks, int32_t block_size,
+                     const char* key_blob, const int64_t* key_off, uint8_t* out_digests) {
+  if (n_blocks < 0 || block_size < 1) return ALORA_EINVAL;
+  if (n_blocks == 0) return ALORA_OK;
+  if (tokens == nullptr || key_off == nullptr || out_digests == nullptr) return ALORA_EINVAL;
+  const uint8_t* prev = parent;
+  for (int64_t i = 0; i < n_blocks; ++i) {
+    const int64_t k0 = key_off[i], k1 = key_off[i + 1];
+    if (k1 < k0) return ALORA_EINVAL;
+    hash_one(prev, tokens + i * block_size, block_size, key_blob + k0, static_cast<int32_t>(k1 - k0),
+             out_digests + 16 * i);
+    prev = out_digests + 16 * i;
+  }
+  return ALORA_OK;
+}
+
+}  // extern "C"

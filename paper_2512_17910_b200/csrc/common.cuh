@@ -1,0 +1,90 @@
+// Shared helpers for the sm_100a kernels of libalora_sm100a.so.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/alora_sm100a.h"
+
+#define ALORA_CUDA_CHECK(expr)                  \
+  do {                                          \
+    cudaError_t _e = (expr);                    \
+    if (_e != cudaSuccess) return ALORA_ECUDA;  \
+  } while (0)
+
+#define ALORA_LAUNCH_CHECK()                          \
+  do {                                                \
+    cudaError_t _e = cudaGetLastError();              \
+    if (_e != cudaSuccess) return ALORA_ECUDA;        \
+  } while (0)
+
+namespace alora {
+
+constexpr int kNumSMs = 148;
+constexpr int kGluBlock = 64;  // gate|up interleave granularity of w_in_t (llama)
+
+__device__ __forceinline__ float to_f32(float v) { return v; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 v) { return __bfloat162float(v); }
+
+template <typename T>
+__device__ __forceinline__ T from_f32(float v);
+template <>
+__device__ __forceinline__ float from_f32<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Block-wide reductions in a fixed order (deterministic): warp tree, then warp 0.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* smem /* >= 32 */) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = (lane < nw) ? smem[lane] : T(0);
+  if (wid == 0) r = warp_sum(r);
+  if (threadIdx.x == 0) smem[0] = r;
+  __syncthreads();
+  return smem[0];
+}
+
+template <typename T>
+__device__ __forceinline__ T block_max(T v, T* smem, T lowest) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_max(v);
+  __syncthreads();
+  if (lane == 0) smem[wid] = v;
+  __syncthreads();
+  T r = (lane < nw) ? smem[lane] : lowest;
+  if (wid == 0) r = warp_max(r);
+  if (threadIdx.x == 0) smem[0] = r;
+  __syncthreads();
+  return smem[0];
+}
+
+// Sequence owning packed row m: cu_q is ascending with cu_q[0] = 0.
+__device__ __forceinline__ int seq_of_row(const int32_t* cu_q, int n_seqs, int m) {
+  int lo = 0, hi = n_seqs - 1;
+  while (lo < hi) {
+    int mid = (lo + hi + 1) >> 1;
+    if (cu_q[mid] <= m) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+}  // namespace alora

@@ -1,0 +1,64 @@
+// Internal launchers (host functions) shared by capi.cu and runtime.cu.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace alora {
+
+enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3 };
+
+// ---- fp32 storage / fp64 accumulation (parity tier), parity_f64.cu
+int embed_f32(const int32_t* tokens, const int32_t* positions, const float* embed, const float* pos_table, int M,
+              int d, float* x, cudaStream_t st);
+int rmsnorm_f64(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps, float* out,
+                cudaStream_t st);
+int gemm_f64(int epi, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc, int M, int N, int K,
+             cudaStream_t st);
+int lora_f64(const float* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply, const float* down,
+             const float* up_t, int n_slots, int R, const uint8_t* slot_targets, float* s_ws, int Nq, int Nkv,
+             float* out, int ld_out, cudaStream_t st);
+int rope_f64(float* qkv, int ld, const int32_t* positions, int M, int H, int Hkv, int D, const float* cos_t,
+             const float* sin_t, cudaStream_t st);
+int silu_mul_f64(const float* gu, int M, int F, float* a, cudaStream_t st);
+int attn_f64(const float* q, int64_t ld_q, int M, int n_seqs, const int32_t* cu_q, const int32_t* start_pos,
+             const int32_t* block_table, int max_blocks, const float* kv, int n_layers, int layer, int B, int H,
+             int Hkv, int D, float unused, float* out, int64_t ld_out, cudaStream_t st);
+
+// ---- dtype-generic, kv_write.cu / misc.cu
+int kv_write(int dtype, const void* k, const void* v, int64_t ld_src, const int32_t* slot_mapping, int M,
+             int kv_width, void* kv_pool, int n_layers, int layer, int B, cudaStream_t st);
+int argmax_rows(const float* logits, int rows, int vocab, int32_t* out_ids, cudaStream_t st);
+
+// ---- bf16 storage / fp32 accumulation (tensor-core tier)
+int embed_bf16(const int32_t* tokens, const int32_t* positions, const __nv_bfloat16* embed, const float* pos_table,
+               int M, int d, float* x, cudaStream_t st);
+// out_bf16[r] = bf16( rmsnorm(x[rows[r]]) * w )
+int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps,
+                 __nv_bfloat16* out, cudaStream_t st);
+int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+                     const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets, __nv_bfloat16* s,
+                     cudaStream_t st);
+int rope_bf16(__nv_bfloat16* qkv, int ld, const int32_t* positions, int M, int H, int Hkv, int D,
+              const float* cos_t, const float* sin_t, cudaStream_t st);
+int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int32_t* cu_q,
+              const int32_t* start_pos, const int32_t* block_table, int max_blocks, int max_q, int max_ctx,
+              const __nv_bfloat16* kv, int n_layers, int layer, int B, int H, int Hkv, int D,
+              __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes, cudaStream_t st);
+int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D);
+
+// tcgen05 GEMM: C = epi(A[M,K] @ Bt[N,K]^T (+ S_t[M,Ks] @ Ut[N,Ks]^T lora part)), bf16 in, fp32 accumulate.
+struct GemmLora {
+  const __nv_bfloat16* s = nullptr;    // [3][M][Ks] shrink output (K-major), nullptr = no LoRA
+  const __nv_bfloat16* up_t = nullptr; // [N][Ks]
+  int ks = 0;                          // n_slots * rank
+  int n_q = 0, n_kv = 0;               // column ranges of the q|k|v targets
+  const uint32_t* tile_slot_mask = nullptr;  // [ceil(M/128)] bitmask of slots present (taking the delta)
+  int rank = 0;
+};
+int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* C, int ldc,
+              int M, int N, int K, const GemmLora* lora, cudaStream_t st);
+int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st);
+
+}  // namespace alora

@@ -1,0 +1,364 @@
+// C ABI entry points and the native step executor.
+//
+// alora_model_forward replaces Model.forward_step / _forward_one
+// (model.py:233-272): instead of a Python loop per span and per layer, all
+// spans of an engine step are packed into one varlen batch and every layer's
+// kernels are launched from here, on the caller's stream, with no host sync.
+
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace alora;
+
+namespace {
+
+struct Model {
+  AloraModelDesc d;
+  std::vector<const void*> w_qkv_t, w_o_t, w_in_t, w_out_t, lora_down, lora_up_t;
+  std::vector<const float*> attn_norm, mlp_norm;
+  int32_t last_launches = 0;
+};
+
+inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+// Workspace carve-up shared by alora_model_workspace_bytes and the executor.
+struct Ws {
+  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, total;
+  int64_t attn_ws_bytes;
+};
+
+Ws plan_ws(const AloraModelDesc& d) {
+  const int64_t T = d.max_tokens, S = d.max_seqs;
+  const int64_t e = d.dtype == ALORA_BF16 ? 2 : 4;
+  const int64_t nq = (int64_t)d.n_heads * d.head_dim, nkv = (int64_t)d.n_kv_heads * d.head_dim;
+  const int64_t F = d.ffn_dim;
+  const int64_t ks = (int64_t)d.n_slots * d.lora_rank;
+  Ws w{};
+  int64_t off = 0;
+  auto take = [&](int64_t bytes) { int64_t o = off; off = align_up(off + bytes, 256); return o; };
+  w.x = take(T * d.d_model * 4);
+  w.h = take(T * d.d_model * e);
+  w.qkv = take(T * (nq + 2 * nkv) * e);
+  w.attn = take(T * nq * e);
+  w.gu = take(d.arch == ALORA_ARCH_LLAMA && d.dtype == ALORA_F32 ? T * 2 * F * 4 : 0);
+  w.act = take(T * F * e);
+  w.s = take(d.dtype == ALORA_BF16 ? 3 * T * ks * 2 : 3 * T * d.lora_rank * 4);
+  w.masks = take((T / 128 + 2) * 4);
+  w.hf = take(S * d.d_model * e);
+  w.attn_ws_bytes = d.dtype == ALORA_BF16
+                        ? attn_bf16_workspace(d.max_tokens, d.max_seqs, d.max_tokens, d.max_seq_len, d.n_heads,
+                                              d.n_kv_heads, d.head_dim)
+                        : 0;
+  w.attn_ws = take(w.attn_ws_bytes);
+  w.total = off;
+  return w;
+}
+
+int validate(const AloraModelDesc* d) {
+  if (!d) return ALORA_EINVAL;
+  if (d->arch != ALORA_ARCH_REF && d->arch != ALORA_ARCH_LLAMA) return ALORA_EINVAL;
+  if (d->dtype != ALORA_F32 && d->dtype != ALORA_BF16) return ALORA_EINVAL;
+  if (d->n_layers < 1 || d->d_model < 1 || d->n_heads < 1 || d->n_kv_heads < 1 || d->head_dim < 2 ||
+      d->ffn_dim < 1 || d->vocab < 1 || d->max_tokens < 1 || d->max_seqs < 1)
+    return ALORA_EINVAL;
+  if (d->n_heads % d->n_kv_heads != 0 || d->head_dim % 2 != 0) return ALORA_EINVAL;
+  if (d->arch == ALORA_ARCH_REF && (d->n_kv_heads != d->n_heads || d->n_heads * d->head_dim != d->d_model))
+    return ALORA_EINVAL;
+  if (d->n_slots < 0 || d->lora_rank < 0 || (d->n_slots > 0 && d->lora_rank < 1)) return ALORA_EINVAL;
+  if (d->dtype == ALORA_BF16 && d->n_slots > 32) return ALORA_EINVAL;  // tile slot masks are 32-bit
+  return ALORA_OK;
+}
+
+int forward_f32(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
+  const AloraModelDesc& d = mdl.d;
+  const Ws w = plan_ws(d);
+  char* base = static_cast<char*>(d.workspace);
+  float* x = reinterpret_cast<float*>(base + w.x);
+  float* h = reinterpret_cast<float*>(base + w.h);
+  float* qkv = reinterpret_cast<float*>(base + w.qkv);
+  float* attn = reinterpret_cast<float*>(base + w.attn);
+  float* gu = reinterpret_cast<float*>(base + w.gu);
+  float* act = reinterpret_cast<float*>(base + w.act);
+  float* sws = reinterpret_cast<float*>(base + w.s);
+  float* hf = reinterpret_cast<float*>(base + w.hf);
+  const int M = s.n_tokens, S = s.n_seqs, dm = d.d_model, F = d.ffn_dim;
+  const int H = d.n_heads, Hkv = d.n_kv_heads, D = d.head_dim;
+  const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
+  const bool llama = d.arch == ALORA_ARCH_LLAMA;
+  int n = 0;
+  int rc;
+#define RUN(call)                      \
+  do {                                 \
+    rc = (call);                       \
+    if (rc != ALORA_OK) return rc;     \
+    ++n;                               \
+  } while (0)
+  RUN(embed_f32(s.tokens, s.positions, static_cast<const float*>(d.embed), llama ? nullptr : d.pos_table, M, dm, x,
+                st));
+  for (int l = 0; l < d.n_layers; ++l) {
+    RUN(rmsnorm_f64(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    RUN(gemm_f64(kEpiStore, h, dm, static_cast<const float*>(mdl.w_qkv_t[l]), dm, qkv, Nqkv, M, Nqkv, dm, st));
+    if (d.n_slots > 0) {
+      RUN(lora_f64(h, M, dm, s.row_slot, s.row_apply, static_cast<const float*>(mdl.lora_down[l]),
+                   static_cast<const float*>(mdl.lora_up_t[l]), d.n_slots, d.lora_rank, d.slot_targets, sws, Nq, Nkv,
+                   qkv, Nqkv, st));
+      ++n;  // shrink + expand
+    }
+    if (llama) RUN(rope_f64(qkv, Nqkv, s.positions, M, H, Hkv, D, d.rope_cos, d.rope_sin, st));
+    RUN(kv_write(ALORA_F32, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
+                 d.block_size, st));
+    RUN(attn_f64(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks,
+                 static_cast<const float*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, 0.f, attn, Nq, st));
+    RUN(gemm_f64(kEpiAdd, attn, Nq, static_cast<const float*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq, st));
+    RUN(rmsnorm_f64(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    if (llama) {
+      RUN(gemm_f64(kEpiStore, h, dm, static_cast<const float*>(mdl.w_in_t[l]), dm, gu, 2 * F, M, 2 * F, dm, st));
+      RUN(silu_mul_f64(gu, M, F, act, st));
+    } else {
+      RUN(gemm_f64(kEpiRelu, h, dm, static_cast<const float*>(mdl.w_in_t[l]), dm, act, F, M, F, dm, st));
+    }
+    RUN(gemm_f64(kEpiAdd, act, F, static_cast<const float*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, st));
+  }
+  RUN(rmsnorm_f64(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
+  RUN(gemm_f64(kEpiStore, hf, dm, static_cast<const float*>(d.unembed_t), dm, s.logits, d.vocab, S, d.vocab, dm,
+               st));
+  RUN(argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
+#undef RUN
+  mdl.last_launches = n;
+  return ALORA_OK;
+}
+
+int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
+  const AloraModelDesc& d = mdl.d;
+  const Ws w = plan_ws(d);
+  char* base = static_cast<char*>(d.workspace);
+  float* x = reinterpret_cast<float*>(base + w.x);
+  auto* h = reinterpret_cast<__nv_bfloat16*>(base + w.h);
+  auto* qkv = reinterpret_cast<__nv_bfloat16*>(base + w.qkv);
+  auto* attn = reinterpret_cast<__nv_bfloat16*>(base + w.attn);
+  auto* act = reinterpret_cast<__nv_bfloat16*>(base + w.act);
+  auto* sws = reinterpret_cast<__nv_bfloat16*>(base + w.s);
+  auto* masks = reinterpret_cast<uint32_t*>(base + w.masks);
+  auto* hf = reinterpret_cast<__nv_bfloat16*>(base + w.hf);
+  void* aws = base + w.attn_ws;
+  const int M = s.n_tokens, S = s.n_seqs, dm = d.d_model, F = d.ffn_dim;
+  const int H = d.n_heads, Hkv = d.n_kv_heads, D = d.head_dim;
+  const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
+  const bool llama = d.arch == ALORA_ARCH_LLAMA;
+  const bool lora = d.n_slots > 0;
+  int n = 0;
+  int rc;
+#define RUN(call)                      \
+  do {                                 \
+    rc = (call);                       \
+    if (rc != ALORA_OK) return rc;     \
+    ++n;                               \
+  } while (0)
+  RUN(embed_bf16(s.tokens, s.positions, static_cast<const __nv_bfloat16*>(d.embed), llama ? nullptr : d.pos_table,
+                 M, dm, x, st));
+  if (lora) RUN(lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
+  for (int l = 0; l < d.n_layers; ++l) {
+    RUN(rmsnorm_bf16(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    GemmLora gl;
+    if (lora) {
+      RUN(lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
+                           d.n_slots, d.lora_rank, d.slot_targets, sws, st));
+      gl.s = sws;
+      gl.up_t = static_cast<const __nv_bfloat16*>(mdl.lora_up_t[l]);
+      gl.ks = d.n_slots * d.lora_rank;
+      gl.n_q = Nq;
+      gl.n_kv = Nkv;
+      gl.tile_slot_mask = masks;
+      gl.rank = d.lora_rank;
+    }
+    RUN(gemm_bf16(kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv, Nqkv, M, Nqkv, dm,
+                  lora ? &gl : nullptr, st));
+    if (llama) RUN(rope_bf16(qkv, Nqkv, s.positions, M, H, Hkv, D, d.rope_cos, d.rope_sin, st));
+    RUN(kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
+                 d.block_size, st));
+    RUN(attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
+                  static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
+                  aws, w.attn_ws_bytes, st));
+    RUN(gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq,
+                  nullptr, st));
+    RUN(rmsnorm_bf16(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    RUN(gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act,
+                  F, M, llama ? 2 * F : F, dm, nullptr, st));
+    RUN(gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
+                  st));
+  }
+  RUN(rmsnorm_bf16(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
+  RUN(gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm,
+                s.logits, d.vocab, S, d.vocab, dm, nullptr, st));
+  RUN(argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
+#undef RUN
+  mdl.last_launches = n;
+  return ALORA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* alora_version(void) {
+  return "libalora_sm100a 0.1 (sm_100a, tcgen05/TMA; fp64-acc parity tier + bf16 tensor-core tier)";
+}
+
+int alora_qkv_proj(int32_t dtype, const void* x, int32_t M, int32_t K, const void* w_qkv_t, int32_t Nq,
+                   int32_t Nkv, const int32_t* row_slot, const uint8_t* row_apply, const void* lora_down,
+                   const void* lora_up_t, int32_t n_slots, int32_t rank, const uint8_t* slot_targets, void* s_ws,
+                   void* out, int32_t ld_out, void* stream) {
+  if (M < 0 || K < 1 || Nq < 1 || Nkv < 1 || ld_out < Nq + 2 * Nkv) return ALORA_EINVAL;
+  if (M == 0) return ALORA_OK;
+  if (!x || !w_qkv_t || !out) return ALORA_EINVAL;
+  const bool lora = n_slots > 0 && rank > 0 && lora_down && lora_up_t && row_slot && row_apply && slot_targets && s_ws;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int N = Nq + 2 * Nkv;
+  int rc;
+  if (dtype == ALORA_F32) {
+    rc = gemm_f64(kEpiStore, static_cast<const float*>(x), K, static_cast<const float*>(w_qkv_t), K,
+                  static_cast<float*>(out), ld_out, M, N, K, st);
+    if (rc != ALORA_OK || !lora) return rc;
+    return lora_f64(static_cast<const float*>(x), M, K, row_slot, row_apply, static_cast<const float*>(lora_down),
+                    static_cast<const float*>(lora_up_t), n_slots, rank, slot_targets, static_cast<float*>(s_ws), Nq,
+                    Nkv, static_cast<float*>(out), ld_out, st);
+  }
+  if (dtype != ALORA_BF16) return ALORA_EINVAL;
+  GemmLora gl;
+  if (lora) {
+    if (n_slots > 32) return ALORA_EINVAL;
+    // masks live after the shrink output in the caller's workspace
+    auto* sws = static_cast<__nv_bfloat16*>(s_ws);
+    auto* masks = reinterpret_cast<uint32_t*>(sws + align_up(3LL * M * n_slots * rank, 128));
+    rc = lora_tile_masks(row_slot, row_apply, M, masks, st);
+    if (rc != ALORA_OK) return rc;
+    rc = lora_shrink_bf16(static_cast<const __nv_bfloat16*>(x), M, K, row_slot, row_apply,
+                          static_cast<const __nv_bfloat16*>(lora_down), n_slots, rank, slot_targets, sws, st);
+    if (rc != ALORA_OK) return rc;
+    gl.s = sws;
+    gl.up_t = static_cast<const __nv_bfloat16*>(lora_up_t);
+    gl.ks = n_slots * rank;
+    gl.n_q = Nq;
+    gl.n_kv = Nkv;
+    gl.tile_slot_mask = masks;
+    gl.rank = rank;
+  }
+  return gemm_bf16(kEpiStore, static_cast<const __nv_bfloat16*>(x), K, static_cast<const __nv_bfloat16*>(w_qkv_t),
+                   K, out, ld_out, M, N, K, lora ? &gl : nullptr, st);
+}
+
+int alora_kv_write(int32_t dtype, const void* k, const void* v, int64_t ld_src, const int32_t* slot_mapping,
+                   int32_t M, int32_t kv_width, void* kv_pool, int32_t n_layers, int32_t layer, int32_t block_size,
+                   void* stream) {
+  if (dtype != ALORA_F32 && dtype != ALORA_BF16) return ALORA_EINVAL;
+  if (M > 0 && (!k || !v || !slot_mapping || !kv_pool)) return ALORA_EINVAL;
+  return kv_write(dtype, k, v, ld_src, slot_mapping, M, kv_width, kv_pool, n_layers, layer, block_size,
+                  static_cast<cudaStream_t>(stream));
+}
+
+int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t n_rows, int32_t n_seqs,
+                             const int32_t* cu_q, const int32_t* start_pos, const int32_t* block_table,
+                             int32_t max_blocks, int32_t max_q, int32_t max_ctx, const void* kv_pool,
+                             int32_t n_layers, int32_t layer, int32_t block_size, int32_t n_heads,
+                             int32_t n_kv_heads, int32_t head_dim, void* out, int64_t ld_out, void* workspace,
+                             int64_t workspace_bytes, void* stream) {
+  if (n_seqs < 0 || n_rows < 0 || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || head_dim < 1 ||
+      block_size < 1 || layer < 0 || layer >= n_layers || max_blocks < 1)
+    return ALORA_EINVAL;
+  if (n_seqs == 0 || n_rows == 0) return ALORA_OK;
+  if (!q || !cu_q || !start_pos || !block_table || !kv_pool || !out) return ALORA_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (dtype == ALORA_F32)
+    return attn_f64(static_cast<const float*>(q), ld_q, n_rows, n_seqs, cu_q, start_pos, block_table, max_blocks,
+                    static_cast<const float*>(kv_pool), n_layers, layer, block_size, n_heads, n_kv_heads, head_dim,
+                    0.f, static_cast<float*>(out), ld_out, st);
+  if (dtype != ALORA_BF16) return ALORA_EINVAL;
+  const int64_t need = attn_bf16_workspace(n_rows, n_seqs, max_q, max_ctx, n_heads, n_kv_heads, head_dim);
+  if (need > 0 && (workspace == nullptr || workspace_bytes < need)) return ALORA_EINVAL;
+  return attn_bf16(static_cast<const __nv_bfloat16*>(q), ld_q, n_rows, n_seqs, cu_q, start_pos, block_table,
+                   max_blocks, max_q, max_ctx, static_cast<const __nv_bfloat16*>(kv_pool), n_layers, layer,
+                   block_size, n_heads, n_kv_heads, head_dim, static_cast<__nv_bfloat16*>(out), ld_out, workspace,
+                   workspace_bytes, st);
+}
+
+int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs, int32_t max_q, int32_t max_ctx,
+                                   int32_t n_heads, int32_t n_kv_heads, int32_t head_dim) {
+  if (dtype != ALORA_BF16) return 0;
+  return attn_bf16_workspace(n_rows, n_seqs, max_q, max_ctx, n_heads, n_kv_heads, head_dim);
+}
+
+int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream) {
+  if (rows < 0) return ALORA_EINVAL;
+  return argmax_rows(logits, rows, vocab, out_ids, static_cast<cudaStream_t>(stream));
+}
+
+int64_t alora_model_workspace_bytes(const AloraModelDesc* desc) {
+  if (validate(desc) != ALORA_OK) return -1;
+  return plan_ws(*desc).total;
+}
+
+int alora_model_create(const AloraModelDesc* desc, void** out_handle) {
+  int rc = validate(desc);
+  if (rc != ALORA_OK || !out_handle) return ALORA_EINVAL;
+  Model* m = new (std::nothrow) Model();
+  if (!m) return ALORA_ECUDA;
+  m->d = *desc;
+  const int L = desc->n_layers;
+  auto copy_ptrs = [L](const void* const* src, std::vector<const void*>& dst) {
+    dst.assign(L, nullptr);
+    if (src) for (int i = 0; i < L; ++i) dst[i] = src[i];
+  };
+  copy_ptrs(desc->w_qkv_t, m->w_qkv_t);
+  copy_ptrs(desc->w_o_t, m->w_o_t);
+  copy_ptrs(desc->w_in_t, m->w_in_t);
+  copy_ptrs(desc->w_out_t, m->w_out_t);
+  copy_ptrs(desc->lora_down, m->lora_down);
+  copy_ptrs(desc->lora_up_t, m->lora_up_t);
+  m->attn_norm.assign(L, nullptr);
+  m->mlp_norm.assign(L, nullptr);
+  for (int i = 0; i < L; ++i) {
+    if (desc->attn_norm) m->attn_norm[i] = desc->attn_norm[i];
+    if (desc->mlp_norm) m->mlp_norm[i] = desc->mlp_norm[i];
+  }
+  // host arrays are not retained
+  m->d.w_qkv_t = m->d.w_o_t = m->d.w_in_t = m->d.w_out_t = m->d.lora_down = m->d.lora_up_t = nullptr;
+  m->d.attn_norm = m->d.mlp_norm = nullptr;
+  for (int i = 0; i < L; ++i)
+    if (!m->w_qkv_t[i] || !m->w_o_t[i] || !m->w_in_t[i] || !m->w_out_t[i] ||
+        (desc->n_slots > 0 && (!m->lora_down[i] || !m->lora_up_t[i]))) {
+      delete m;
+      return ALORA_EINVAL;
+    }
+  if (!desc->embed || !desc->unembed_t || !desc->kv_pool || !desc->workspace ||
+      desc->workspace_bytes < plan_ws(*desc).total) {
+    delete m;
+    return ALORA_EINVAL;
+  }
+  *out_handle = m;
+  return ALORA_OK;
+}
+
+int alora_model_destroy(void* handle) {
+  delete static_cast<Model*>(handle);
+  return ALORA_OK;
+}
+
+int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream) {
+  if (!handle || !step) return ALORA_EINVAL;
+  Model& m = *static_cast<Model*>(handle);
+  if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
+    return ALORA_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  return m.d.dtype == ALORA_F32 ? forward_f32(m, *step, st) : forward_bf16(m, *step, st);
+}
+
+int32_t alora_model_last_launches(void* handle) {
+  return handle ? static_cast<Model*>(handle)->last_launches : -1;
+}
+
+}  // extern "C"

@@ -1,0 +1,278 @@
+"""Host-side logic of the drop-in, on CPU: native hashing, BlockPool, scheduler, engine.
+
+The engine is driven with the CPU oracle model (tests only) and a host
+storage pool, and must reproduce the reference's own pipeline runs
+(tests/golden/pipelines.json, produced by aloraserve) exactly: generated ids,
+cache hits, first block tables, virtual-clock metrics CSV, step trace, pool
+digests and every sampled logits row.
+"""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden_json, golden_npz
+import oracle as O
+import paper_2512_17910_b200 as P
+from paper_2512_17910_b200 import _native
+
+
+# ------------------------------------------------------------------ C ABI ---
+def test_library_exports_every_header_symbol():
+    hdr = open(os.path.join(ROOT, "include", "alora_sm100a.h")).read()
+    declared = set(re.findall(r"\b(alora_[a-z0-9_]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    assert declared == set(_native.EXPORTS), declared ^ set(_native.EXPORTS)
+    for name in declared:
+        assert hasattr(_native.lib, name)
+    assert "sm_100a" in P.native_version()
+
+
+def test_native_hash_matches_reference_kats_and_chains():
+    g = golden_json("hash_kat.json")
+    for row in g["kats"]:
+        parent = None if row["parent"] is None else bytes.fromhex(row["parent"])
+        assert P.hash_block(parent, row["tokens"], row["key"], row["block_size"]).hex() == row["digest"]
+    for ch in g["chains"]:
+        keys = P.compute_block_keys(ch["tokens"], ch["block_size"], **ch["keys_kw"])
+        assert keys == ch["keys"]
+        n = len(ch["tokens"]) // ch["block_size"]
+        assert [d.hex() for d in P.hash_chain(ch["tokens"], n, ch["block_size"], keys)] == ch["digests"]
+
+
+def test_native_hash_long_keys_and_multiblock_messages():
+    rng = np.random.default_rng(5)
+    for B in (1, 7, 16, 31, 32, 33, 64, 100):  # messages straddling 128-byte compression blocks
+        for key in ("", "k", "x" * 200, "adapter-ü"):
+            toks = rng.integers(0, 2**32, B, dtype=np.uint64).tolist()
+            parent = bytes(rng.integers(0, 256, 16, dtype=np.uint8))
+            for p in (None, parent):
+                assert P.hash_block(p, toks, key, B) == O.hash_block(p, toks, key, B)
+
+
+def test_hash_validation_errors():
+    with pytest.raises(ValueError):
+        P.hash_block(None, [1, 2], "", 3)
+    with pytest.raises(ValueError):
+        P.hash_block(b"short", [1, 2, 3], "", 3)
+    with pytest.raises(ValueError):
+        P.hash_block(None, [2**32], "", 1)
+    with pytest.raises(ValueError):
+        P.compute_block_keys([1, 2], 2, inv_start=1)
+    with pytest.raises(ValueError):
+        P.compute_block_keys([1, 2], 2, adapter_id="a", inv_start=5)
+
+
+def test_block_keys_match_oracle_exhaustively():
+    for B in (1, 2, 3, 4, 16):
+        for n in range(0, 40):
+            seq = list(range(n))
+            assert P.compute_block_keys(seq, B) == O.compute_block_keys(seq, B)
+            assert P.compute_block_keys(seq, B, adapter_id="a") == O.compute_block_keys(seq, B, adapter_id="a")
+            for inv in range(0, n + 1):
+                assert P.compute_block_keys(seq, B, "a", inv) == O.compute_block_keys(seq, B, "a", inv)
+
+
+# -------------------------------------------------------------- BlockPool ---
+def make_pool(total=16, B=4):
+    return P.BlockPool(total, B, n_layers=1, d_model=8, storage="numpy")
+
+
+def commit_seq(pool, rid, tokens, keys=None):
+    B = pool.block_size
+    keys = keys if keys is not None else [""] * (-(-len(tokens) // B))
+    ids, hit = pool.find_cached_prefix(rid, tokens, keys)
+    pool.allocate(rid, -(-len(tokens) // B) - len(ids))
+    pool.set_fill(rid, len(tokens))
+    pool.commit_and_free(rid, tokens, keys)
+    return hit
+
+
+def test_pool_reuse_law_and_last_token_rule():
+    pool = make_pool()
+    toks = list(range(10))
+    assert commit_seq(pool, "a", toks) == 0
+    assert commit_seq(pool, "b", toks) == 8
+    pool2 = make_pool()
+    commit_seq(pool2, "a", list(range(8)))
+    ids, hit = pool2.find_cached_prefix("b", list(range(8)), ["", ""])
+    assert hit == 4 and len(ids) == 1  # aligned prompt: last token always computed
+    pool2.release("b")
+    pool.check_conservation()
+    pool2.check_conservation()
+
+
+def test_pool_lru_eviction_tail_first_and_exhaustion():
+    pool = make_pool(total=4, B=2)
+    commit_seq(pool, "a", [1, 2, 3, 4, 5, 6])  # 3 blocks, released tail first
+    order = list(pool._free)
+    assert order[-1] == 0  # chain head released last = evicted last
+    with pytest.raises(P.PoolExhaustedError):
+        pool.allocate("x", 5)
+    assert pool.num_free == 4  # atomic
+    got = pool.allocate("x", 2)
+    assert 0 not in got
+    pool.release("x")
+    pool.check_conservation()
+
+
+def test_pool_last_writer_wins_and_refcount_pinning():
+    pool = make_pool()
+    commit_seq(pool, "a", list(range(9)))
+    commit_seq(pool, "b", list(range(9)))  # same digests re-committed by b's fresh tail
+    d = P.hash_block(None, [0, 1, 2, 3], "", 4)
+    assert d in pool._index
+    ids1, _ = pool.find_cached_prefix("r1", list(range(9)), ["", "", ""])
+    ids2, _ = pool.find_cached_prefix("r2", list(range(9)), ["", "", ""])
+    assert ids1 == ids2 and pool.blocks[ids1[0]].ref_count == 2
+    pool.release("r1")
+    pool.release("r2")
+    pool.check_conservation()
+
+
+def test_pool_random_walk_conservation():
+    rng = np.random.default_rng(0)
+    pool = make_pool(total=24, B=3)
+    live = {}
+    for step in range(300):
+        if live and rng.random() < 0.5:
+            rid = list(live)[int(rng.integers(len(live)))]
+            toks = live.pop(rid)
+            if rng.random() < 0.5:
+                pool.set_fill(rid, len(toks))
+                pool.commit_and_free(rid, toks, [""] * (-(-len(toks) // 3)))
+            else:
+                pool.release(rid)
+        else:
+            rid = f"r{step}"
+            toks = rng.integers(0, 5, int(rng.integers(1, 12))).tolist()
+            ids, _ = pool.find_cached_prefix(rid, toks, [""] * (-(-len(toks) // 3)))
+            try:
+                pool.allocate(rid, -(-len(toks) // 3) - len(ids))
+                live[rid] = toks
+            except P.PoolExhaustedError:
+                pool.release(rid)
+        pool.check_conservation()
+
+
+# ----------------------------------------------------------------- engine ---
+def detect_cases():
+    assert P.detect_invocation([9, 8, 7, 1, 2, 3], [1, 2, 3]) == 3
+    assert P.detect_invocation([1, 2, 3, 0, 1, 2, 3], [1, 2, 3]) == 4
+    assert P.detect_invocation([4, 5], [4, 5]) == 0
+
+
+def test_detect_invocation():
+    detect_cases()
+    with pytest.raises(P.InvocationNotFoundError):
+        P.detect_invocation([1, 2, 3], [7, 8])
+    with pytest.raises(P.InvocationNotFoundError):
+        P.detect_invocation([1], [1, 2])
+    with pytest.raises(ValueError):
+        P.detect_invocation([1, 2], [])
+    rng = np.random.default_rng(1)
+    for _ in range(200):
+        p = rng.integers(0, 3, int(rng.integers(1, 20)))
+        inv = rng.integers(0, 3, int(rng.integers(1, 4)))
+        try:
+            want = O.detect_invocation(p, inv)
+        except ValueError:
+            with pytest.raises(P.InvocationNotFoundError):
+                P.detect_invocation(p, inv)
+            continue
+        assert P.detect_invocation(p, inv) == want
+
+
+def oracle_engine(dims, spec, block_size, token_budget, pool_blocks):
+    model = O.OracleModel(O.OracleConfig(**dims))
+    return P.build_engine(spec, model=P.ModelConfig(**dims), pool_blocks=pool_blocks, block_size=block_size,
+                          token_budget=token_budget, engine_model=model, pool_storage="numpy")
+
+
+def _run_golden(name):
+    g = golden_json("pipelines.json")[name]
+    logits = golden_npz("pipeline_logits.npz")[name]
+    spec = P.PipelineSpec(**g["spec"])
+    eng = oracle_engine(g["model"], spec, **g["engine"])
+    sink = {}
+    eng.on_logits = lambda rid, pos, row: sink.__setitem__(f"{rid}@{pos}", np.array(row, copy=True))
+    tables = {}
+    orig = eng.scheduler._cache_lookup
+
+    def spy(req):
+        orig(req)
+        bt = eng.pool.block_table(req.request_id)
+        tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
+
+    eng.scheduler._cache_lookup = spy
+    rows = P.run_sync_pipeline(spec, eng)
+    return g, logits, eng, rows, sink, tables
+
+
+@pytest.mark.parametrize("name", ["d64_multi_alora", "d64_adapter_base_alora", "d64_ba_lora", "d64_bab_alora_b8",
+                                  "c1_bab_alora"])
+def test_engine_reproduces_reference_pipeline(name):
+    g, logits, eng, rows, sink, tables = _run_golden(name)
+    for rid, r in g["requests"].items():
+        mine = eng.finished[rid]
+        assert mine.prompt.tolist() == r["prompt"], rid
+        assert list(map(int, mine.generated)) == r["generated"], rid
+        assert (mine.hit_tokens, mine.computed_tokens) == (r["hit_tokens"], r["computed_tokens"]), rid
+    assert tables == g["first_tables"]
+    assert P.render_csv(rows) == g["metrics_csv"]
+    assert eng.trace == g["trace"]
+    assert eng.pool.dump_state() == g["pool_dump"]
+    assert sorted(sink) == g["logit_keys"]
+    np.testing.assert_array_equal(np.stack([sink[k] for k in sorted(sink)]), logits)
+
+
+def test_submit_validation():
+    spec = P.PipelineSpec()
+    eng = oracle_engine({}, spec, 4, 64, 128)
+    with pytest.raises(ValueError):
+        eng.submit(np.zeros(0, dtype=np.int64))
+    with pytest.raises(ValueError):
+        eng.submit(np.zeros((2, 3), dtype=np.int64))
+    with pytest.raises(ValueError):
+        eng.submit([1, 2], max_new_tokens=0)
+    with pytest.raises(ValueError):
+        eng.submit([1, 256])
+    with pytest.raises(ValueError):
+        eng.submit([1] * 100, max_new_tokens=8093)
+    with pytest.raises(ValueError):
+        eng.submit([1, 2], adapter_id="nope")
+    with pytest.raises(P.InvocationNotFoundError):
+        eng.submit([1, 2, 3], adapter_id="adapter0")
+    small = oracle_engine({}, spec, 4, 64, 2)
+    with pytest.raises(ValueError, match="cannot ever fit"):
+        small.submit([1] * 12, max_new_tokens=1)
+
+
+def test_activation_mask_layout():
+    spec = P.PipelineSpec()
+    eng = oracle_engine({}, spec, 4, 64, 128)
+    inv = list(eng.adapters["adapter0"].invocation_tokens)
+    eng.submit(np.asarray([5, 6] + inv), adapter_id="adapter0", max_new_tokens=1, request_id="a")
+    eng.submit(np.asarray([9, 9, 9]), max_new_tokens=1, request_id="b")
+    eng.scheduler._drain_intake()
+    ra, rb = list(eng.scheduler.waiting)
+    mask = P.build_activation_mask([P.ScheduledSpan(ra, 0, 5, "prefill"), P.ScheduledSpan(rb, 1, 3, "prefill")])
+    assert mask.values.tolist() == [True, True, False, False, False, True, True]
+    assert mask.slices == {"a": slice(0, 5), "b": slice(5, 7)}
+    assert mask.inv_start["b"] == rb.total_tokens
+    assert P.build_activation_mask([ ]).values.shape == (0,)
+
+
+def test_engine_config_json(tmp_path):
+    import json
+    p = tmp_path / "e.json"
+    p.write_text(json.dumps({"model": {"n_layers": 1, "seed": 3}, "scheduler": {"token_budget": 32},
+                             "pool_blocks": 64, "block_size": 8,
+                             "adapters": [{"adapter_id": "x", "rank": 4, "seed": 0, "invocation_tokens": [250]}]}))
+    cfg = P.load_engine_config(p)
+    assert cfg.model.n_layers == 1 and cfg.scheduler.token_budget == 32 and cfg.block_size == 8
+    p.write_text(json.dumps({"pool_block": 3}))
+    with pytest.raises(ValueError, match="unknown engine config keys"):
+        P.load_engine_config(p)
