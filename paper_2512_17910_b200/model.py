@@ -309,6 +309,10 @@ class Model:
             return self._handle
         self.close()
         self._keep = []
+        need = _native.lib.alora_model_workspace_bytes(ctypes.byref(self._desc(kv=None, probe=True)))
+        if need > self._ws.numel():  # the adapter bank grew: the LoRA workspace grows with it
+            self._ws = self._torch.empty(int(need), dtype=self._torch.uint8, device="cuda")
+            key = (kv.data_ptr(), tuple(kv.shape), self._ws.data_ptr(), self._bank_version)
         desc = self._desc(kv)
         h = ctypes.c_void_p()
         _native.check(_native.lib.alora_model_create(ctypes.byref(desc), ctypes.byref(h)), "alora_model_create")
