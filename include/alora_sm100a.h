@@ -110,6 +110,13 @@ int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs
                                    int32_t max_ctx, int32_t n_heads, int32_t n_kv_heads,
                                    int32_t head_dim);
 
+/* Dense bf16 GEMM on tcgen05 (the engine behind alora_qkv_proj and the O/MLP/lm_head
+ * projections of alora_model_forward): C = epi(A[M,K] . Bt[N,K]^T), fp32 accumulate.
+ * epi: 0 store bf16, 1 C(fp32) += acc, 2 relu -> bf16, 3 SwiGLU of 64-interleaved
+ * gate|up column blocks -> bf16 [M, N/2], 16 store fp32. */
+int alora_gemm_bf16(int32_t epi, const void* A, int32_t lda, const void* Bt, int32_t ldb, void* C,
+                    int32_t ldc, int32_t M, int32_t N, int32_t K, void* stream);
+
 /* Greedy next token per row of logits [rows, V] fp32: argmax, ties -> lowest id (model.py:190-195). */
 int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream);
 

@@ -2,8 +2,6 @@
 #include "common.cuh"
 #include "kernels.h"
 namespace alora {
-int gemm_bf16(int, const __nv_bfloat16*, int, const __nv_bfloat16*, int, void*, int, int, int, int, const GemmLora*,
-              cudaStream_t) { return ALORA_EUNSUPPORTED; }
 int attn_bf16(const __nv_bfloat16*, int64_t, int, int, const int32_t*, const int32_t*, const int32_t*, int, int, int,
               const __nv_bfloat16*, int, int, int, int, int, int, __nv_bfloat16*, int64_t, void*, int64_t,
               cudaStream_t) { return ALORA_EUNSUPPORTED; }

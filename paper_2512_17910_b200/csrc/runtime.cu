@@ -292,6 +292,14 @@ int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs
   return attn_bf16_workspace(n_rows, n_seqs, max_q, max_ctx, n_heads, n_kv_heads, head_dim);
 }
 
+int alora_gemm_bf16(int32_t epi, const void* A, int32_t lda, const void* Bt, int32_t ldb, void* C, int32_t ldc,
+                    int32_t M, int32_t N, int32_t K, void* stream) {
+  if (!A || !Bt || !C) return ALORA_EINVAL;
+  if (epi != kEpiStore && epi != kEpiAdd && epi != kEpiRelu && epi != kEpiSwiglu && epi != 16) return ALORA_EINVAL;
+  return gemm_bf16(epi, static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(Bt), ldb, C,
+                   ldc, M, N, K, nullptr, static_cast<cudaStream_t>(stream));
+}
+
 int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream) {
   if (rows < 0) return ALORA_EINVAL;
   return argmax_rows(logits, rows, vocab, out_ids, static_cast<cudaStream_t>(stream));
