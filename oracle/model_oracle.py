@@ -131,16 +131,18 @@ def oracle_weights(cfg: OracleConfig) -> dict:
                 "w_up": _init(cfg.seed, f"l{li}.w_up", (d, cfg.ffn), s_d),
                 "w_down": _init(cfg.seed, f"l{li}.w_down", (cfg.ffn, d), s_f),
             })
-        w["embed"] = _init(cfg.seed, "embed", (cfg.vocab_size, d), 1.0)
+        w["embed"] = _init(cfg.seed, "embed", (cfg.vocab_size, d), s_d)  # tied lm_head: unit-scale logits
         w["final_norm"] = 1.0 + _init(cfg.seed, "final_norm", (d,))
         w["unembed"] = None  # tied: logits = h @ embed.T
     else:
         raise ValueError(f"unknown arch {cfg.arch!r}")
     if cfg.numerics == "bf16":
+        # GEMM operands are bf16 on the GPU; RMSNorm gains stay fp32 there, so they do here
         for layer in w["layers"]:
             for k in layer:
-                layer[k] = bf16_round(layer[k])
-        for k in ("embed", "unembed", "final_norm"):
+                if not k.endswith("_norm"):
+                    layer[k] = bf16_round(layer[k])
+        for k in ("embed", "unembed"):
             if w.get(k) is not None:
                 w[k] = bf16_round(w[k])
     return w

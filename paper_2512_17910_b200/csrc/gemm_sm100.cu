@@ -42,6 +42,10 @@ struct GemmArgs {
   int rank;
   int n_q, n_kv;  // q | k | v column ranges
   const uint32_t* tile_slot_mask;
+  const int32_t* positions;  // kEpiRope
+  const float* rope_cos;
+  const float* rope_sin;
+  int rope_cols, head_dim;
 };
 
 template <int BN>
@@ -166,7 +170,44 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int epi = args.epi & 15;
     const bool out_f32 = (args.epi & 16) != 0;
     const bool live = row < args.M;
-    if (epi == kEpiSwiglu) {
+    if (epi == kEpiRope && n0 < args.rope_cols) {
+      // q/k heads: x1 = cols [i*32, +32), x2 = cols [half + i*32, +32) of each head; fp32 rotate, one bf16 rounding
+      const int D = args.head_dim, half = D / 2;
+      const int pos = live ? args.positions[row] : 0;
+      const float* cs = args.rope_cos + (int64_t)pos * half;
+      const float* sn = args.rope_sin + (int64_t)pos * half;
+      for (int hb = 0; hb < BN; hb += D) {
+        for (int i = 0; i < half / 32; ++i) {
+          uint32_t x1[32], x2[32];
+          sm100::tmem_ld_32x32b_x32(trow + hb + i * 32, x1);
+          sm100::tmem_ld_32x32b_x32(trow + hb + half + i * 32, x2);
+          sm100::tmem_ld_wait();
+          if (!live) continue;
+          __nv_bfloat16* d1 = static_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc + n0 + hb + i * 32;
+          __nv_bfloat16* d2 = d1 + half;
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            __align__(16) __nv_bfloat162 o1[4], o2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float r1[2], r2[2];
+#pragma unroll
+              for (int q = 0; q < 2; ++q) {
+                const int j = v * 8 + e * 2 + q;
+                const float c = __ldg(cs + i * 32 + j), s = __ldg(sn + i * 32 + j);
+                const float a = __uint_as_float(x1[j]), b = __uint_as_float(x2[j]);
+                r1[q] = a * c - b * s;
+                r2[q] = b * c + a * s;
+              }
+              o1[e] = __floats2bfloat162_rn(r1[0], r1[1]);
+              o2[e] = __floats2bfloat162_rn(r2[0], r2[1]);
+            }
+            *reinterpret_cast<int4*>(d1 + v * 8) = *reinterpret_cast<int4*>(o1);
+            *reinterpret_cast<int4*>(d2 + v * 8) = *reinterpret_cast<int4*>(o2);
+          }
+        }
+      }
+    } else if (epi == kEpiSwiglu) {
       // tile columns [0,64) gate, [64,128) up -> 64 outputs at column n0/2
       for (int c = 0; c < BN / 128; ++c) {
         for (int h = 0; h < 2; ++h) {
@@ -268,7 +309,17 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (N % 64 != 0) return ALORA_EINVAL;
   if (base_epi == kEpiSwiglu && N % 128 != 0) return ALORA_EINVAL;
   if (base_epi == kEpiSwiglu) BN = 128;
-  GemmArgs args{Cout, ldc, M, N, K, epi, 0, 1, 0, 0, nullptr};
+  GemmArgs args{Cout, ldc, M, N, K, epi, 0, 1, 0, 0, nullptr, nullptr, nullptr, nullptr, 0, 0};
+  if (base_epi == kEpiRope) {
+    if (!lora || !lora->positions || !lora->rope_cos || !lora->rope_sin || lora->head_dim < 64 ||
+        lora->head_dim % 64 || lora->rope_cols % BN || BN % lora->head_dim)
+      return ALORA_EINVAL;
+    args.positions = lora->positions;
+    args.rope_cos = lora->rope_cos;
+    args.rope_sin = lora->rope_sin;
+    args.rope_cols = lora->rope_cols;
+    args.head_dim = lora->head_dim;
+  }
   CUtensorMap ta, tb, ts, tu;
   if (!make_tmap_2d(&ta, A, M, K, lda, kBM, kBK)) return ALORA_ECUDA;
   if (!make_tmap_2d(&tb, Bt, N, K, ldb, BN, kBK)) return ALORA_ECUDA;

@@ -7,7 +7,7 @@
 
 namespace alora {
 
-enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3 };
+enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3, kEpiRope = 4 };
 
 // ---- fp32 storage / fp64 accumulation (parity tier), parity_f64.cu
 int embed_f32(const int32_t* tokens, const int32_t* positions, const float* embed, const float* pos_table, int M,
@@ -47,6 +47,7 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
               const __nv_bfloat16* kv, int n_layers, int layer, int B, int H, int Hkv, int D,
               __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes, cudaStream_t st);
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D);
+int64_t attn_bf16_workspace_bound(int H, int D);
 
 // tcgen05 GEMM: C = epi(A[M,K] @ Bt[N,K]^T (+ S_t[M,Ks] @ Ut[N,Ks]^T lora part)), bf16 in, fp32 accumulate.
 struct GemmLora {
@@ -56,6 +57,12 @@ struct GemmLora {
   int n_q = 0, n_kv = 0;               // column ranges of the q|k|v targets
   const uint32_t* tile_slot_mask = nullptr;  // [ceil(M/128)] bitmask of slots present (taking the delta)
   int rank = 0;
+  // kEpiRope: rotate-half RoPE in fp32 on the accumulator of columns < rope_cols (q and k heads), one rounding
+  const int32_t* positions = nullptr;
+  const float* rope_cos = nullptr;  // [max_seq_len, head_dim/2]
+  const float* rope_sin = nullptr;
+  int rope_cols = 0;
+  int head_dim = 0;
 };
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* C, int ldc,
               int M, int N, int K, const GemmLora* lora, cudaStream_t st);

@@ -51,8 +51,7 @@ Ws plan_ws(const AloraModelDesc& d) {
   w.masks = take((T / 128 + 2) * 4);
   w.hf = take(S * d.d_model * e);
   w.attn_ws_bytes = d.dtype == ALORA_BF16
-                        ? attn_bf16_workspace(d.max_tokens, d.max_seqs, d.max_tokens, d.max_seq_len, d.n_heads,
-                                              d.n_kv_heads, d.head_dim)
+                        ? attn_bf16_workspace_bound(d.n_heads, d.head_dim)
                         : 0;
   w.attn_ws = take(w.attn_ws_bytes);
   w.total = off;
@@ -176,9 +175,15 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       gl.tile_slot_mask = masks;
       gl.rank = d.lora_rank;
     }
-    RUN(gemm_bf16(kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv, Nqkv, M, Nqkv, dm,
-                  lora ? &gl : nullptr, st));
-    if (llama) RUN(rope_bf16(qkv, Nqkv, s.positions, M, H, Hkv, D, d.rope_cos, d.rope_sin, st));
+    if (llama) {  // RoPE fused into the QKV epilogue: fp32 rotate of the accumulator, one bf16 rounding
+      gl.positions = s.positions;
+      gl.rope_cos = d.rope_cos;
+      gl.rope_sin = d.rope_sin;
+      gl.rope_cols = Nq + Nkv;
+      gl.head_dim = D;
+    }
+    RUN(gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
+                  Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st));
     RUN(kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                  d.block_size, st));
     RUN(attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,

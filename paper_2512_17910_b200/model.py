@@ -176,7 +176,7 @@ class Model:
                 return (t.rand(shape, generator=g, device="cuda", dtype=t.float32) * 2 - 1).mul_(bound).to(self._tdt)
 
             nqkv = cfg.q_width + 2 * cfg.kv_width
-            self.embed = rnd((cfg.vocab_size, d), 1.0 if cfg.arch == "llama" else 0.1)
+            self.embed = rnd((cfg.vocab_size, d), float(np.sqrt(3.0 / d)) if cfg.arch == "llama" else 0.1)
             self.unembed_t = self.embed if cfg.arch == "llama" else rnd((cfg.vocab_size, d), 0.1)
             self.final_norm = (1 + 0.1 * (2 * t.rand(d, generator=g, device="cuda") - 1)) if cfg.arch == "llama" else None
             b_d, b_q, b_f = (np.sqrt(3.0 / d), np.sqrt(3.0 / cfg.q_width), np.sqrt(3.0 / cfg.ffn)) \

@@ -65,7 +65,7 @@ def generate_weights(config) -> BaseWeights:
             w_in=_uniform(c.seed, f"l{li}.w_gate", (d, c.ffn), b_d),
             w_up=_uniform(c.seed, f"l{li}.w_up", (d, c.ffn), b_d),
             w_out=_uniform(c.seed, f"l{li}.w_down", (c.ffn, d), b_f)))
-    return BaseWeights(embed=_uniform(c.seed, "embed", (c.vocab_size, d), 1.0), layers=layers, unembed=None,
+    return BaseWeights(embed=_uniform(c.seed, "embed", (c.vocab_size, d), b_d), layers=layers, unembed=None,
                        final_norm=1.0 + _uniform(c.seed, "final_norm", (d,), 0.1))
 
 
