@@ -170,6 +170,9 @@ typedef struct AloraStepDesc {
   const int32_t* last_row;      /* [S] row whose logits are produced */
   float* logits;                /* [S, V] fp32 out */
   int32_t* next_ids;            /* [S] argmax out */
+  /* host-side shape summary, used only for the profiler's algorithmic bytes/flops */
+  double attn_kv_tokens;        /* sum over spans of (start_pos + n) */
+  double attn_qk_pairs;         /* sum over spans of n * (start_pos + (n + 1) / 2) */
 } AloraStepDesc;
 
 int64_t alora_model_workspace_bytes(const AloraModelDesc* desc);
@@ -180,6 +183,15 @@ int alora_model_destroy(void* handle);
 int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream);
 /* Count of kernel launches issued by the last alora_model_forward. */
 int32_t alora_model_last_launches(void* handle);
+
+/* Per-kernel profiling with CUDA events on the launch stream: while enabled,
+ * every launch of alora_model_forward is bracketed by events and tagged with
+ * its algorithmic bytes and flops. profile_read (after a stream sync)
+ * aggregates by kernel kind: names (max_kinds x 32 chars), total ms, launch
+ * counts, bytes and flops; returns the number of kinds. */
+int alora_model_set_profiling(void* handle, int32_t enable);
+int alora_model_profile_read(void* handle, int32_t max_kinds, char* names, float* ms, int32_t* counts,
+                             double* bytes, double* flops);
 
 #ifdef __cplusplus
 }

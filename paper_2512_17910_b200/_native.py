@@ -62,6 +62,7 @@ class AloraStepDesc(ctypes.Structure):
         ("tokens", c_void_p), ("positions", c_void_p), ("slot_mapping", c_void_p), ("row_slot", c_void_p),
         ("row_apply", c_void_p), ("cu_q", c_void_p), ("start_pos", c_void_p), ("block_table", c_void_p),
         ("last_row", c_void_p), ("logits", c_void_p), ("next_ids", c_void_p),
+        ("attn_kv_tokens", ctypes.c_double), ("attn_qk_pairs", ctypes.c_double),
     ]
 
 
@@ -97,6 +98,9 @@ EXPORTS = {
     "alora_model_destroy": _sig("alora_model_destroy", c_i32, c_void_p),
     "alora_model_forward": _sig("alora_model_forward", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc), c_void_p),
     "alora_model_last_launches": _sig("alora_model_last_launches", c_i32, c_void_p),
+    "alora_model_set_profiling": _sig("alora_model_set_profiling", c_i32, c_void_p, c_i32),
+    "alora_model_profile_read": _sig("alora_model_profile_read", c_i32, c_void_p, c_i32, c_void_p, c_void_p,
+                                     c_void_p, c_void_p, c_void_p),
 }
 
 

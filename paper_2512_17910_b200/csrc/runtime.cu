@@ -17,11 +17,57 @@ using namespace alora;
 
 namespace {
 
+// Event-bracketed launch records (alora_model_set_profiling).
+struct ProfRec {
+  const char* kind;
+  int ev0, ev1;
+  double bytes, flops;
+};
+
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> events;
+  int used = 0;
+  std::vector<ProfRec> recs;
+  int event(cudaStream_t st) {
+    if (used == (int)events.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return -1;
+      events.push_back(e);
+    }
+    cudaEventRecord(events[used], st);
+    return used++;
+  }
+  ~Profiler() {
+    for (auto e : events) cudaEventDestroy(e);
+  }
+};
+
 struct Model {
   AloraModelDesc d;
   std::vector<const void*> w_qkv_t, w_o_t, w_in_t, w_out_t, lora_down, lora_up_t;
   std::vector<const float*> attn_norm, mlp_norm;
   int32_t last_launches = 0;
+  Profiler prof;
+};
+
+// Runs one launcher; counts it and, when profiling, brackets it with events and tags its algorithmic cost.
+struct Launcher {
+  Model& m;
+  cudaStream_t st;
+  int n = 0;
+  template <typename F>
+  int operator()(const char* kind, double bytes, double flops, F&& fn) {
+    int e0 = m.prof.on ? m.prof.event(st) : -1;
+    const int rc = fn();
+    if (rc != ALORA_OK) return rc;
+    ++n;
+    if (m.prof.on) {
+      const int e1 = m.prof.event(st);
+      if (e0 >= 0 && e1 >= 0) m.prof.recs.push_back({kind, e0, e1, bytes, flops});
+    }
+    return ALORA_OK;
+  }
 };
 
 inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
@@ -150,22 +196,28 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
   const bool llama = d.arch == ALORA_ARCH_LLAMA;
   const bool lora = d.n_slots > 0;
-  int n = 0;
+  Launcher run{mdl, st};
   int rc;
-#define RUN(call)                      \
-  do {                                 \
-    rc = (call);                       \
-    if (rc != ALORA_OK) return rc;     \
-    ++n;                               \
+  const double m_ = M, dm_ = dm, F_ = F, Nqkv_ = Nqkv, Nq_ = Nq, V_ = d.vocab, S_ = S, ks_ = (double)d.n_slots * d.lora_rank;
+  // algorithmic bytes of a bf16 GEMM: A + B read once, C written (and read for +=)
+  auto gemm_bytes = [](double m, double n, double k, double out_b, bool rmw) {
+    return 2.0 * (m * k + n * k) + m * n * out_b * (rmw ? 2.0 : 1.0);
+  };
+#define RUN(kind, bytes, flops, call)                                           \
+  do {                                                                          \
+    rc = run(kind, bytes, flops, [&]() { return (call); });                     \
+    if (rc != ALORA_OK) return rc;                                              \
   } while (0)
-  RUN(embed_bf16(s.tokens, s.positions, static_cast<const __nv_bfloat16*>(d.embed), llama ? nullptr : d.pos_table,
-                 M, dm, x, st));
-  if (lora) RUN(lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
+  RUN("embed", m_ * dm_ * 6, 0, embed_bf16(s.tokens, s.positions, static_cast<const __nv_bfloat16*>(d.embed),
+                                           llama ? nullptr : d.pos_table, M, dm, x, st));
+  if (lora) RUN("lora_masks", m_ * 5, 0, lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
   for (int l = 0; l < d.n_layers; ++l) {
-    RUN(rmsnorm_bf16(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     GemmLora gl;
     if (lora) {
-      RUN(lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
+      RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * d.n_slots * d.lora_rank * dm_ * 2 + 3.0 * m_ * ks_ * 2,
+          2.0 * 3 * m_ * d.lora_rank * dm_,
+          lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
                            d.n_slots, d.lora_rank, d.slot_targets, sws, st));
       gl.s = sws;
       gl.up_t = static_cast<const __nv_bfloat16*>(mdl.lora_up_t[l]);
@@ -182,27 +234,35 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       gl.rope_cols = Nq + Nkv;
       gl.head_dim = D;
     }
-    RUN(gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
+    RUN("gemm_qkv", gemm_bytes(m_, Nqkv_, dm_, 2, false) + (lora ? 2.0 * Nqkv_ * ks_ : 0.0), 2.0 * m_ * Nqkv_ * dm_,
+        gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
                   Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st));
-    RUN(kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
+    RUN("kv_write", 2.0 * 2 * m_ * Nkv * 2, 0,
+        kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                  d.block_size, st));
-    RUN(attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
+    RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
+        attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
                   static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
                   aws, w.attn_ws_bytes, st));
-    RUN(gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq,
-                  nullptr, st));
-    RUN(rmsnorm_bf16(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
-    RUN(gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act,
-                  F, M, llama ? 2 * F : F, dm, nullptr, st));
-    RUN(gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
+    RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
+        gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq, nullptr,
+                  st));
+    RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    const double n_in = llama ? 2 * F_ : F_;
+    RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2, 2.0 * m_ * n_in * dm_,
+        gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act, F,
+                  M, llama ? 2 * F : F, dm, nullptr, st));
+    RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true), 2.0 * m_ * dm_ * F_,
+        gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
                   st));
   }
-  RUN(rmsnorm_bf16(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
-  RUN(gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm,
-                s.logits, d.vocab, S, d.vocab, dm, nullptr, st));
-  RUN(argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
+  RUN("rmsnorm", S_ * dm_ * 6, 0, rmsnorm_bf16(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
+  RUN("gemm_lm_head", gemm_bytes(S_, V_, dm_, 4, false), 2.0 * S_ * V_ * dm_,
+      gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm, s.logits,
+                d.vocab, S, d.vocab, dm, nullptr, st));
+  RUN("argmax", S_ * V_ * 4, 0, argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
 #undef RUN
-  mdl.last_launches = n;
+  mdl.last_launches = run.n;
   return ALORA_OK;
 }
 
@@ -372,6 +432,42 @@ int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream) {
 
 int32_t alora_model_last_launches(void* handle) {
   return handle ? static_cast<Model*>(handle)->last_launches : -1;
+}
+
+int alora_model_set_profiling(void* handle, int32_t enable) {
+  if (!handle) return ALORA_EINVAL;
+  Profiler& p = static_cast<Model*>(handle)->prof;
+  p.on = enable != 0;
+  p.recs.clear();
+  p.used = 0;
+  return ALORA_OK;
+}
+
+int alora_model_profile_read(void* handle, int32_t max_kinds, char* names, float* ms, int32_t* counts,
+                             double* bytes, double* flops) {
+  if (!handle || max_kinds < 1 || !names || !ms || !counts || !bytes || !flops) return ALORA_EINVAL;
+  Profiler& p = static_cast<Model*>(handle)->prof;
+  std::vector<const char*> kinds;
+  for (const ProfRec& r : p.recs) {
+    int k = 0;
+    while (k < (int)kinds.size() && std::strcmp(kinds[k], r.kind) != 0) ++k;
+    if (k == (int)kinds.size()) {
+      if (k == max_kinds) continue;
+      kinds.push_back(r.kind);
+      std::strncpy(names + 32 * k, r.kind, 31);
+      names[32 * k + 31] = 0;
+      ms[k] = 0.f;
+      counts[k] = 0;
+      bytes[k] = flops[k] = 0.0;
+    }
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, p.events[r.ev0], p.events[r.ev1]) != cudaSuccess) return ALORA_ECUDA;
+    ms[k] += t;
+    counts[k] += 1;
+    bytes[k] += r.bytes;
+    flops[k] += r.flops;
+  }
+  return (int)kinds.size();
 }
 
 }  // extern "C"

@@ -317,6 +317,8 @@ class Model:
         h = ctypes.c_void_p()
         _native.check(_native.lib.alora_model_create(ctypes.byref(desc), ctypes.byref(h)), "alora_model_create")
         self._handle, self._handle_key = h, key
+        if getattr(self, "_profiling", False):
+            _native.lib.alora_model_set_profiling(h, 1)
         return h
 
     def close(self):
@@ -390,6 +392,8 @@ class Model:
             p = positions[cu[i]:cu[i + 1]]
             slot_map[cu[i]:cu[i + 1]] = tb[p // block_size] * block_size + p % block_size
         return {
+            "attn_kv_tokens": float(sum(s + n for s, n in zip(starts, lens))),
+            "attn_qk_pairs": float(sum(n * (s + (n + 1) / 2) for s, n in zip(starts, lens))),
             "M": M, "S": S, "maxb": maxb, "max_q": int(max(lens)),
             "max_ctx": int(max(s + n for s, n in zip(starts, lens))),
             "tokens": np.concatenate(toks).astype(np.int32), "positions": positions, "slot_mapping": slot_map,
@@ -402,6 +406,25 @@ class Model:
 
     def run_packed(self, p: dict, kv, want_logits: bool = True):
         """One native forward over a packed step. Returns (next_ids[S], logits[S, V] or None) on the host."""
+        t = self._torch
+        st = self.stage(p, kv)
+        self.launch(st)
+        S = p["S"]
+        self._ids_host[:S].copy_(self._ids[:S], non_blocking=True)
+        logits = self._logits[:S].cpu().numpy() if want_logits else None
+        t.cuda.current_stream().synchronize()
+        self.last_d2h_bytes = 4 * S + (logits.nbytes if logits is not None else 0)
+        return self._ids_host[:S].numpy().copy(), logits
+
+    def launch(self, st) -> None:
+        """Enqueue one staged step (alora_model_forward) on the current stream; no host sync."""
+        stream = self._torch.cuda.current_stream().cuda_stream
+        _native.check(_native.lib.alora_model_forward(self._handle, ctypes.byref(st), ctypes.c_void_p(stream)),
+                      "alora_model_forward")
+        self.last_launches = _native.lib.alora_model_last_launches(self._handle)
+
+    def stage(self, p: dict, kv):
+        """Upload a packed step's metadata (one pinned H2D copy on the current stream); returns its descriptor."""
         t = self._torch
         self._check_pool(kv)
         self._grow_workspace(p["M"])
@@ -427,15 +450,35 @@ class Model:
         st.last_row, st.block_table = ptr["last_row"], ptr["block_table"]
         st.row_apply = base + 4 * int(offs[len(self._FIELDS)])
         st.logits, st.next_ids = self._logits.data_ptr(), self._ids.data_ptr()
-        stream = t.cuda.current_stream().cuda_stream
-        _native.check(_native.lib.alora_model_forward(handle, ctypes.byref(st), ctypes.c_void_p(stream)),
-                      "alora_model_forward")
-        self.last_launches = _native.lib.alora_model_last_launches(handle)
-        S = p["S"]
-        self._ids_host[:S].copy_(self._ids[:S], non_blocking=True)
-        logits = self._logits[:S].cpu().numpy() if want_logits else None
-        t.cuda.current_stream().synchronize()
-        return self._ids_host[:S].numpy().copy(), logits
+        st.attn_kv_tokens, st.attn_qk_pairs = p.get("attn_kv_tokens", 0.0), p.get("attn_qk_pairs", 0.0)
+        self.last_h2d_bytes = 4 * total
+        return st
+
+    def set_profiling(self, enable: bool, kv=None) -> None:
+        """CUDA-event bracketing of every native launch (per-kernel time + algorithmic bytes/flops)."""
+        self._profiling = bool(enable)
+        if self._handle is not None:
+            _native.check(_native.lib.alora_model_set_profiling(self._handle, int(enable)), "set_profiling")
+
+    def profile_read(self) -> dict:
+        """{kind: {"ms", "launches", "bytes", "flops"}} accumulated since set_profiling(True); syncs the stream."""
+        if self._handle is None:
+            return {}
+        self._torch.cuda.current_stream().synchronize()
+        k = 32
+        names = ctypes.create_string_buffer(32 * k)
+        ms = (ctypes.c_float * k)()
+        cnt = (ctypes.c_int32 * k)()
+        by = (ctypes.c_double * k)()
+        fl = (ctypes.c_double * k)()
+        n = _native.lib.alora_model_profile_read(self._handle, k, names, ms, cnt, by, fl)
+        if n < 0:
+            _native.check(n, "profile_read")
+        out = {}
+        for i in range(n):
+            name = names.raw[32 * i:32 * i + 32].split(b"\0")[0].decode()
+            out[name] = {"ms": float(ms[i]), "launches": int(cnt[i]), "bytes": float(by[i]), "flops": float(fl[i])}
+        return out
 
     def forward_step(self, seqs, kv) -> dict:
         """Run every span of a step; returns {request_id: float32[V] logits of the span's last row}."""
