@@ -100,12 +100,13 @@ int alora_kv_write(int32_t dtype, const void* k, const void* v, int64_t ld_src,
 int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t n_rows,
                              int32_t n_seqs, const int32_t* cu_q, const int32_t* start_pos,
                              const int32_t* block_table, int32_t max_blocks, int32_t max_q,
-                             int32_t max_ctx, const void* kv_pool, int32_t n_layers, int32_t layer,
-                             int32_t block_size, int32_t n_heads, int32_t n_kv_heads,
-                             int32_t head_dim, void* out, int64_t ld_out, void* workspace,
-                             int64_t workspace_bytes, void* stream);
+                             int32_t max_ctx, const void* kv_pool, int32_t total_blocks,
+                             int32_t n_layers, int32_t layer, int32_t block_size, int32_t n_heads,
+                             int32_t n_kv_heads, int32_t head_dim, void* out, int64_t ld_out,
+                             void* workspace, int64_t workspace_bytes, void* stream);
 
-/* Device workspace alora_paged_prefill_attn needs (bf16 split-KV partials; 0 for fp32). */
+/* Device workspace alora_paged_prefill_attn needs (bf16 split-KV partials + merge counters at
+ * the end of the buffer; 0 for fp32). Zero-fill it once: the counters reset themselves. */
 int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs, int32_t max_q,
                                    int32_t max_ctx, int32_t n_heads, int32_t n_kv_heads,
                                    int32_t head_dim);
@@ -113,9 +114,15 @@ int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs
 /* Dense bf16 GEMM on tcgen05 (the engine behind alora_qkv_proj and the O/MLP/lm_head
  * projections of alora_model_forward): C = epi(A[M,K] . Bt[N,K]^T), fp32 accumulate.
  * epi: 0 store bf16, 1 C(fp32) += acc, 2 relu -> bf16, 3 SwiGLU of 64-interleaved
- * gate|up column blocks -> bf16 [M, N/2], 16 store fp32. */
+ * gate|up column blocks -> bf16 [M, N/2], 16 store fp32.
+ * workspace (optional; zero-filled once, >= alora_gemm_workspace_bytes()) enables split-K
+ * when the output tiles cannot fill the 148 SMs: the splits of a tile are co-resident
+ * (cooperative launch), publish fp32 partials to L2 and each reduces a slice of rows in
+ * split order (deterministic for a given split count). */
 int alora_gemm_bf16(int32_t epi, const void* A, int32_t lda, const void* Bt, int32_t ldb, void* C,
-                    int32_t ldc, int32_t M, int32_t N, int32_t K, void* stream);
+                    int32_t ldc, int32_t M, int32_t N, int32_t K, void* workspace,
+                    int64_t workspace_bytes, void* stream);
+int64_t alora_gemm_workspace_bytes(void);
 
 /* Greedy next token per row of logits [rows, V] fp32: argmax, ties -> lowest id (model.py:190-195). */
 int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream);

@@ -86,11 +86,12 @@ EXPORTS = {
                            c_void_p, c_i32, c_i32, c_i32, c_void_p),
     "alora_paged_prefill_attn": _sig("alora_paged_prefill_attn", c_i32, c_i32, c_void_p, c_i64, c_i32, c_i32,
                                      c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_i32, c_void_p, c_i32, c_i32,
-                                     c_i32, c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p, c_i64, c_void_p),
+                                     c_i32, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p, c_i64, c_void_p),
     "alora_attn_workspace_bytes": _sig("alora_attn_workspace_bytes", c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                                        c_i32, c_i32, c_i32),
     "alora_gemm_bf16": _sig("alora_gemm_bf16", c_i32, c_i32, c_void_p, c_i32, c_void_p, c_i32, c_void_p, c_i32,
-                            c_i32, c_i32, c_i32, c_void_p),
+                            c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p),
+    "alora_gemm_workspace_bytes": _sig("alora_gemm_workspace_bytes", c_i64),
     "alora_argmax": _sig("alora_argmax", c_i32, c_void_p, c_i32, c_i32, c_void_p, c_void_p),
     "alora_model_workspace_bytes": _sig("alora_model_workspace_bytes", c_i64, ctypes.POINTER(AloraModelDesc)),
     "alora_model_create": _sig("alora_model_create", c_i32, ctypes.POINTER(AloraModelDesc),

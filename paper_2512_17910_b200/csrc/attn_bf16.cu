@@ -1,29 +1,44 @@
 // Paged causal prefill attention, bf16 tier (model.py:149-187 generalised to GQA).
 //
-// Work item = (sequence, kv head, 64-row query tile, KV partition). Query rows
+// Work item = (sequence, kv head, 128-row query tile, KV partition). Query rows
 // are GQA-packed: row r of a sequence's tile space is (token r / G, q head
 // kvh*G + r % G), so one K/V tile read from HBM serves all G query heads that
-// share it. K/V tiles of 64 keys are gathered page by page through the block
-// table with cp.async (16-byte chunks, XOR-swizzled smem rows, double
-// buffered); QK^T and PV use mma.sync m16n8k16 bf16 with fp32 accumulation and
-// an fp32 online softmax (exp2). When a step has too few work items to fill
-// the 148 SMs (the aLoRA suffix turn: few query rows, long cached prefix) the
-// key range is split into partitions whose partial (m, l, O) are merged by a
-// second kernel in a fixed partition order.
+// share it. A CTA runs 8 warps of 16 rows; only ceil(rows/16) warps compute, so
+// a 20-token aLoRA suffix (80 packed rows at G=4) costs 5 warps, not two full
+// 64-row tiles. K/V tiles of 64 keys are gathered page by page through the
+// block table with cp.async (one table lookup per key row, 16-byte chunks,
+// XOR-swizzled smem rows, 3-stage ring); QK^T and PV use mma.sync m16n8k16 bf16
+// with fp32 accumulation and an fp32 online softmax (ex2.approx). Causal masks
+// are evaluated only on tiles that cross the diagonal or the partition end.
+//
+// When a step has too few work items to fill the 148 SMs (the aLoRA suffix turn
+// and decode: few query rows, long cached prefix) the key range is split into
+// partitions; each partition CTA publishes (m, l, O) partials and the last one
+// to arrive for a query tile merges them in partition order (deterministic),
+// so no separate combine kernel runs.
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
+#include "sm100.cuh"
+#include "tma_host.h"
 
 namespace alora {
 
 namespace {
 
-constexpr int kQT = 64;       // packed query rows per CTA
+constexpr int kQT = 128;      // packed query rows per CTA (8 warps x 16)
 constexpr int kKT = 64;       // keys per KV tile
-constexpr int kThreadsA = 128;
-constexpr int kTargetCtas = 2 * kNumSMs;
+constexpr int kThreadsA = 256;
+constexpr int kTargetCtas = 2 * kNumSMs;  // two resident CTAs per SM
+constexpr int kStagesA = 3;               // cp.async ring depth for K/V tiles
+constexpr int kMinPartKeys = 128;
+constexpr int kMaxCounters = 4096;
+constexpr int kMaxParts = 8;  // split-KV partitions per query tile (merge keeps them all in registers)
 
 struct AttnArgs {
   const __nv_bfloat16* q;
@@ -35,12 +50,15 @@ struct AttnArgs {
   const __nv_bfloat16* kv;
   int n_layers, layer, B, H, Hkv, D;
   float scale_log2;  // log2(e) / sqrt(D)
-  int part_size;     // keys per partition (multiple of kKT); >= max_ctx when not split
+  int part_size;     // keys per partition (multiple of kKT)
   int n_parts;
+  int n_qtiles;      // gridDim.x
   __nv_bfloat16* out;
   int64_t ld_out;
-  float* ws_o;  // [n_parts][M*H][D] when split
-  float* ws_ml; // [n_parts][M*H][2]
+  float* ws_o;   // [n_parts][M*H][D] when split
+  float* ws_ml;  // [n_parts][M*H][2]
+  int* counters; // [n_seqs * Hkv * n_qtiles], zero between launches
+  unsigned long long* trace;  // optional per-CTA %globaltimer stamps (ALORA_ATTN_TRACE=1)
   int M;
 };
 
@@ -69,6 +87,12 @@ __device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], 
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
+// 2^x on the SFU (ex2.approx.ftz): exp2(-inf) = +0, as the softmax needs for masked keys.
+__device__ __forceinline__ float fast_exp2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -83,11 +107,16 @@ __device__ __forceinline__ __nv_bfloat16* tile_ptr(__nv_bfloat16* base, int row,
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) {
+__device__ void merge_partials(const AttnArgs& a, int s, int kvh, int qt, int row0, int start, int rows_here,
+                               int parts_here, int G, int* s_last);
+
+template <int D>
+__global__ void __launch_bounds__(kThreadsA, D == 64 ? 2 : 1) attn_bf16_kernel(const AttnArgs a) {
   extern __shared__ __align__(128) uint8_t smem_attn[];
   __nv_bfloat16* sQ = reinterpret_cast<__nv_bfloat16*>(smem_attn);
-  __nv_bfloat16* sK = sQ + kQT * D;       // [2][kKT][D]
-  __nv_bfloat16* sV = sK + 2 * kKT * D;   // [2][kKT][D]
+  __nv_bfloat16* sK = sQ + kQT * D;             // [kStagesA][kKT][D]
+  __nv_bfloat16* sV = sK + kStagesA * kKT * D;  // [kStagesA][kKT][D]
+  __shared__ int s_last;
 
   const int G = a.H / a.Hkv;
   const int s = blockIdx.z / a.Hkv, kvh = blockIdx.z % a.Hkv;
@@ -96,13 +125,17 @@ __global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) 
   const int n_tok = a.cu_q[s + 1] - row0;
   const int R = n_tok * G;
   if (qt * kQT >= R) return;
+  const int rows_here = min(kQT, R - qt * kQT);
   const int start = a.start_pos[s];
-  const int last_tok = min(n_tok - 1, (qt * kQT + kQT - 1) / G);
-  const int key_end = min(start + last_tok + 1, (part + 1) * a.part_size);  // exclusive
+  const int last_tok = (qt * kQT + rows_here - 1) / G;
+  const int tile_end = start + last_tok + 1;  // exclusive key bound of the whole tile
   const int key_begin = part * a.part_size;
+  const int key_end = min(tile_end, key_begin + a.part_size);
   if (key_begin >= key_end) return;  // nothing visible in this partition for any row of the tile
+  const int parts_here = min(a.n_parts, (tile_end + a.part_size - 1) / a.part_size);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool active = warp * 16 < rows_here;  // warp-uniform
   const int kvw = a.Hkv * D;
   const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;
   constexpr int CH = D / 8;  // 16-byte chunks per row
@@ -110,59 +143,77 @@ __global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) 
   // ---- Q tile (packed rows) -> smem
   for (int i = tid; i < kQT * CH; i += kThreadsA) {
     const int r = i / CH, c = i % CH;
+    const bool valid = r < rows_here;
     const int pr = qt * kQT + r;
-    const bool valid = pr < R;
     const int tok = valid ? pr / G : 0, g = valid ? pr % G : 0;
     const __nv_bfloat16* src = a.q + (int64_t)(row0 + tok) * a.ld_q + (kvh * G + g) * D + c * 8;
     cp_async16(tile_ptr<D>(sQ, r, c * 8), valid ? src : a.q, valid);
   }
+  // K/V loader: thread owns key row tid/4 and a quarter of its chunks (one block-table lookup per row)
+  const int lrow = tid >> 2, lq = tid & 3;
+  const int64_t vstep = (int64_t)a.B * kvw;
   auto load_kv = [&](int buf, int k0) {
     __nv_bfloat16* dk = sK + buf * kKT * D;
     __nv_bfloat16* dv = sV + buf * kKT * D;
-    for (int i = tid; i < kKT * CH; i += kThreadsA) {
-      const int r = i / CH, c = i % CH;
-      const int t = k0 + r;
-      const bool valid = t < key_end;
-      const __nv_bfloat16* ksrc = a.kv;
-      if (valid) {
-        const int64_t blk = bt[t / a.B];
-        ksrc = a.kv + ((((blk * a.n_layers + a.layer) * 2) * a.B + (t % a.B)) * (int64_t)kvw) + kvh * D + c * 8;
-      }
-      cp_async16(tile_ptr<D>(dk, r, c * 8), ksrc, valid);
-      cp_async16(tile_ptr<D>(dv, r, c * 8), valid ? ksrc + (int64_t)a.B * kvw : a.kv, valid);
+    const int t = k0 + lrow;
+    const bool valid = t < key_end;
+    const __nv_bfloat16* ksrc = a.kv;
+    if (valid) {
+      const int bi = t / a.B;
+      const int64_t blk = bt[bi];
+      ksrc = a.kv + ((((blk * a.n_layers + a.layer) * 2) * a.B + (t - bi * a.B)) * (int64_t)kvw) + kvh * D;
+    }
+#pragma unroll
+    for (int cc = 0; cc < CH / 4; ++cc) {
+      const int c = lq * (CH / 4) + cc;
+      cp_async16(tile_ptr<D>(dk, lrow, c * 8), valid ? ksrc + c * 8 : a.kv, valid);
+      cp_async16(tile_ptr<D>(dv, lrow, c * 8), valid ? ksrc + vstep + c * 8 : a.kv, valid);
     }
   };
-  load_kv(0, key_begin);
-  cp_async_commit();
+  const int n_tiles = (key_end - key_begin + kKT - 1) / kKT;
+#pragma unroll
+  for (int p = 0; p < kStagesA - 1; ++p) {  // prologue (Q rides with tile 0's group)
+    if (p < n_tiles) load_kv(p, key_begin + p * kKT);
+    cp_async_commit();
+  }
 
   // per-thread rows: lane/4 and lane/4 + 8 of this warp's 16-row slice
   const int wr = warp * 16;
   int pos_r[2];
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int pr = qt * kQT + wr + (lane >> 2) + h * 8;
-    pos_r[h] = pr < R ? start + pr / G : -1;
+    const int r = wr + (lane >> 2) + h * 8;
+    pos_r[h] = r < rows_here ? start + (qt * kQT + r) / G : -1;
   }
+  const int min_pos = start + (qt * kQT + wr) / G;  // this warp's first row sees the fewest keys
   float m_r[2] = {-INFINITY, -INFINITY}, l_r[2] = {0.f, 0.f};
   float o[D / 8][4];
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   uint32_t qf[D / 16][4];
+  // Per-lane swizzled smem offsets (elements) of the ldmatrix rows: the XOR pattern depends only on the lane
+  // because every fragment row block starts at a multiple of 8 rows.
+  int koff[D / 16], voff[D / 16];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    koff[kk] = ((lane & 7) + (lane >> 4) * 8) * D + (((kk * 2 + ((lane >> 3) & 1)) ^ (lane & 7)) << 3);
+    voff[kk] = (lane & 15) * D + (((kk * 2 + (lane >> 4)) ^ (lane & 7)) << 3);
+  }
 
-  const int n_tiles = (key_end - key_begin + kKT - 1) / kKT;
   for (int it = 0; it < n_tiles; ++it) {
     const int k0 = key_begin + it * kKT;
-    if (it + 1 < n_tiles) load_kv((it + 1) & 1, k0 + kKT);
+    cp_async_wait<kStagesA - 2>();  // tile `it` has landed
+    __syncthreads();                // ... for every thread, and buffer (it-1) % kStagesA is free again
+    if (it + kStagesA - 1 < n_tiles) load_kv((it + kStagesA - 1) % kStagesA, k0 + (kStagesA - 1) * kKT);
     cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
+    if (!active) continue;
     if (it == 0) {
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         ldsm_x4(qf[kk], tile_ptr<D>(sQ, wr + (lane & 15), kk * 16 + (lane >> 4) * 8));
     }
-    const __nv_bfloat16* cK = sK + (it & 1) * kKT * D;
-    const __nv_bfloat16* cV = sV + (it & 1) * kKT * D;
+    const __nv_bfloat16* cK = sK + (it % kStagesA) * kKT * D;
+    const __nv_bfloat16* cV = sV + (it % kStagesA) * kKT * D;
     // S = Q K^T  (16 x 64 per warp)
     float sc[kKT / 8][4];
 #pragma unroll
@@ -172,24 +223,24 @@ __global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) 
 #pragma unroll
       for (int jn = 0; jn < kKT / 16; ++jn) {
         uint32_t b[4];
-        const int key = jn * 16 + (lane & 7) + (lane >> 4) * 8;
-        ldsm_x4(b, tile_ptr<D>(const_cast<__nv_bfloat16*>(cK), key, kk * 16 + ((lane >> 3) & 1) * 8));
+        ldsm_x4(b, cK + jn * 16 * D + koff[kk]);
         mma16816(sc[2 * jn], qf[kk], b[0], b[1]);
         mma16816(sc[2 * jn + 1], qf[kk], b[2], b[3]);
       }
     }
-    // mask + online softmax (log2 domain)
+    // mask (only tiles crossing this warp's causal edge or the partition end) + online softmax (log2)
+    const bool need_mask = (k0 + kKT - 1 > min_pos) || (k0 + kKT > key_end);
     float mnew[2];
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       float mx = m_r[h];
+      const int lim = min(pos_r[h], key_end - 1);
 #pragma unroll
       for (int j = 0; j < kKT / 8; ++j) {
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int key = k0 + j * 8 + 2 * (lane & 3) + e;
           float v = sc[j][h * 2 + e] * a.scale_log2;
-          if (key > pos_r[h] || key >= key_end) v = -INFINITY;
+          if (need_mask && (k0 + j * 8 + 2 * (lane & 3) + e > lim)) v = -INFINITY;
           sc[j][h * 2 + e] = v;
           mx = fmaxf(mx, v);
         }
@@ -198,24 +249,22 @@ __global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) 
       mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
       mnew[h] = mx;
     }
-    float rs[2] = {0.f, 0.f};
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const float base = mnew[h] == -INFINITY ? 0.f : mnew[h];
-      const float corr = exp2f(m_r[h] - base);
+      const float corr = fast_exp2(m_r[h] - base);
 #pragma unroll
       for (int j = 0; j < D / 8; ++j) { o[j][h * 2] *= corr; o[j][h * 2 + 1] *= corr; }
-      l_r[h] *= corr;
-      m_r[h] = mnew[h];
+      float rs = 0.f;
 #pragma unroll
       for (int j = 0; j < kKT / 8; ++j) {
-        sc[j][h * 2] = exp2f(sc[j][h * 2] - base);
-        sc[j][h * 2 + 1] = exp2f(sc[j][h * 2 + 1] - base);
-        rs[h] += sc[j][h * 2] + sc[j][h * 2 + 1];
+        sc[j][h * 2] = fast_exp2(sc[j][h * 2] - base);
+        sc[j][h * 2 + 1] = fast_exp2(sc[j][h * 2 + 1] - base);
+        rs += sc[j][h * 2] + sc[j][h * 2 + 1];
       }
+      l_r[h] = l_r[h] * corr + rs;
+      m_r[h] = mnew[h];
     }
-    l_r[0] += rs[0];
-    l_r[1] += rs[1];
     // O += P V
 #pragma unroll
     for (int kk = 0; kk < kKT / 16; ++kk) {
@@ -227,141 +276,536 @@ __global__ void __launch_bounds__(kThreadsA) attn_bf16_kernel(const AttnArgs a) 
 #pragma unroll
       for (int jd = 0; jd < D / 16; ++jd) {
         uint32_t b[4];
-        ldsm_x4_t(b, tile_ptr<D>(const_cast<__nv_bfloat16*>(cV), kk * 16 + (lane & 15), jd * 16 + (lane >> 4) * 8));
+        ldsm_x4_t(b, cV + kk * 16 * D + voff[jd]);
         mma16816(o[2 * jd], pa, b[0], b[1]);
         mma16816(o[2 * jd + 1], pa, b[2], b[3]);
       }
     }
-    __syncthreads();
   }
-  // finalize: full row sums across the 4 lanes of a quad
+  cp_async_wait<0>();
+  if (active) {
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
-    l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
-  }
+    for (int h = 0; h < 2; ++h) {  // full row sums across the 4 lanes of a quad
+      l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 1);
+      l_r[h] += __shfl_xor_sync(0xffffffffu, l_r[h], 2);
+    }
 #pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int pr = qt * kQT + wr + (lane >> 2) + h * 8;
-    if (pr >= R || pos_r[h] < key_begin) continue;
-    const int tok = pr / G, head = kvh * G + pr % G;
-    const int64_t grow = row0 + tok;
-    if (a.n_parts == 1) {
-      const float inv = 1.f / l_r[h];
-      __nv_bfloat16* dst = a.out + grow * a.ld_out + head * D;
+    for (int h = 0; h < 2; ++h) {
+      const int r = wr + (lane >> 2) + h * 8;
+      if (r >= rows_here || pos_r[h] < key_begin) continue;
+      const int pr = qt * kQT + r;
+      const int tok = pr / G, head = kvh * G + pr % G;
+      const int64_t grow = row0 + tok;
+      if (parts_here == 1) {
+        const float inv = 1.f / l_r[h];
+        __nv_bfloat16* dst = a.out + grow * a.ld_out + head * D;
 #pragma unroll
-      for (int j = 0; j < D / 8; ++j)
-        *reinterpret_cast<__nv_bfloat162*>(dst + j * 8 + 2 * (lane & 3)) =
-            __floats2bfloat162_rn(o[j][h * 2] * inv, o[j][h * 2 + 1] * inv);
-    } else {
-      const int64_t slot = ((int64_t)part * a.M + grow) * a.H + head;
-      float* dst = a.ws_o + slot * D;
+        for (int j = 0; j < D / 8; ++j)
+          *reinterpret_cast<__nv_bfloat162*>(dst + j * 8 + 2 * (lane & 3)) =
+              __floats2bfloat162_rn(o[j][h * 2] * inv, o[j][h * 2 + 1] * inv);
+      } else {
+        const int64_t slot = ((int64_t)part * a.M + grow) * a.H + head;
+        float* dst = a.ws_o + slot * D;
 #pragma unroll
-      for (int j = 0; j < D / 8; ++j)
-        *reinterpret_cast<float2*>(dst + j * 8 + 2 * (lane & 3)) = make_float2(o[j][h * 2], o[j][h * 2 + 1]);
-      if ((lane & 3) == 0) {
-        a.ws_ml[slot * 2] = m_r[h];
-        a.ws_ml[slot * 2 + 1] = l_r[h];
+        for (int j = 0; j < D / 8; ++j)
+          __stcg(reinterpret_cast<float2*>(dst + j * 8 + 2 * (lane & 3)), make_float2(o[j][h * 2], o[j][h * 2 + 1]));
+        if ((lane & 3) == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_r[h], l_r[h]));
       }
     }
   }
+  if (parts_here == 1) return;
+  merge_partials<D>(a, s, kvh, qt, row0, start, rows_here, parts_here, G, &s_last);
 }
 
-// Merge partitions in fixed order: one warp per (row, head).
-__global__ void attn_combine_kernel(const AttnArgs a, int n_seqs) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (w >= a.M * a.H) return;
-  const int row = w / a.H, head = w % a.H;
-  const int s = seq_of_row(a.cu_q, n_seqs, row);
-  const int pos = a.start_pos[s] + (row - a.cu_q[s]);
-  const int np = min(a.n_parts, pos / a.part_size + 1);
-  float m = -INFINITY;
-  for (int p = 0; p < np; ++p) m = fmaxf(m, a.ws_ml[(((int64_t)p * a.M + row) * a.H + head) * 2]);
-  float l = 0.f;
-  float acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int p = 0; p < np; ++p) {
-    const int64_t slot = ((int64_t)p * a.M + row) * a.H + head;
-    const float wgt = exp2f(a.ws_ml[slot * 2] - m);
-    l += wgt * a.ws_ml[slot * 2 + 1];
-    for (int i = 0; i < a.D / 32; ++i) acc[i] += wgt * a.ws_o[slot * a.D + lane + 32 * i];
+// Last partition CTA to arrive for query tile (s, kvh, qt) merges the partials in partition order.
+// Called by every thread of the CTA after its own partials are stored.
+template <int D>
+__device__ void merge_partials(const AttnArgs& a, int s, int kvh, int qt, int row0, int start, int rows_here,
+                               int parts_here, int G, int* s_last) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  __syncthreads();  // CTA-scope: every thread's partial stores happen-before thread 0's cumulative gpu fence
+  int* ctr = a.counters + ((int64_t)s * a.Hkv + kvh) * a.n_qtiles + qt;
+  if (tid == 0) {
+    __threadfence();
+    const int prev = atomicAdd(ctr, 1);
+    *s_last = prev == parts_here - 1;
+    if (*s_last) {
+      *ctr = 0;  // ready for the next launch
+      __threadfence();
+    }
   }
-  const float inv = 1.f / l;
-  for (int i = 0; i < a.D / 32; ++i)
-    a.out[(int64_t)row * a.ld_out + head * a.D + lane + 32 * i] = __float2bfloat16_rn(acc[i] * inv);
+  __syncthreads();
+  if (!*s_last) return;
+  constexpr int G8 = D / 8;
+  for (int i = tid; i < rows_here * G8; i += nthr) {
+    const int r = i / G8, c8 = (i % G8) * 8;
+    const int pr = qt * kQT + r;
+    const int tok = pr / G, head = kvh * G + pr % G;
+    const int64_t grow = row0 + tok;
+    const int np_row = min(parts_here, (start + tok) / a.part_size + 1);
+    // all loads of a round are issued before any is consumed: two L2 round trips per item, not 2 * np
+    const int64_t slot0 = (int64_t)grow * a.H + head, pstride = (int64_t)a.M * a.H;
+    float2 ml[kMaxParts];
+#pragma unroll
+    for (int p = 0; p < kMaxParts; ++p)
+      ml[p] = p < np_row ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml + (slot0 + p * pstride) * 2))
+                         : make_float2(-INFINITY, 0.f);
+    float4 x0[kMaxParts], x1[kMaxParts];
+#pragma unroll
+    for (int p = 0; p < kMaxParts; ++p) {
+      if (p < np_row) {
+        x0[p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8));
+        x1[p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8 + 4));
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int p = 0; p < kMaxParts; ++p) mx = fmaxf(mx, ml[p].x);
+    float l = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int p = 0; p < kMaxParts; ++p) {  // partition order: deterministic
+      if (p >= np_row) break;
+      const float w = fast_exp2(ml[p].x - mx);
+      l += w * ml[p].y;
+      acc[0] += w * x0[p].x; acc[1] += w * x0[p].y; acc[2] += w * x0[p].z; acc[3] += w * x0[p].w;
+      acc[4] += w * x1[p].x; acc[5] += w * x1[p].y; acc[6] += w * x1[p].z; acc[7] += w * x1[p].w;
+    }
+    const float inv = 1.f / l;
+    __align__(16) __nv_bfloat162 ov[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ov[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+    *reinterpret_cast<int4*>(a.out + grow * a.ld_out + head * D + c8) = *reinterpret_cast<int4*>(ov);
+  }
 }
+
+// ============================================================================================================
+// tcgen05 variant: QK^T and PV on the 5th-gen tensor cores with S and O accumulated in TMEM.
+//   warps 0-3  softmax: thread = query row = TMEM lane; tcgen05.ld its 64 scores per tile, online softmax
+//              (lazy rescale: O in TMEM is rescaled only when the row max grows by > 2^8), P -> smem (SW128)
+//   warp 4     producer: Q once (cp.async gather of the GQA-packed rows), then K/V tiles of 64 keys as TMA
+//              boxes of [B keys x 64 dims], one per page (the block table is the gather index), 4-stage ring
+//   warp 5     TMEM allocator + single-thread MMA issuer: S_t = Q K_t^T (M=128, N=64), O += P_t V_t (N=D,
+//              V as an MN-major operand), S double-buffered so S_{t+1} overlaps softmax_t.
+// Operands live in 64-column (128-byte) swizzled sub-tiles: [D/64][rows][64] bf16.
+// ============================================================================================================
+namespace tc {
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ATTN_TRACE(slot)                                                                                    \
+  do {                                                                                                      \
+    if (a.trace) a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 6 + (slot)] = gtimer(); \
+  } while (0)
+
+constexpr int kNS = 4;          // K/V stages
+constexpr int kThreads = 192;   // 4 softmax + 1 producer + 1 MMA warps
+constexpr float kRescaleLog2 = 8.f;
+
+template <int D>
+struct Smem {
+  static constexpr int kQBytes = kQT * D * 2;        // [D/64][128][64]
+  static constexpr int kKVBytes = kKT * D * 2;       // one K (or V) tile [D/64][64][64]
+  static constexpr int kPBytes = kQT * kKT * 2;      // [128][64]
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + kQBytes;
+  static constexpr int kV = kK + kNS * kKVBytes;
+  static constexpr int kP = kV + kNS * kKVBytes;
+  static constexpr int kBar = kP + 2 * kPBytes;
+  static constexpr int kTotal = kBar + 256 + 1024;  // barriers + TMEM slot + alignment slack
+};
+
+// byte offset of (row, 16B chunk c) inside a [D/64][rows][64] swizzled operand
+__device__ __forceinline__ uint32_t sw_off(int row, int c, int rows) {
+  return (uint32_t)((c >> 3) * rows * 128 + row * 128 + (((c & 7) ^ (row & 7)) << 4));
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
+                                                              const __grid_constant__ CUtensorMap tm_kv) {
+  using L = Smem<D>;
+  extern __shared__ uint8_t smem_raw_tc[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_tc) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kBar);
+  uint64_t* q_full = bars;             // 1
+  uint64_t* kv_full = bars + 1;        // kNS
+  uint64_t* kv_empty = kv_full + kNS;  // kNS
+  uint64_t* s_full = kv_empty + kNS;   // 2
+  uint64_t* p_full = s_full + 2;       // 2
+  uint64_t* pv_done = p_full + 2;      // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  __shared__ int s_last;
+
+  const int G = a.H / a.Hkv;
+  const int s = blockIdx.z / a.Hkv, kvh = blockIdx.z % a.Hkv;
+  const int qt = blockIdx.x, part = blockIdx.y;
+  const int row0 = a.cu_q[s];
+  const int n_tok = a.cu_q[s + 1] - row0;
+  const int R = n_tok * G;
+  if (qt * kQT >= R) return;
+  const int rows_here = min(kQT, R - qt * kQT);
+  const int start = a.start_pos[s];
+  const int tile_end = start + (qt * kQT + rows_here - 1) / G + 1;
+  const int key_begin = part * a.part_size;
+  const int key_end = min(tile_end, key_begin + a.part_size);
+  if (key_begin >= key_end) return;
+  const int parts_here = min(a.n_parts, (tile_end + a.part_size - 1) / a.part_size);
+  const int n_tiles = (key_end - key_begin + kKT - 1) / kKT;
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) ATTN_TRACE(0);
+  constexpr int CH = D / 8;
+  if (tid == 0) {
+    sm100::mbar_init(q_full, 32);
+    for (int i = 0; i < kNS; ++i) {
+      sm100::mbar_init(&kv_full[i], 1);
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&p_full[i], 128);
+      sm100::mbar_init(&pv_done[i], 1);
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 5) sm100::tmem_alloc<256>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tS[2] = {tmem, tmem + 64};
+  const uint32_t tO = tmem + 128;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------------ producer warp
+    // Q: the 32 lanes gather the 128 GQA-packed rows (4 each) with cp.async into the swizzled layout
+    for (int p = lane; p < kQT; p += 32) {
+      const bool valid = p < rows_here;
+      const int pr = qt * kQT + p;
+      const __nv_bfloat16* src = a.q + (int64_t)(row0 + (valid ? pr / G : 0)) * a.ld_q + (kvh * G + (valid ? pr % G : 0)) * D;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cp_async16(sm + L::kQ + sw_off(p, c, kQT), valid ? src + c * 8 : a.q, valid);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    sm100::fence_proxy_async_smem();
+    sm100::mbar_arrive(q_full);
+    // K/V: one lane issues TMA boxes of [B keys x 64 dims] page by page (the block table is the gather index)
+    if (lane == 0) {
+      const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;
+      const int last_blk = (key_end - 1) / a.B;
+      const int per_tile = kKT / a.B;
+      const uint64_t pol = sm100::policy_evict_last();  // prefix blocks are shared by requests of the step
+      for (int t = 0; t < n_tiles; ++t) {
+        const int st = t % kNS;
+        if (t >= kNS) sm100::mbar_wait(&kv_empty[st], ((t / kNS) - 1) & 1);
+        sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
+        uint8_t* dk = sm + L::kK + st * L::kKVBytes;
+        uint8_t* dv = sm + L::kV + st * L::kKVBytes;
+        const int b0 = (key_begin + t * kKT) / a.B;
+        for (int j = 0; j < per_tile; ++j) {
+          const int64_t blk = bt[min(b0 + j, last_blk)];  // past the end: a valid duplicate, masked later
+          const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+#pragma unroll
+          for (int sub = 0; sub < D / 64; ++sub) {
+            sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk,
+                               pol);
+            sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
+                               rowk + a.B, pol);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (sm100::elect_one()) {
+      constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
+      constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
+      sm100::mbar_wait(q_full, 0);
+      ATTN_TRACE(1);
+      sm100::tc_fence_after();
+      auto issue_s = [&](int t) {
+        const int st = t % kNS;
+        sm100::mbar_wait(&kv_full[st], (t / kNS) & 1);
+        sm100::tc_fence_after();
+        const uint8_t* qb = sm + L::kQ;
+        const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks) {  // K = D in 16-wide steps; sub-tile every 4 steps
+          const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
+          const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
+          sm100::mma_bf16_ss(tS[t & 1], da, db, idesc_s, ks > 0 ? 1u : 0u);
+        }
+        sm100::mma_commit(&s_full[t & 1]);
+      };
+      issue_s(0);
+      for (int t = 0; t < n_tiles; ++t) {
+        if (t + 1 < n_tiles) issue_s(t + 1);  // S buffer (t+1)&1 was drained: p_full for t-1 was awaited
+        sm100::mbar_wait(&p_full[t & 1], (t >> 1) & 1);
+        sm100::tc_fence_after();
+        const uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
+        const uint8_t* vb = sm + L::kV + (t % kNS) * L::kKVBytes;
+#pragma unroll
+        for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
+          const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
+          const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
+          sm100::mma_bf16_ss(tO, da, db, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+        }
+        sm100::mma_commit(&pv_done[t & 1]);
+        sm100::mma_commit(&kv_empty[t % kNS]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ------------------------------------------------------------------ softmax (warps 0-3)
+    const int r = tid;  // TMEM lane == packed row
+    const bool live = r < rows_here;
+    const bool warp_live = warp * 32 < rows_here;
+    const int pos = live ? start + (qt * kQT + r) / G : -1;
+    const int lim = min(pos, key_end - 1);
+    const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < n_tiles; ++t) {
+      const int k0 = key_begin + t * kKT;
+      sm100::mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+      sm100::tc_fence_after();
+      if (t == 0 && tid == 0) ATTN_TRACE(2);
+      float sv[kKT];
+      if (warp_live) {
+        uint32_t r0[32], r1[32];
+        sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base, r0);
+        sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base + 32, r1);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sv[j] = __uint_as_float(r0[j]) * a.scale_log2;
+          sv[j + 32] = __uint_as_float(r1[j]) * a.scale_log2;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < kKT; ++j) sv[j] = -INFINITY;
+      }
+      const bool need_mask = k0 + kKT - 1 > lim;
+      float mt = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < kKT; ++j) {
+        if (need_mask && k0 + j > lim) sv[j] = -INFINITY;
+        mt = fmaxf(mt, sv[j]);
+      }
+      const float m_new = fmaxf(m_run, mt);
+      // lazy rescale: only when the max grew by more than 2^8 (or on the first finite max)
+      const bool grow = m_new > m_run + kRescaleLog2 || (m_run == -INFINITY && m_new != -INFINITY);
+      if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY) && warp_live) {
+        const float corr = grow && m_run != -INFINITY ? fast_exp2(m_run - m_new) : 1.f;
+        sm100::mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV_{t-1}
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t ov[32];
+          sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
+          sm100::tmem_st_32x32b_x32(tO + lane_base + c, ov);
+        }
+        sm100::tmem_st_wait();
+        l_run *= corr;
+      }
+      if (grow) m_run = m_new;
+      const float base = m_run == -INFINITY ? 0.f : m_run;
+      float rs = 0.f;
+      if (t >= 2) sm100::mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);  // P buffer t&1 drained by PV_{t-2}
+      uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {  // 8 keys -> one 16-byte swizzled chunk at a time (few live registers)
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float p0 = fast_exp2(sv[c * 8 + 2 * e] - base), p1 = fast_exp2(sv[c * 8 + 2 * e + 1] - base);
+          rs += p0 + p1;
+          pk[e] = pack_bf16(p0, p1);
+        }
+        *reinterpret_cast<int4*>(pb + sw_off(r, c, kQT)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
+      }
+      l_run += rs;
+      sm100::fence_proxy_async_smem();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&p_full[t & 1]);
+    }
+    if (tid == 0) ATTN_TRACE(3);
+    // final O
+    sm100::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    sm100::tc_fence_after();
+    if (warp_live) {
+      const int pr = qt * kQT + r;
+      const int tok = live ? pr / G : 0, head = kvh * G + (live ? pr % G : 0);
+      const int64_t grow_ = row0 + tok;
+      const bool emit = live && pos >= key_begin;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t ov[32];
+        sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+        sm100::tmem_ld_wait();
+        if (!emit) continue;
+        if (parts_here == 1) {
+          __nv_bfloat16* dst = a.out + grow_ * a.ld_out + head * D + c;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            __align__(16) __nv_bfloat162 o2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              o2[e] = __floats2bfloat162_rn(__uint_as_float(ov[q * 8 + e * 2]) * inv,
+                                            __uint_as_float(ov[q * 8 + e * 2 + 1]) * inv);
+            *reinterpret_cast<int4*>(dst + q * 8) = *reinterpret_cast<int4*>(o2);
+          }
+        } else {
+          const int64_t slot = ((int64_t)part * a.M + grow_) * a.H + head;
+          float* dst = a.ws_o + slot * D + c;
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            __stcg(reinterpret_cast<float4*>(dst + q * 4),
+                   make_float4(__uint_as_float(ov[q * 4]), __uint_as_float(ov[q * 4 + 1]),
+                               __uint_as_float(ov[q * 4 + 2]), __uint_as_float(ov[q * 4 + 3])));
+          if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run, l_run));
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) sm100::tmem_dealloc<256>(tmem);
+  if (tid == 0) ATTN_TRACE(4);
+  if (parts_here > 1) merge_partials<D>(a, s, kvh, qt, row0, start, rows_here, parts_here, G, &s_last);
+  if (tid == 0) ATTN_TRACE(5);
+}
+
+}  // namespace tc
 
 // Partition plan shared by the workspace query and the launch.
-void plan(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int& part_size, int& n_parts) {
+void plan(int n_seqs, int max_q, int max_ctx, int H, int Hkv, int& part_size, int& n_parts, int& n_qtiles) {
   const int G = H / Hkv;
-  const int qtiles = (max_q * G + kQT - 1) / kQT;
-  const int64_t items = (int64_t)qtiles * n_seqs * Hkv;
-  const int max_parts = (max_ctx + 255) / 256;  // at least 256 keys per partition
+  n_qtiles = (max_q * G + kQT - 1) / kQT;
+  const int64_t items = (int64_t)n_qtiles * n_seqs * Hkv;
+  const int max_parts = (max_ctx + kMinPartKeys - 1) / kMinPartKeys;
   int np = 1;
-  if (items < kTargetCtas) np = (int)((kTargetCtas + items - 1) / items);
-  np = std::max(1, std::min(np, max_parts));
+  if (items < kTargetCtas && items <= kMaxCounters) np = (int)((kTargetCtas + items - 1) / items);
+  np = std::max(1, std::min({np, max_parts, kMaxParts}));
   int ps = (max_ctx + np - 1) / np;
   ps = (ps + kKT - 1) / kKT * kKT;
   n_parts = (max_ctx + ps - 1) / ps;
   part_size = ps;
-  (void)M;
 }
 
 template <int D>
-int launch_attn(const AttnArgs& a, int n_seqs, int max_q, cudaStream_t st) {
-  const int G = a.H / a.Hkv;
-  const int smem = (kQT + 4 * kKT) * D * 2;
-  static bool configured = false;
-  if (!configured) {
-    if (cudaFuncSetAttribute(attn_bf16_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-      return ALORA_ECUDA;
-    configured = true;
+int launch_attn(const AttnArgs& a, int n_seqs, int64_t kv_rows, cudaStream_t st) {
+  dim3 grid(a.n_qtiles, a.n_parts, n_seqs * a.Hkv);
+  static const bool force_mma = getenv("ALORA_ATTN_MMA") != nullptr;  // A/B switch to the mma.sync kernel
+  // the tcgen05 kernel loads pages with TMA boxes of [B x 64]: B must tile the 64-key KV tile
+  const bool use_tc = !force_mma && a.B <= kKT && kKT % a.B == 0 && kv_rows > 0 && kv_rows < (1ll << 31);
+  CUtensorMap tm{};
+  if (use_tc && !make_tmap_2d(&tm, a.kv, (uint64_t)kv_rows, (uint64_t)a.Hkv * D, (uint64_t)a.Hkv * D, a.B, 64))
+    return ALORA_ECUDA;
+  if (!use_tc) {
+    const int smem = (kQT + 2 * kStagesA * kKT) * D * 2;
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(attn_bf16_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return ALORA_ECUDA;
+      configured = true;
+    }
+    attn_bf16_kernel<D><<<grid, kThreadsA, smem, st>>>(a);
+  } else {
+    const int smem = tc::Smem<D>::kTotal;
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(tc::attn_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return ALORA_ECUDA;
+      configured = true;
+    }
+    static const bool tracing = getenv("ALORA_ATTN_TRACE") != nullptr;
+    static unsigned long long* tbuf = nullptr;
+    const int n_ctas = grid.x * grid.y * grid.z;
+    AttnArgs ta = a;
+    if (tracing) {
+      if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 6 * 65536);
+      cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
+      ta.trace = tbuf;
+    }
+    tc::attn_tc_kernel<D><<<grid, tc::kThreads, smem, st>>>(ta, tm);
+    if (tracing) {  // debug: per-phase means over the CTAs that ran (early-exit CTAs have no stamps)
+      std::vector<unsigned long long> h(6 * n_ctas);
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+      unsigned long long t0 = ~0ull, t1 = 0;
+      double ph[5] = {0, 0, 0, 0, 0};
+      int live = 0;
+      for (int c = 0; c < n_ctas; ++c) {
+        if (!h[6 * c] || !h[6 * c + 5]) continue;
+        ++live;
+        t0 = std::min(t0, h[6 * c]);
+        t1 = std::max(t1, h[6 * c + 5]);
+        for (int p = 0; p < 5; ++p)
+          if (h[6 * c + p + 1] && h[6 * c + p]) ph[p] += double(h[6 * c + p + 1] - h[6 * c + p]);
+      }
+      fprintf(stderr, "[attn trace] ctas %d/%d span %.2f us; mean start->Q %.2f, Q->S0 %.2f, S0->last P %.2f, "
+              "->epilogue %.2f, merge %.2f us (parts %d, part keys %d)\n", live, n_ctas, (t1 - t0) / 1e3,
+              ph[0] / live / 1e3, ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3, ph[4] / live / 1e3,
+              a.n_parts, a.part_size);
+    }
   }
-  dim3 grid((max_q * G + kQT - 1) / kQT, a.n_parts, n_seqs * a.Hkv);
-  attn_bf16_kernel<D><<<grid, kThreadsA, smem, st>>>(a);
   ALORA_LAUNCH_CHECK();
-  if (a.n_parts > 1) {
-    const int warps = a.M * a.H;
-    attn_combine_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(a, n_seqs);
-    ALORA_LAUNCH_CHECK();
-  }
   return ALORA_OK;
 }
 
 }  // namespace
 
-// Upper bound over all steps: a split happens only when items < kTargetCtas, and then
-// n_parts * M * H <= 2 * kTargetCtas * kQT (see plan()).
+void configure_attention() {
+  prefer_max_smem(attn_bf16_kernel<64>);
+  prefer_max_smem(attn_bf16_kernel<128>);
+  prefer_max_smem(tc::attn_tc_kernel<64>);
+  prefer_max_smem(tc::attn_tc_kernel<128>);
+}
+
+// Upper bound over all steps: a split happens only when items < kTargetCtas; then every item covers <= kQT
+// packed rows, so n_parts * M * H <= kQT * (kTargetCtas + items) < 2 * kQT * kTargetCtas.
 int64_t attn_bf16_workspace_bound(int H, int D) {
   (void)H;
-  return (int64_t)2 * kTargetCtas * kQT * (D + 2) * 4;
+  return (int64_t)2 * kTargetCtas * kQT * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
 }
 
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D) {
-  int ps, np;
-  plan(M, n_seqs, max_q, max_ctx, H, Hkv, ps, np);
+  int ps, np, nq;
+  plan(n_seqs, max_q, max_ctx, H, Hkv, ps, np, nq);
   if (np <= 1) return 0;
-  return (int64_t)np * M * H * (D + 2) * 4;
+  return (int64_t)np * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
 }
 
 int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int32_t* cu_q, const int32_t* start_pos,
               const int32_t* block_table, int max_blocks, int max_q, int max_ctx, const __nv_bfloat16* kv,
               int n_layers, int layer, int B, int H, int Hkv, int D, __nv_bfloat16* out, int64_t ld_out, void* ws,
-              int64_t ws_bytes, cudaStream_t st) {
+              int64_t ws_bytes, cudaStream_t st, int total_blocks) {
   if (M == 0 || n_seqs == 0) return ALORA_OK;
-  if (H % Hkv || (D != 64 && D != 128) || ld_q % 8 || max_q < 1 || max_ctx < 1) return ALORA_EINVAL;
+  if (H % Hkv || (D != 64 && D != 128) || ld_q % 8 || ld_out % 8 || max_q < 1 || max_ctx < 1) return ALORA_EINVAL;
   AttnArgs a{};
   a.q = q; a.ld_q = ld_q; a.cu_q = cu_q; a.start_pos = start_pos; a.block_table = block_table;
   a.max_blocks = max_blocks; a.kv = kv; a.n_layers = n_layers; a.layer = layer; a.B = B; a.H = H; a.Hkv = Hkv;
   a.D = D; a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   a.out = out; a.ld_out = ld_out; a.M = M;
-  plan(M, n_seqs, max_q, max_ctx, H, Hkv, a.part_size, a.n_parts);
+  plan(n_seqs, max_q, max_ctx, H, Hkv, a.part_size, a.n_parts, a.n_qtiles);
   if (a.n_parts > 1) {
-    const int64_t need = (int64_t)a.n_parts * M * H * (D + 2) * 4;
+    const int64_t need = (int64_t)a.n_parts * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
     if (ws == nullptr || ws_bytes < need) return ALORA_EINVAL;
+    // counters live at the END of the caller's buffer so their position does not depend on the step shape
+    a.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + ws_bytes - (int64_t)kMaxCounters * 4);
     a.ws_o = static_cast<float*>(ws);
     a.ws_ml = a.ws_o + (int64_t)a.n_parts * M * H * D;
   }
-  return D == 64 ? launch_attn<64>(a, n_seqs, max_q, st) : launch_attn<128>(a, n_seqs, max_q, st);
+  const int64_t kv_rows = (int64_t)total_blocks * n_layers * 2 * B;
+  return D == 64 ? launch_attn<64>(a, n_seqs, kv_rows, st) : launch_attn<128>(a, n_seqs, kv_rows, st);
 }
 
 }  // namespace alora

@@ -168,6 +168,14 @@ __global__ void lora_tile_masks_kernel(const int32_t* __restrict__ row_slot, con
   if (threadIdx.x == 0) masks[tile] = part[0] | part[1] | part[2] | part[3];
 }
 
+void configure_bf16_ops() {
+  prefer_max_smem(embed_bf16_kernel);
+  prefer_max_smem(rmsnorm_bf16_kernel);
+  prefer_max_smem(rope_bf16_kernel);
+  prefer_max_smem(lora_shrink_bf16_kernel);
+  prefer_max_smem(lora_tile_masks_kernel);
+}
+
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st) {
   if (M == 0) return ALORA_OK;
   lora_tile_masks_kernel<<<(M + 127) / 128, 128, 0, st>>>(row_slot, row_apply, M, masks);

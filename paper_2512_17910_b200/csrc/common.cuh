@@ -21,6 +21,15 @@
 
 namespace alora {
 
+// Every kernel asks for the max-shared-memory carveout so the SMs never switch the
+// L1/smem split between the 200 KB tcgen05 GEMM and the small kernels around it
+// (a carveout change drains the SM and costs microseconds per launch).
+template <typename Kernel>
+inline void prefer_max_smem(Kernel kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       static_cast<int>(cudaSharedmemCarveoutMaxShared));
+}
+
 constexpr int kNumSMs = 148;
 constexpr int kGluBlock = 64;  // gate|up interleave granularity of w_in_t (llama)
 

@@ -11,13 +11,27 @@
 // second pass. K-blocks of the LoRA range whose adapters are absent from the
 // 128-row tile (per-tile slot mask) are skipped entirely.
 //
-// Structure (one 128 x BN output tile per CTA, 192 threads):
+// Structure (one 128 x BN output tile per CTA and K split, 192 threads):
 //   warp 0      TMA producer: A/B (or S/U) 64-wide K slabs -> smem ring (SW128)
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 cols -> fused epilogue -> global
 // mbarrier ring: full[s] (TMA tx bytes) / empty[s] (tcgen05.commit), tmem_full.
-// Each output element accumulates its K range in a fixed order (no split-K):
-// the result of a row does not depend on M or on its neighbours.
+//
+// Weight-streaming launches (few output tiles: small M) split K across a
+// thread-block cluster of up to 8 CTAs (cluster dims 1x1xS) so that every SM
+// streams a disjoint slab of the weights exactly once. Each CTA parks its fp32
+// partial tile in its own shared memory; after a cluster barrier CTA r reduces
+// rows [r*128/S, (r+1)*128/S) over distributed shared memory, summing the S
+// partials in rank order (deterministic), and runs the epilogue for those
+// rows. No global partials, no second kernel.
+// Epilogues: bf16 store, fp32 store, residual add (C += acc), ReLU, SwiGLU of
+// 64-interleaved gate|up blocks, rotate-half RoPE on q/k columns, and the
+// LoRA-shrink row/slot select.
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -32,6 +46,7 @@ constexpr int kBM = 128;
 constexpr int kBK = 64;
 constexpr int kThreads = 192;
 constexpr int kSmemBudget = 200 * 1024;
+constexpr int kMaxSplits = 8;  // portable cluster size
 
 struct GemmArgs {
   void* C;
@@ -46,15 +61,35 @@ struct GemmArgs {
   const float* rope_cos;
   const float* rope_sin;
   int rope_cols, head_dim;
+  const int32_t* sel_row_slot;  // kEpiLoraSelect
+  const uint8_t* sel_row_apply;
+  const uint8_t* sel_targets;
+  int sel_sr, sel_rank;
+  int splits;                 // K splits (blockIdx.z); grid <= SM count, cooperative launch
+  float* partial;             // [splits][m_tiles*128][N] fp32 when splits > 1
+  int* counters;              // 2 per output tile (arrive, depart); zero between launches
+  unsigned long long* trace;  // optional per-CTA %globaltimer stamps (ALORA_GEMM_TRACE=1)
 };
+
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(slot)                                                                                   \
+  do {                                                                                                \
+    if (args.trace) args.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 6 + (slot)] = gtime(); \
+  } while (0)
 
 template <int BN>
 struct Cfg {
   static constexpr int kABytes = kBM * kBK * 2;
   static constexpr int kBBytes = BN * kBK * 2;
   static constexpr int kStage = kABytes + kBBytes;
-  static constexpr int kStages = (kSmemBudget / kStage) > 8 ? 8 : (kSmemBudget / kStage);
+  static constexpr int kStages = (kSmemBudget / kStage) > 10 ? 10 : (kSmemBudget / kStage);
   static constexpr int kTmemCols = BN < 32 ? 32 : BN;
+  static constexpr int kRedStride = BN + 4;  // fp32 partial-tile row stride (floats) in smem
+  static_assert(kBM * kRedStride * 4 <= kStages * kStage, "partial tile must fit in the stage ring");
   static constexpr int kSmem = 1024 + kStages * kStage + 256;
 };
 
@@ -67,6 +102,101 @@ __device__ __forceinline__ bool lora_block_present(int j, int rank, uint32_t mas
 }
 
 __device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], bool relu) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float a0 = v[q * 8 + e * 2], a1 = v[q * 8 + e * 2 + 1];
+      if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
+      o[e] = __floats2bfloat162_rn(a0, a1);
+    }
+    *reinterpret_cast<int4*>(dst + q * 8) = *reinterpret_cast<int4*>(o);
+  }
+}
+
+// Epilogue work is cut into units of 32 (or paired 2x32) columns of one row.
+template <int BN>
+__device__ __forceinline__ int units_per_row(const GemmArgs& a, int n0) {
+  const int epi = a.epi & 15;
+  if (epi == kEpiRope && n0 < a.rope_cols) return (BN / a.head_dim) * (a.head_dim / 64);
+  if (epi == kEpiSwiglu) return (BN / 128) * 2;
+  return BN / 32;
+}
+
+// Emit one unit for `row`; fetch(c0, v) provides the 32 fp32 accumulators of tile columns [c0, c0+32).
+template <int BN, typename Fetch>
+__device__ __forceinline__ void emit_unit(const GemmArgs& a, int n0, int row, int u, Fetch&& fetch) {
+  const bool live = row < a.M;
+  const int epi = a.epi & 15;
+  if (epi == kEpiRope && n0 < a.rope_cols) {
+    // q/k heads: x1 = cols [i*32, +32), x2 = cols [half + i*32, +32) of the head; fp32 rotate, one rounding
+    const int D = a.head_dim, half = D / 2, per_head = half / 32;
+    const int hb = (u / per_head) * D, i = u % per_head;
+    float x1[32], x2[32];
+    fetch(hb + i * 32, x1);
+    fetch(hb + half + i * 32, x2);
+    if (!live) return;
+    const int pos = a.positions[row];
+    const float* cs = a.rope_cos + (int64_t)pos * half + i * 32;
+    const float* sn = a.rope_sin + (int64_t)pos * half + i * 32;
+    float r1[32], r2[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const float c = __ldg(cs + j), s = __ldg(sn + j);
+      r1[j] = x1[j] * c - x2[j] * s;
+      r2[j] = x2[j] * c + x1[j] * s;
+    }
+    __nv_bfloat16* d1 = static_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + n0 + hb + i * 32;
+    store_bf16x32(d1, r1, false);
+    store_bf16x32(d1 + half, r2, false);
+    return;
+  }
+  if (epi == kEpiSwiglu) {
+    // tile columns [c*128, +64) gate, [c*128+64, +64) up -> 64 outputs at column n0/2 + c*64
+    const int c = u / 2, h = u % 2;
+    float g[32], v[32];
+    fetch(c * 128 + h * 32, g);
+    fetch(c * 128 + 64 + h * 32, v);
+    if (!live) return;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) g[j] = silu(g[j]) * v[j];
+    store_bf16x32(static_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + n0 / 2 + c * 64 + h * 32, g, false);
+    return;
+  }
+  float v[32];
+  const int c0 = u * 32;
+  fetch(c0, v);
+  const int col = n0 + c0;
+  if (!live || col >= a.N) return;
+  if (epi == kEpiLoraSelect) {
+    const int slot = a.sel_row_slot[row];
+    const bool takes = slot >= 0 && a.sel_row_apply[row];
+    const int t = col / a.sel_sr, off = col % a.sel_sr;  // 32-col units never straddle a plane
+    const bool tgt = takes && ((a.sel_targets[slot] >> t) & 1u);
+#pragma unroll
+    for (int e = 0; e < 32; ++e)
+      if (!(tgt && (off + e) / a.sel_rank == slot)) v[e] = 0.f;
+    store_bf16x32(static_cast<__nv_bfloat16*>(a.C) + ((int64_t)t * a.M + row) * a.sel_sr + off, v, false);
+  } else if (epi == kEpiAdd) {
+    float* dst = static_cast<float*>(a.C) + (int64_t)row * a.ldc + col;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      float4 x = *reinterpret_cast<float4*>(dst + q * 4);
+      x.x += v[q * 4]; x.y += v[q * 4 + 1]; x.z += v[q * 4 + 2]; x.w += v[q * 4 + 3];
+      *reinterpret_cast<float4*>(dst + q * 4) = x;
+    }
+  } else if (a.epi & 16) {
+    float* dst = static_cast<float*>(a.C) + (int64_t)row * a.ldc + col;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      *reinterpret_cast<float4*>(dst + q * 4) = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
+  } else {
+    store_bf16x32(static_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + col, v, epi == kEpiRelu);
+  }
+}
 
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -83,11 +213,16 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m_tile = blockIdx.y, m0 = m_tile * kBM;
-  const int nkb = (args.K + kBK - 1) / kBK;
-  // LoRA range of this N tile
+  const int split = blockIdx.z;  // == cluster rank when splits > 1
+  const int S = args.splits;
+  if (threadIdx.x == 0) TRACE(0);
+  // this split's base K range (LoRA blocks ride with the last split)
+  const int nkb_all = (args.K + kBK - 1) / kBK;
+  const int per = (nkb_all + S - 1) / S;
+  const int kb0 = min(nkb_all, split * per), kb1 = min(nkb_all, kb0 + per);
   int target = 0, nkl = 0;
   uint32_t mask = 0;
-  if (args.ks > 0) {
+  if (args.ks > 0 && split == S - 1) {
     target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
     nkl = (args.ks + kBK - 1) / kBK;
     mask = args.tile_slot_mask[m_tile];
@@ -108,15 +243,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  int n_iters = kb1 - kb0;
+  for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
 
   if (warp == 0) {
     if (sm100::elect_one()) {
-      const uint64_t pol_act = sm100::policy_evict_last();   // activations: re-read by every N tile
-      const uint64_t pol_w = sm100::policy_evict_first();    // weights: streamed once per forward
+      const uint64_t pol_act = sm100::policy_evict_last();  // activations: re-read by every N tile
+      const uint64_t pol_w = sm100::policy_evict_first();   // weights: streamed once per forward
       int s = 0;
       uint32_t phase = 0;
       auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
-      for (int kb = 0; kb < nkb; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         sm100::mbar_wait(&empty[s], phase ^ 1);
         uint8_t* sa = smem + s * C::kStage;
         sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
@@ -140,9 +277,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       int s = 0;
       uint32_t phase = 0;
       uint32_t acc = 0;
-      auto consume = [&] {
+      for (int it = 0; it < n_iters; ++it) {
         sm100::mbar_wait(&full[s], phase);
         sm100::tc_fence_after();
+        if (it == 0) TRACE(1);
         const uint8_t* sa = smem + s * C::kStage;
         const uint64_t da = sm100::umma_desc_sw128(sa);
         const uint64_t db = sm100::umma_desc_sw128(sa + C::kABytes);
@@ -153,132 +291,100 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         sm100::mma_commit(&empty[s]);
         if (++s == C::kStages) { s = 0; phase ^= 1; }
-      };
-      for (int kb = 0; kb < nkb; ++kb) consume();
-      for (int j = 0; j < nkl; ++j)
-        if (lora_block_present(j, args.rank, mask)) consume();
+      }
       sm100::mma_commit(tmem_full);
     }
     __syncwarp();
   } else {
-    // epilogue: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
+    // epilogue warps: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
     const int quarter = warp & 3;
-    const int row = m0 + quarter * 32 + lane;
+    const int trow_idx = quarter * 32 + lane;
     sm100::mbar_wait(tmem_full, 0);
     sm100::tc_fence_after();
+    if (threadIdx.x == 64) TRACE(2);
     const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-    const int epi = args.epi & 15;
-    const bool out_f32 = (args.epi & 16) != 0;
-    const bool live = row < args.M;
-    if (epi == kEpiRope && n0 < args.rope_cols) {
-      // q/k heads: x1 = cols [i*32, +32), x2 = cols [half + i*32, +32) of each head; fp32 rotate, one bf16 rounding
-      const int D = args.head_dim, half = D / 2;
-      const int pos = live ? args.positions[row] : 0;
-      const float* cs = args.rope_cos + (int64_t)pos * half;
-      const float* sn = args.rope_sin + (int64_t)pos * half;
-      for (int hb = 0; hb < BN; hb += D) {
-        for (int i = 0; i < half / 32; ++i) {
-          uint32_t x1[32], x2[32];
-          sm100::tmem_ld_32x32b_x32(trow + hb + i * 32, x1);
-          sm100::tmem_ld_32x32b_x32(trow + hb + half + i * 32, x2);
-          sm100::tmem_ld_wait();
-          if (!live) continue;
-          __nv_bfloat16* d1 = static_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc + n0 + hb + i * 32;
-          __nv_bfloat16* d2 = d1 + half;
+    auto tmem_fetch = [&](int c0, float (&v)[32]) {  // warp-collective
+      uint32_t r[32];
+      sm100::tmem_ld_32x32b_x32(trow + c0, r);
+      sm100::tmem_ld_wait();
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            __align__(16) __nv_bfloat162 o1[4], o2[4];
+      for (int i = 0; i < 32; ++i) v[i] = n_iters > 0 ? __uint_as_float(r[i]) : 0.f;
+    };
+    const bool quarter_live = m0 + quarter * 32 < args.M;  // warp-uniform: skip all-padding lane quarters
+    if (S == 1) {
+      const int units = units_per_row<BN>(args, n0);
+      if (quarter_live)
+        for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, m0 + trow_idx, u, tmem_fetch);
+    } else if (quarter_live) {
+      // publish this split's fp32 partial rows (L2-resident workspace [S][m_tiles*128][N])
+      float* part = args.partial + ((int64_t)(split * gridDim.y + m_tile) * kBM + trow_idx) * args.N + n0;
+      const bool row_live = m0 + trow_idx < args.M;
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tmem_fetch(c, v);
+        if (!row_live) continue;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float r1[2], r2[2];
-#pragma unroll
-              for (int q = 0; q < 2; ++q) {
-                const int j = v * 8 + e * 2 + q;
-                const float c = __ldg(cs + i * 32 + j), s = __ldg(sn + i * 32 + j);
-                const float a = __uint_as_float(x1[j]), b = __uint_as_float(x2[j]);
-                r1[q] = a * c - b * s;
-                r2[q] = b * c + a * s;
-              }
-              o1[e] = __floats2bfloat162_rn(r1[0], r1[1]);
-              o2[e] = __floats2bfloat162_rn(r2[0], r2[1]);
-            }
-            *reinterpret_cast<int4*>(d1 + v * 8) = *reinterpret_cast<int4*>(o1);
-            *reinterpret_cast<int4*>(d2 + v * 8) = *reinterpret_cast<int4*>(o2);
-          }
-        }
+        for (int q = 0; q < 8; ++q)
+          __stcg(reinterpret_cast<float4*>(part + c + q * 4), make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]));
       }
-    } else if (epi == kEpiSwiglu) {
-      // tile columns [0,64) gate, [64,128) up -> 64 outputs at column n0/2
-      for (int c = 0; c < BN / 128; ++c) {
-        for (int h = 0; h < 2; ++h) {
-          uint32_t g[32], u[32];
-          sm100::tmem_ld_32x32b_x32(trow + c * 128 + h * 32, g);
-          sm100::tmem_ld_32x32b_x32(trow + c * 128 + 64 + h * 32, u);
-          sm100::tmem_ld_wait();
-          if (live) {
-            __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc + n0 / 2 + c * 64 + h * 32;
+    }
+  }
+  if (threadIdx.x == 64) TRACE(3);
+  if (S > 1 && warp >= 2) {
+    // all S splits of this tile are co-resident (cooperative launch, grid <= SM count): wait for every
+    // partial, then split k reduces rows [k*R/S, (k+1)*R/S) in split order and runs their epilogue
+    int* arrive = args.counters + 2 * (m_tile * gridDim.x + blockIdx.x);
+    __threadfence();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 64) {
+      atomicAdd(arrive, 1);
+      while (*reinterpret_cast<volatile int*>(arrive) < S) __nanosleep(32);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    __threadfence();
+    if (threadIdx.x == 64) TRACE(4);
+    const int valid_rows = min(kBM, args.M - m0);
+    const int r_beg = split * valid_rows / S, r_end = (split + 1) * valid_rows / S;
+    const int my_rows = r_end - r_beg;
+    float* red = reinterpret_cast<float*>(smem);  // [my_rows][kRedStride] in the idle stage ring
+    constexpr int G4 = BN / 4;
+    const int64_t pstride = (int64_t)gridDim.y * kBM * args.N;
+    for (int g = threadIdx.x - 64; g < my_rows * G4; g += kThreads - 64) {
+      const int rl = g / G4, c4 = (g % G4) * 4;
+      const float* src = args.partial + ((int64_t)m_tile * kBM + r_beg + rl) * args.N + n0 + c4;
+      float4 p[kMaxSplits];
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              __align__(16) __nv_bfloat162 o[4];
+      for (int k = 0; k < kMaxSplits; ++k)
+        if (k < S) p[k] = __ldcg(reinterpret_cast<const float4*>(src + k * pstride));
+      float4 acc = p[0];
 #pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const int i = v * 8 + e * 2;
-                const float a0 = silu(__uint_as_float(g[i])) * __uint_as_float(u[i]);
-                const float a1 = silu(__uint_as_float(g[i + 1])) * __uint_as_float(u[i + 1]);
-                o[e] = __floats2bfloat162_rn(a0, a1);
-              }
-              *reinterpret_cast<int4*>(dst + v * 8) = *reinterpret_cast<int4*>(o);
-            }
-          }
+      for (int k = 1; k < kMaxSplits; ++k)
+        if (k < S) { acc.x += p[k].x; acc.y += p[k].y; acc.z += p[k].z; acc.w += p[k].w; }
+      *reinterpret_cast<float4*>(red + rl * C::kRedStride + c4) = acc;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    const int units = units_per_row<BN>(args, n0);
+    for (int w = threadIdx.x - 64; w < my_rows * units; w += kThreads - 64) {
+      const int rl = w / units, u = w % units;
+      auto smem_fetch = [&](int c0, float (&v)[32]) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 t = *reinterpret_cast<const float4*>(red + rl * C::kRedStride + c0 + q * 4);
+          v[q * 4] = t.x; v[q * 4 + 1] = t.y; v[q * 4 + 2] = t.z; v[q * 4 + 3] = t.w;
         }
-      }
-    } else {
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        sm100::tmem_ld_32x32b_x32(trow + c * 32, r);
-        sm100::tmem_ld_wait();
-        if (!live) continue;
-        const int col = n0 + c * 32;
-        if (col >= args.N) continue;
-        if (epi == kEpiAdd) {
-          float* dst = static_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
-#pragma unroll
-          for (int v = 0; v < 8; ++v) {
-            float4 x = *reinterpret_cast<float4*>(dst + v * 4);
-            x.x += __uint_as_float(r[v * 4 + 0]);
-            x.y += __uint_as_float(r[v * 4 + 1]);
-            x.z += __uint_as_float(r[v * 4 + 2]);
-            x.w += __uint_as_float(r[v * 4 + 3]);
-            *reinterpret_cast<float4*>(dst + v * 4) = x;
-          }
-        } else if (out_f32) {
-          float* dst = static_cast<float*>(args.C) + (int64_t)row * args.ldc + col;
-#pragma unroll
-          for (int v = 0; v < 8; ++v)
-            *reinterpret_cast<float4*>(dst + v * 4) =
-                make_float4(__uint_as_float(r[v * 4]), __uint_as_float(r[v * 4 + 1]), __uint_as_float(r[v * 4 + 2]),
-                            __uint_as_float(r[v * 4 + 3]));
-        } else {
-          __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(args.C) + (int64_t)row * args.ldc + col;
-          const bool relu = epi == kEpiRelu;
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            __align__(16) __nv_bfloat162 o[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              float a0 = __uint_as_float(r[v * 8 + e * 2]), a1 = __uint_as_float(r[v * 8 + e * 2 + 1]);
-              if (relu) { a0 = fmaxf(a0, 0.f); a1 = fmaxf(a1, 0.f); }
-              o[e] = __floats2bfloat162_rn(a0, a1);
-            }
-            *reinterpret_cast<int4*>(dst + v * 8) = *reinterpret_cast<int4*>(o);
-          }
-        }
-      }
+      };
+      emit_unit<BN>(args, n0, m0 + r_beg + rl, u, smem_fetch);
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 64 && atomicAdd(arrive + 1, 1) == S - 1) {  // last one out resets for the next launch
+      arrive[0] = 0;
+      arrive[1] = 0;
     }
   }
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  if (threadIdx.x == 64) TRACE(5);
 }
 
 template <int BN>
@@ -292,24 +398,95 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, con
       return ALORA_ECUDA;
     configured = true;
   }
-  dim3 grid((args.N + BN - 1) / BN, (args.M + kBM - 1) / kBM);
-  gemm_bf16_kernel<BN><<<grid, kThreads, C::kSmem, st>>>(a, b, s, u, args);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((args.N + BN - 1) / BN, (args.M + kBM - 1) / kBM, args.splits);
+  cfg.blockDim = dim3(kThreads, 1, 1);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;  // split-K tiles spin-wait on each other: co-residency required
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = args.splits > 1 ? 1 : 0;
+  GemmArgs targs = args;
+  static unsigned long long* trace_buf = nullptr;
+  static const bool tracing = getenv("ALORA_GEMM_TRACE") != nullptr;
+  const int n_ctas = cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z;
+  if (tracing) {
+    if (!trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 6 * 65536);
+    cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
+    targs.trace = trace_buf;
+  }
+  if (cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN>, a, b, s, u, targs) != cudaSuccess) return ALORA_ECUDA;
   ALORA_LAUNCH_CHECK();
+  if (tracing) {  // phase timings relative to the earliest CTA start (debug only)
+    std::vector<unsigned long long> h(6 * n_ctas);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, tend = 0;
+    double ph[5] = {0, 0, 0, 0, 0};
+    for (int c = 0; c < n_ctas; ++c) {
+      t0 = std::min(t0, h[6 * c]);
+      tend = std::max(tend, h[6 * c + 5]);
+      for (int p = 0; p < 5; ++p)
+        if (h[6 * c + p + 1] && h[6 * c + p]) ph[p] += double(h[6 * c + p + 1] - h[6 * c + p]);
+    }
+    unsigned long long last_start = 0;
+    for (int c = 0; c < n_ctas; ++c) last_start = std::max(last_start, h[6 * c]);
+    fprintf(stderr,
+            "[gemm trace] M=%d N=%d K=%d BN=%d splits=%d ctas=%d span %.2f us, last CTA start +%.2f us; mean "
+            "setup->1st data %.2f, mainloop %.2f, epi %.2f, sync %.2f, reduce+exit %.2f us\n",
+            args.M, args.N, args.K, BN, args.splits, n_ctas, (tend - t0) / 1e3, (last_start - t0) / 1e3,
+            ph[0] / n_ctas / 1e3, ph[1] / n_ctas / 1e3, ph[2] / n_ctas / 1e3, ph[3] / n_ctas / 1e3,
+            ph[4] / n_ctas / 1e3);
+  }
   return ALORA_OK;
 }
 
 }  // namespace
 
+void configure_gemm() {
+  prefer_max_smem(gemm_bf16_kernel<32>);
+  prefer_max_smem(gemm_bf16_kernel<64>);
+  prefer_max_smem(gemm_bf16_kernel<128>);
+  prefer_max_smem(gemm_bf16_kernel<256>);
+}
+
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* Cout, int ldc, int M,
-              int N, int K, const GemmLora* lora, cudaStream_t st) {
+              int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws, int max_splits) {
   if (M == 0 || N == 0) return ALORA_OK;
   if (M < 0 || N < 0 || K < 1 || lda % 8 || ldb % 8 || ldc % 8) return ALORA_EINVAL;
   const int base_epi = epi & 15;
-  int BN = (N % 128 == 0) ? 128 : 64;
-  if (N % 64 != 0) return ALORA_EINVAL;
+  if (N % 32 != 0) return ALORA_EINVAL;
   if (base_epi == kEpiSwiglu && N % 128 != 0) return ALORA_EINVAL;
-  if (base_epi == kEpiSwiglu) BN = 128;
-  GemmArgs args{Cout, ldc, M, N, K, epi, 0, 1, 0, 0, nullptr, nullptr, nullptr, nullptr, 0, 0};
+  // Tile width: large M keeps 128 (256 for SwiGLU); small M (weight streaming, <= 2 row tiles) picks the
+  // widest BN that still gives ~one full wave of CTAs, so every SM streams weights without a K split.
+  const int m_tiles_ = (M + kBM - 1) / kBM;
+  int bn_min = 32;
+  if (base_epi == kEpiSwiglu) bn_min = 128;
+  if (base_epi == kEpiRope) bn_min = std::max(64, lora ? lora->head_dim : 64);
+  if (lora && lora->s && lora->ks > 0) {
+    while (bn_min < 128 && ((lora->n_q % bn_min) || (lora->n_kv % bn_min))) bn_min *= 2;
+  }
+  auto fits = [&](int bn) {
+    return bn >= bn_min && N % bn == 0 && (base_epi != kEpiSwiglu || bn % 128 == 0) &&
+           (!lora || !lora->s || lora->ks == 0 || ((lora->n_q % bn) == 0 && (lora->n_kv % bn) == 0)) &&
+           (base_epi != kEpiRope || (lora->rope_cols % bn == 0 && bn % lora->head_dim == 0));
+  };
+  int BN = 0;
+  if (m_tiles_ <= 2) {
+    for (int bn : {256, 128, 64, 32})
+      if (fits(bn) && m_tiles_ * (N / bn) >= (kNumSMs * 3) / 4) { BN = bn; break; }
+    if (BN == 0)
+      for (int bn : {32, 64, 128, 256})
+        if (fits(bn)) { BN = bn; break; }
+  } else {
+    for (int bn : {base_epi == kEpiSwiglu ? 256 : 128, 128, 64, 32})
+      if (fits(bn)) { BN = bn; break; }
+  }
+  if (BN == 0) return ALORA_EINVAL;
+  GemmArgs args{};
+  args.C = Cout; args.ldc = ldc; args.M = M; args.N = N; args.K = K; args.epi = epi; args.rank = 1; args.splits = 1;
   if (base_epi == kEpiRope) {
     if (!lora || !lora->positions || !lora->rope_cos || !lora->rope_sin || lora->head_dim < 64 ||
         lora->head_dim % 64 || lora->rope_cols % BN || BN % lora->head_dim)
@@ -319,6 +496,16 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.rope_sin = lora->rope_sin;
     args.rope_cols = lora->rope_cols;
     args.head_dim = lora->head_dim;
+  }
+  if (base_epi == kEpiLoraSelect) {
+    if (!lora || !lora->sel_row_slot || !lora->sel_row_apply || !lora->sel_targets || lora->sel_sr % 32 ||
+        lora->sel_rank < 1 || N != 3 * lora->sel_sr)
+      return ALORA_EINVAL;
+    args.sel_row_slot = lora->sel_row_slot;
+    args.sel_row_apply = lora->sel_row_apply;
+    args.sel_targets = lora->sel_targets;
+    args.sel_sr = lora->sel_sr;
+    args.sel_rank = lora->sel_rank;
   }
   CUtensorMap ta, tb, ts, tu;
   if (!make_tmap_2d(&ta, A, M, K, lda, kBM, kBK)) return ALORA_ECUDA;
@@ -335,7 +522,35 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.n_kv = lora->n_kv;
     args.tile_slot_mask = lora->tile_slot_mask;
   }
-  return BN == 128 ? launch<128>(ta, tb, ts, tu, args, st) : launch<64>(ta, tb, ts, tu, args, st);
+  // split K when the tile grid cannot fill the machine (weight-streaming small-M launches): the largest
+  // split count with tiles * splits <= 148 (one co-resident CTA per SM) and >= 4 K-blocks per split
+  const int m_tiles = (M + kBM - 1) / kBM;
+  const int tiles = m_tiles * (N / BN);
+  const int nkb = (K + kBK - 1) / kBK;
+  int splits = 1;
+  if (ws != nullptr && ws->partial != nullptr && tiles * 2 <= kNumSMs) {
+    splits = std::min({max_splits, kMaxSplits, kNumSMs / tiles, nkb / 4});
+    splits = std::max(1, splits);
+    const int per = (nkb + splits - 1) / splits;
+    splits = (nkb + per - 1) / per;  // no empty trailing splits
+    if ((int64_t)splits * m_tiles * kBM * N * 4 > ws->partial_bytes || 2 * tiles > ws->n_counters) splits = 1;
+  }
+  args.splits = splits;
+  if (splits > 1) {
+    args.partial = static_cast<float*>(ws->partial);
+    args.counters = ws->counters;
+  }
+  switch (BN) {
+    case 256: return launch<256>(ta, tb, ts, tu, args, st);
+    case 128: return launch<128>(ta, tb, ts, tu, args, st);
+    case 64: return launch<64>(ta, tb, ts, tu, args, st);
+    default: return launch<32>(ta, tb, ts, tu, args, st);
+  }
+}
+
+int64_t gemm_bf16_workspace_bytes() {
+  // splits * m_tiles <= 148 partial tile rows of 128 x N(<= 148 * 128 cols per split group) fp32, plus counters
+  return (int64_t)kNumSMs * kBM * 128 * 4 + (int64_t)kGemmCounters * 4;
 }
 
 }  // namespace alora

@@ -7,7 +7,14 @@
 
 namespace alora {
 
-enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3, kEpiRope = 4 };
+// One-time kernel attribute setup (shared-memory carveout, dynamic smem limits); idempotent.
+void configure_kernels();
+void configure_bf16_ops();
+void configure_kv_ops();
+void configure_attention();
+void configure_gemm();
+
+enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3, kEpiRope = 4, kEpiLoraSelect = 5 };
 
 // ---- fp32 storage / fp64 accumulation (parity tier), parity_f64.cu
 int embed_f32(const int32_t* tokens, const int32_t* positions, const float* embed, const float* pos_table, int M,
@@ -45,7 +52,8 @@ int rope_bf16(__nv_bfloat16* qkv, int ld, const int32_t* positions, int M, int H
 int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int32_t* cu_q,
               const int32_t* start_pos, const int32_t* block_table, int max_blocks, int max_q, int max_ctx,
               const __nv_bfloat16* kv, int n_layers, int layer, int B, int H, int Hkv, int D,
-              __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes, cudaStream_t st);
+              __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes, cudaStream_t st,
+              int total_blocks = 0 /* > 0 enables the TMA / tcgen05 kernel */);
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D);
 int64_t attn_bf16_workspace_bound(int H, int D);
 
@@ -63,9 +71,38 @@ struct GemmLora {
   const float* rope_sin = nullptr;
   int rope_cols = 0;
   int head_dim = 0;
+  // kEpiLoraSelect (the shrink as a GEMM over all adapters' stacked down rows): column c of [M, 3*SR]
+  // is (t = c / SR, slot = (c % SR) / rank); it is kept only where the row takes slot's delta and slot
+  // targets t, and stored to the 3-plane shrink layout C[t][m][c % SR]; everything else is written 0.
+  const int32_t* sel_row_slot = nullptr;
+  const uint8_t* sel_row_apply = nullptr;
+  const uint8_t* sel_targets = nullptr;
+  int sel_sr = 0;
+  int sel_rank = 0;
 };
+// Split-K scratch: fp32 partial rows + 2 arrival counters per output tile (zeroed once, self-resetting).
+constexpr int kGemmCounters = 16384;
+struct GemmWs {
+  void* partial = nullptr;
+  int64_t partial_bytes = 0;
+  int* counters = nullptr;
+  int n_counters = 0;
+};
+int64_t gemm_bf16_workspace_bytes();
+// Carves a GemmWs out of a caller buffer of gemm_bf16_workspace_bytes() bytes (counters at the end).
+inline GemmWs gemm_ws_from(void* base, int64_t bytes) {
+  GemmWs w;
+  if (base == nullptr || bytes < gemm_bf16_workspace_bytes()) return w;
+  w.n_counters = kGemmCounters;
+  w.partial = base;
+  w.partial_bytes = bytes - (int64_t)kGemmCounters * 4;
+  w.counters = reinterpret_cast<int*>(static_cast<char*>(base) + w.partial_bytes);
+  return w;
+}
+// ws enables split-K (max_splits caps it) when the output tiles cannot fill the 148 SMs.
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* C, int ldc,
-              int M, int N, int K, const GemmLora* lora, cudaStream_t st);
+              int M, int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws = nullptr,
+              int max_splits = 8);
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st);
 
 }  // namespace alora

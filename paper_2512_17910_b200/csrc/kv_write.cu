@@ -114,6 +114,12 @@ __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32
   }
 }
 
+void configure_kv_ops() {
+  prefer_max_smem(kv_write_vec_kernel);
+  prefer_max_smem(kv_write_scalar_kernel);
+  prefer_max_smem(argmax_kernel);
+}
+
 int argmax_rows(const float* logits, int rows, int vocab, int32_t* out_ids, cudaStream_t st) {
   if (rows == 0) return ALORA_OK;
   if (vocab <= 0) return ALORA_EINVAL;

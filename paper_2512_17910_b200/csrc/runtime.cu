@@ -7,6 +7,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <new>
 #include <vector>
 
@@ -14,6 +15,18 @@
 #include "kernels.h"
 
 using namespace alora;
+
+namespace alora {
+void configure_kernels() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    configure_bf16_ops();
+    configure_kv_ops();
+    configure_attention();
+    configure_gemm();
+  });
+}
+}  // namespace alora
 
 namespace {
 
@@ -74,8 +87,8 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Workspace carve-up shared by alora_model_workspace_bytes and the executor.
 struct Ws {
-  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, total;
-  int64_t attn_ws_bytes;
+  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, total;
+  int64_t attn_ws_bytes, gemm_ws_bytes;
 };
 
 Ws plan_ws(const AloraModelDesc& d) {
@@ -100,6 +113,8 @@ Ws plan_ws(const AloraModelDesc& d) {
                         ? attn_bf16_workspace_bound(d.n_heads, d.head_dim)
                         : 0;
   w.attn_ws = take(w.attn_ws_bytes);
+  w.gemm_ws_bytes = d.dtype == ALORA_BF16 ? gemm_bf16_workspace_bytes() : 0;
+  w.gemm_ws = take(w.gemm_ws_bytes);  // split-K counters must start zeroed: the caller zero-fills the workspace
   w.total = off;
   return w;
 }
@@ -117,6 +132,22 @@ int validate(const AloraModelDesc* d) {
   if (d->n_slots < 0 || d->lora_rank < 0 || (d->n_slots > 0 && d->lora_rank < 1)) return ALORA_EINVAL;
   if (d->dtype == ALORA_BF16 && d->n_slots > 32) return ALORA_EINVAL;  // tile slot masks are 32-bit
   return ALORA_OK;
+}
+
+// LoRA shrink for every row against all adapters' stacked down rows [3*SR, K] on the tensor cores, with the
+// per-row slot/target select in the epilogue; the SIMT segmented kernel covers SR that is not a multiple of 64.
+int shrink(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+           const __nv_bfloat16* down, int n_slots, int R, const uint8_t* targets, __nv_bfloat16* s, cudaStream_t st,
+           const GemmWs* gw) {
+  const int SR = n_slots * R;
+  if (SR % 64 != 0) return lora_shrink_bf16(h, M, K, row_slot, row_apply, down, n_slots, R, targets, s, st);
+  GemmLora g;
+  g.sel_row_slot = row_slot;
+  g.sel_row_apply = row_apply;
+  g.sel_targets = targets;
+  g.sel_sr = SR;
+  g.sel_rank = R;
+  return gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, 3 * SR, K, &g, st, gw);
 }
 
 int forward_f32(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
@@ -191,6 +222,8 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   auto* masks = reinterpret_cast<uint32_t*>(base + w.masks);
   auto* hf = reinterpret_cast<__nv_bfloat16*>(base + w.hf);
   void* aws = base + w.attn_ws;
+  const GemmWs gws = gemm_ws_from(base + w.gemm_ws, w.gemm_ws_bytes);
+  const GemmWs* gw = &gws;  // split-K scratch for weight-streaming (small-M) GEMMs
   const int M = s.n_tokens, S = s.n_seqs, dm = d.d_model, F = d.ffn_dim;
   const int H = d.n_heads, Hkv = d.n_kv_heads, D = d.head_dim;
   const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
@@ -215,10 +248,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     GemmLora gl;
     if (lora) {
-      RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * d.n_slots * d.lora_rank * dm_ * 2 + 3.0 * m_ * ks_ * 2,
-          2.0 * 3 * m_ * d.lora_rank * dm_,
-          lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
-                           d.n_slots, d.lora_rank, d.slot_targets, sws, st));
+      RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
+          shrink(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]), d.n_slots,
+                 d.lora_rank, d.slot_targets, sws, st, gw));
       gl.s = sws;
       gl.up_t = static_cast<const __nv_bfloat16*>(mdl.lora_up_t[l]);
       gl.ks = d.n_slots * d.lora_rank;
@@ -236,30 +268,30 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     }
     RUN("gemm_qkv", gemm_bytes(m_, Nqkv_, dm_, 2, false) + (lora ? 2.0 * Nqkv_ * ks_ : 0.0), 2.0 * m_ * Nqkv_ * dm_,
         gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
-                  Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st));
+                  Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st, gw));
     RUN("kv_write", 2.0 * 2 * m_ * Nkv * 2, 0,
         kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                  d.block_size, st));
     RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
         attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
                   static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
-                  aws, w.attn_ws_bytes, st));
+                  aws, w.attn_ws_bytes, st, d.total_blocks));
     RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
         gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq, nullptr,
-                  st));
+                  st, gw));
     RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
     const double n_in = llama ? 2 * F_ : F_;
     RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2, 2.0 * m_ * n_in * dm_,
         gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act, F,
-                  M, llama ? 2 * F : F, dm, nullptr, st));
+                  M, llama ? 2 * F : F, dm, nullptr, st, gw));
     RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true), 2.0 * m_ * dm_ * F_,
         gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
-                  st));
+                  st, gw));
   }
   RUN("rmsnorm", S_ * dm_ * 6, 0, rmsnorm_bf16(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
   RUN("gemm_lm_head", gemm_bytes(S_, V_, dm_, 4, false), 2.0 * S_ * V_ * dm_,
       gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm, s.logits,
-                d.vocab, S, d.vocab, dm, nullptr, st));
+                d.vocab, S, d.vocab, dm, nullptr, st, gw));
   RUN("argmax", S_ * V_ * 4, 0, argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
 #undef RUN
   mdl.last_launches = run.n;
@@ -283,6 +315,7 @@ int alora_qkv_proj(int32_t dtype, const void* x, int32_t M, int32_t K, const voi
   if (!x || !w_qkv_t || !out) return ALORA_EINVAL;
   const bool lora = n_slots > 0 && rank > 0 && lora_down && lora_up_t && row_slot && row_apply && slot_targets && s_ws;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  configure_kernels();
   const int N = Nq + 2 * Nkv;
   int rc;
   if (dtype == ALORA_F32) {
@@ -302,8 +335,8 @@ int alora_qkv_proj(int32_t dtype, const void* x, int32_t M, int32_t K, const voi
     auto* masks = reinterpret_cast<uint32_t*>(sws + align_up(3LL * M * n_slots * rank, 128));
     rc = lora_tile_masks(row_slot, row_apply, M, masks, st);
     if (rc != ALORA_OK) return rc;
-    rc = lora_shrink_bf16(static_cast<const __nv_bfloat16*>(x), M, K, row_slot, row_apply,
-                          static_cast<const __nv_bfloat16*>(lora_down), n_slots, rank, slot_targets, sws, st);
+    rc = shrink(static_cast<const __nv_bfloat16*>(x), M, K, row_slot, row_apply,
+                static_cast<const __nv_bfloat16*>(lora_down), n_slots, rank, slot_targets, sws, st, nullptr);
     if (rc != ALORA_OK) return rc;
     gl.s = sws;
     gl.up_t = static_cast<const __nv_bfloat16*>(lora_up_t);
@@ -322,6 +355,7 @@ int alora_kv_write(int32_t dtype, const void* k, const void* v, int64_t ld_src, 
                    void* stream) {
   if (dtype != ALORA_F32 && dtype != ALORA_BF16) return ALORA_EINVAL;
   if (M > 0 && (!k || !v || !slot_mapping || !kv_pool)) return ALORA_EINVAL;
+  configure_kernels();
   return kv_write(dtype, k, v, ld_src, slot_mapping, M, kv_width, kv_pool, n_layers, layer, block_size,
                   static_cast<cudaStream_t>(stream));
 }
@@ -329,15 +363,16 @@ int alora_kv_write(int32_t dtype, const void* k, const void* v, int64_t ld_src, 
 int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t n_rows, int32_t n_seqs,
                              const int32_t* cu_q, const int32_t* start_pos, const int32_t* block_table,
                              int32_t max_blocks, int32_t max_q, int32_t max_ctx, const void* kv_pool,
-                             int32_t n_layers, int32_t layer, int32_t block_size, int32_t n_heads,
-                             int32_t n_kv_heads, int32_t head_dim, void* out, int64_t ld_out, void* workspace,
-                             int64_t workspace_bytes, void* stream) {
+                             int32_t total_blocks, int32_t n_layers, int32_t layer, int32_t block_size,
+                             int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, void* out, int64_t ld_out,
+                             void* workspace, int64_t workspace_bytes, void* stream) {
   if (n_seqs < 0 || n_rows < 0 || n_heads < 1 || n_kv_heads < 1 || n_heads % n_kv_heads || head_dim < 1 ||
       block_size < 1 || layer < 0 || layer >= n_layers || max_blocks < 1)
     return ALORA_EINVAL;
   if (n_seqs == 0 || n_rows == 0) return ALORA_OK;
   if (!q || !cu_q || !start_pos || !block_table || !kv_pool || !out) return ALORA_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  configure_kernels();
   if (dtype == ALORA_F32)
     return attn_f64(static_cast<const float*>(q), ld_q, n_rows, n_seqs, cu_q, start_pos, block_table, max_blocks,
                     static_cast<const float*>(kv_pool), n_layers, layer, block_size, n_heads, n_kv_heads, head_dim,
@@ -348,7 +383,7 @@ int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t
   return attn_bf16(static_cast<const __nv_bfloat16*>(q), ld_q, n_rows, n_seqs, cu_q, start_pos, block_table,
                    max_blocks, max_q, max_ctx, static_cast<const __nv_bfloat16*>(kv_pool), n_layers, layer,
                    block_size, n_heads, n_kv_heads, head_dim, static_cast<__nv_bfloat16*>(out), ld_out, workspace,
-                   workspace_bytes, st);
+                   workspace_bytes, st, total_blocks);
 }
 
 int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs, int32_t max_q, int32_t max_ctx,
@@ -358,15 +393,20 @@ int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs
 }
 
 int alora_gemm_bf16(int32_t epi, const void* A, int32_t lda, const void* Bt, int32_t ldb, void* C, int32_t ldc,
-                    int32_t M, int32_t N, int32_t K, void* stream) {
+                    int32_t M, int32_t N, int32_t K, void* workspace, int64_t workspace_bytes, void* stream) {
   if (!A || !Bt || !C) return ALORA_EINVAL;
   if (epi != kEpiStore && epi != kEpiAdd && epi != kEpiRelu && epi != kEpiSwiglu && epi != 16) return ALORA_EINVAL;
+  configure_kernels();
+  const GemmWs ws = gemm_ws_from(workspace, workspace_bytes);
   return gemm_bf16(epi, static_cast<const __nv_bfloat16*>(A), lda, static_cast<const __nv_bfloat16*>(Bt), ldb, C,
-                   ldc, M, N, K, nullptr, static_cast<cudaStream_t>(stream));
+                   ldc, M, N, K, nullptr, static_cast<cudaStream_t>(stream), ws.partial ? &ws : nullptr);
 }
+
+int64_t alora_gemm_workspace_bytes(void) { return gemm_bf16_workspace_bytes(); }
 
 int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_ids, void* stream) {
   if (rows < 0) return ALORA_EINVAL;
+  configure_kernels();
   return argmax_rows(logits, rows, vocab, out_ids, static_cast<cudaStream_t>(stream));
 }
 
@@ -378,6 +418,7 @@ int64_t alora_model_workspace_bytes(const AloraModelDesc* desc) {
 int alora_model_create(const AloraModelDesc* desc, void** out_handle) {
   int rc = validate(desc);
   if (rc != ALORA_OK || !out_handle) return ALORA_EINVAL;
+  configure_kernels();
   Model* m = new (std::nothrow) Model();
   if (!m) return ALORA_ECUDA;
   m->d = *desc;

@@ -226,6 +226,8 @@ class Model:
         rank = max(a.rank for _, a in self._adapters.values())
         if cfg.dtype == "bf16":
             rank = -(-rank // 8) * 8  # 16-byte rows for the vector loads / TMA
+            while (n * rank) % 64:  # shrink runs as a tcgen05 GEMM over [3 * n * rank] stacked rows
+                n += 1
         if n > 32 and cfg.dtype == "bf16":
             raise ValueError("the bf16 tier supports at most 32 adapters per model")
         widths = {"q": cfg.q_width, "k": cfg.kv_width, "v": cfg.kv_width}
@@ -265,7 +267,7 @@ class Model:
         nbytes = _native.lib.alora_model_workspace_bytes(ctypes.byref(desc))
         if nbytes < 0:
             raise ValueError("invalid model description")
-        self._ws = self._torch.empty(int(nbytes), dtype=self._torch.uint8, device="cuda")
+        self._ws = self._torch.zeros(int(nbytes), dtype=self._torch.uint8, device="cuda")  # split-K counters = 0
         self._handle_key = None
 
     def _ptr_array(self, tensors):
@@ -311,7 +313,7 @@ class Model:
         self._keep = []
         need = _native.lib.alora_model_workspace_bytes(ctypes.byref(self._desc(kv=None, probe=True)))
         if need > self._ws.numel():  # the adapter bank grew: the LoRA workspace grows with it
-            self._ws = self._torch.empty(int(need), dtype=self._torch.uint8, device="cuda")
+            self._ws = self._torch.zeros(int(need), dtype=self._torch.uint8, device="cuda")
             key = (kv.data_ptr(), tuple(kv.shape), self._ws.data_ptr(), self._bank_version)
         desc = self._desc(kv)
         h = ctypes.c_void_p()
@@ -593,9 +595,9 @@ def paged_attention(q, kv, layer: int, block_ids, fresh_k, fresh_v, start_pos: i
     bt = t.arange(need, dtype=t.int32, device="cuda")
     dt = _native.ALORA_BF16 if dtype == t.bfloat16 else _native.ALORA_F32
     wsb = _native.lib.alora_attn_workspace_bytes(dt, n, 1, n, total, n_heads, hkv, D)
-    ws = t.empty(max(int(wsb), 1), dtype=t.uint8, device="cuda")
+    ws = t.zeros(max(int(wsb), 1), dtype=t.uint8, device="cuda")  # split-KV merge counters start at 0
     rc = _native.lib.alora_paged_prefill_attn(dt, qt.data_ptr(), qt.shape[1], n, 1, cu.data_ptr(), sp.data_ptr(),
-                                              bt.data_ptr(), need, n, total, scratch.data_ptr(), 1, 0, B, n_heads,
+                                              bt.data_ptr(), need, n, total, scratch.data_ptr(), need, 1, 0, B, n_heads,
                                               hkv, D, out.data_ptr(), out.shape[1], ws.data_ptr(), ws.numel(),
                                               ctypes.c_void_p(t.cuda.current_stream().cuda_stream))
     _native.check(rc, "alora_paged_prefill_attn")

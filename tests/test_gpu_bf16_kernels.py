@@ -27,11 +27,46 @@ def _bf(shape, gen, scale=1.0):
     return (torch.randn(shape, generator=gen, device="cuda") * scale).to(torch.bfloat16)
 
 
-def gemm(epi, A, Bt, C, M, N, K):
+_WS = {}
+
+
+def gemm(epi, A, Bt, C, M, N, K, split=False):
+    ws = None
+    if split:
+        if "ws" not in _WS:
+            _WS["ws"] = torch.zeros(lib.alora_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
+        ws = _WS["ws"]
     rc = lib.alora_gemm_bf16(epi, A.data_ptr(), A.shape[1], Bt.data_ptr(), Bt.shape[1], C.data_ptr(), C.shape[1],
-                             M, N, K, _stream())
+                             M, N, K, None if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                             _stream())
     _native.check(rc, "alora_gemm_bf16")
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 2048, 8192), (48, 3072, 2048), (240, 2048, 2048), (130, 1024, 4096)])
+def test_gemm_split_k_deterministic_and_correct(M, N, K):
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A, Bt = _bf((M, K), g), _bf((N, K), g, 0.05)
+    ref = A.double() @ Bt.double().T
+    mag = A.double().abs() @ Bt.double().abs().T
+    outs = []
+    for _ in range(2):
+        C = torch.full((M, N), float("nan"), device="cuda")
+        gemm(16, A, Bt, C, M, N, K, split=True)
+        outs.append(C)
+    assert torch.equal(outs[0], outs[1])  # fixed split order: bitwise repeatable
+    assert ((outs[0].double() - ref).abs() / (mag + 1e-6)).max().item() < 1e-5
+    X = torch.randn((M, N), generator=g, device="cuda")
+    X0 = X.clone()
+    gemm(1, A, Bt, X, M, N, K, split=True)  # residual add epilogue through the split reduction
+    assert ((X.double() - X0.double() - ref).abs() / (mag + 1.0)).max().item() < 1e-5
+    if N % 128 == 0:
+        Sg = torch.empty((M, N // 2), device="cuda", dtype=torch.bfloat16)
+        gemm(3, A, Bt, Sg, M, N, K, split=True)
+        r = ref.view(M, N // 128, 2, 64)
+        gate, up = r[:, :, 0, :].reshape(M, N // 2), r[:, :, 1, :].reshape(M, N // 2)
+        np.testing.assert_allclose(Sg.float().cpu().numpy(), (gate * torch.sigmoid(gate) * up).float().cpu().numpy(),
+                                   rtol=2e-2, atol=2e-2)
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (5, 128, 256), (128, 256, 512), (200, 384, 1000), (1000, 512, 2048),

@@ -74,10 +74,10 @@ def test_paged_attention_bf16_vs_dense(H, Hkv, D, B, starts, lens):
     d_bt = torch.as_tensor(bt).cuda()
     max_q, max_ctx = max(lens), max(s + l for s, l in zip(starts, lens))
     wsb = _native.lib.alora_attn_workspace_bytes(_native.ALORA_BF16, M, n, max_q, max_ctx, H, Hkv, D)
-    ws = torch.empty(max(int(wsb), 1), dtype=torch.uint8, device="cuda")
+    ws = torch.zeros(max(int(wsb), 1), dtype=torch.uint8, device="cuda")
     rc = _native.lib.alora_paged_prefill_attn(
         _native.ALORA_BF16, q.data_ptr(), q.shape[1], M, n, d_cu.data_ptr(), d_sp.data_ptr(), d_bt.data_ptr(), maxb,
-        max_q, max_ctx, dev_pool.data_ptr(), 2, 1, B, H, Hkv, D, out.data_ptr(), out.shape[1], ws.data_ptr(),
+        max_q, max_ctx, dev_pool.data_ptr(), dev_pool.shape[0], 2, 1, B, H, Hkv, D, out.data_ptr(), out.shape[1], ws.data_ptr(),
         ws.numel(), ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
     _native.check(rc, "alora_paged_prefill_attn")
     got = out.float().cpu().numpy()
