@@ -400,7 +400,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (a.trace) a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 6 + (slot)] = gtimer(); \
   } while (0)
 
-constexpr int kNS = 4;          // K/V stages
+// K/V ring depth: D=64 keeps the CTA at ~98 KB of smem so two CTAs (two independent softmax chains) share an SM
+template <int D>
+constexpr int kNS = D == 64 ? 3 : 4;
 constexpr int kThreads = 192;   // 4 softmax + 1 producer + 1 MMA warps
 constexpr float kRescaleLog2 = 8.f;
 
@@ -411,8 +413,8 @@ struct Smem {
   static constexpr int kPBytes = kQT * kKT * 2;      // [128][64]
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;
-  static constexpr int kV = kK + kNS * kKVBytes;
-  static constexpr int kP = kV + kNS * kKVBytes;
+  static constexpr int kV = kK + kNS<D> * kKVBytes;
+  static constexpr int kP = kV + kNS<D> * kKVBytes;
   static constexpr int kBar = kP + 2 * kPBytes;
   static constexpr int kTotal = kBar + 256 + 1024;  // barriers + TMEM slot + alignment slack
 };
@@ -423,16 +425,16 @@ __device__ __forceinline__ uint32_t sw_off(int row, int c, int rows) {
 }
 
 template <int D>
-__global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
+__global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(const AttnArgs a,
                                                               const __grid_constant__ CUtensorMap tm_kv) {
   using L = Smem<D>;
   extern __shared__ uint8_t smem_raw_tc[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_tc) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kBar);
   uint64_t* q_full = bars;             // 1
-  uint64_t* kv_full = bars + 1;        // kNS
-  uint64_t* kv_empty = kv_full + kNS;  // kNS
-  uint64_t* s_full = kv_empty + kNS;   // 2
+  uint64_t* kv_full = bars + 1;        // kNS<D>
+  uint64_t* kv_empty = kv_full + kNS<D>;  // kNS<D>
+  uint64_t* s_full = kv_empty + kNS<D>;   // 2
   uint64_t* p_full = s_full + 2;       // 2
   uint64_t* pv_done = p_full + 2;      // 2
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
@@ -459,7 +461,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
   constexpr int CH = D / 8;
   if (tid == 0) {
     sm100::mbar_init(q_full, 32);
-    for (int i = 0; i < kNS; ++i) {
+    for (int i = 0; i < kNS<D>; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
     }
@@ -475,6 +477,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // q, the block table and this layer's fresh K/V rows come from the kernels before
+  pdl_trigger();
   const uint32_t tS[2] = {tmem, tmem + 64};
   const uint32_t tO = tmem + 128;
 
@@ -499,8 +503,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
       const int per_tile = kKT / a.B;
       const uint64_t pol = sm100::policy_evict_last();  // prefix blocks are shared by requests of the step
       for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % kNS;
-        if (t >= kNS) sm100::mbar_wait(&kv_empty[st], ((t / kNS) - 1) & 1);
+        const int st = t % kNS<D>;
+        if (t >= kNS<D>) sm100::mbar_wait(&kv_empty[st], ((t / kNS<D>) - 1) & 1);
         sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
         uint8_t* dk = sm + L::kK + st * L::kKVBytes;
         uint8_t* dv = sm + L::kV + st * L::kKVBytes;
@@ -528,8 +532,8 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
       ATTN_TRACE(1);
       sm100::tc_fence_after();
       auto issue_s = [&](int t) {
-        const int st = t % kNS;
-        sm100::mbar_wait(&kv_full[st], (t / kNS) & 1);
+        const int st = t % kNS<D>;
+        sm100::mbar_wait(&kv_full[st], (t / kNS<D>) & 1);
         sm100::tc_fence_after();
         const uint8_t* qb = sm + L::kQ;
         const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
@@ -547,7 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
         sm100::mbar_wait(&p_full[t & 1], (t >> 1) & 1);
         sm100::tc_fence_after();
         const uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
-        const uint8_t* vb = sm + L::kV + (t % kNS) * L::kKVBytes;
+        const uint8_t* vb = sm + L::kV + (t % kNS<D>) * L::kKVBytes;
 #pragma unroll
         for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
           const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
@@ -555,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
           sm100::mma_bf16_ss(tO, da, db, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
         }
         sm100::mma_commit(&pv_done[t & 1]);
-        sm100::mma_commit(&kv_empty[t % kNS]);
+        sm100::mma_commit(&kv_empty[t % kNS<D>]);
       }
     }
     __syncwarp();
@@ -685,14 +689,17 @@ __global__ void __launch_bounds__(kThreads, 1) attn_tc_kernel(const AttnArgs a,
 
 }  // namespace tc
 
-// Partition plan shared by the workspace query and the launch.
-void plan(int n_seqs, int max_q, int max_ctx, int H, int Hkv, int& part_size, int& n_parts, int& n_qtiles) {
+// Partition plan shared by the workspace query and the launch. When the step has fewer work items than
+// resident CTA slots (aLoRA suffix turns, decode) the keys are split so that all partitions run in ONE wave:
+// a second wave would double the per-CTA fixed cost (setup, Q load, merge) on the critical path.
+void plan(int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D, int& part_size, int& n_parts, int& n_qtiles) {
   const int G = H / Hkv;
   n_qtiles = (max_q * G + kQT - 1) / kQT;
   const int64_t items = (int64_t)n_qtiles * n_seqs * Hkv;
+  const int slots = D == 64 ? kTargetCtas : kNumSMs;  // resident tcgen05 CTAs (smem/TMEM bound)
   const int max_parts = (max_ctx + kMinPartKeys - 1) / kMinPartKeys;
   int np = 1;
-  if (items < kTargetCtas && items <= kMaxCounters) np = (int)((kTargetCtas + items - 1) / items);
+  if (items < slots && items <= kMaxCounters) np = (int)(slots / items);
   np = std::max(1, std::min({np, max_parts, kMaxParts}));
   int ps = (max_ctx + np - 1) / np;
   ps = (ps + kKT - 1) / kKT * kKT;
@@ -735,7 +742,7 @@ int launch_attn(const AttnArgs& a, int n_seqs, int64_t kv_rows, cudaStream_t st)
       cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
       ta.trace = tbuf;
     }
-    tc::attn_tc_kernel<D><<<grid, tc::kThreads, smem, st>>>(ta, tm);
+    ALORA_CUDA_CHECK(launch_pdl(tc::attn_tc_kernel<D>, grid, dim3(tc::kThreads), smem, st, nullptr, 0, ta, tm));
     if (tracing) {  // debug: per-phase means over the CTAs that ran (early-exit CTAs have no stamps)
       std::vector<unsigned long long> h(6 * n_ctas);
       cudaStreamSynchronize(st);
@@ -779,7 +786,7 @@ int64_t attn_bf16_workspace_bound(int H, int D) {
 
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D) {
   int ps, np, nq;
-  plan(n_seqs, max_q, max_ctx, H, Hkv, ps, np, nq);
+  plan(n_seqs, max_q, max_ctx, H, Hkv, D, ps, np, nq);
   if (np <= 1) return 0;
   return (int64_t)np * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
 }
@@ -795,7 +802,7 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
   a.max_blocks = max_blocks; a.kv = kv; a.n_layers = n_layers; a.layer = layer; a.B = B; a.H = H; a.Hkv = Hkv;
   a.D = D; a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   a.out = out; a.ld_out = ld_out; a.M = M;
-  plan(n_seqs, max_q, max_ctx, H, Hkv, a.part_size, a.n_parts, a.n_qtiles);
+  plan(n_seqs, max_q, max_ctx, H, Hkv, D, a.part_size, a.n_parts, a.n_qtiles);
   if (a.n_parts > 1) {
     const int64_t need = (int64_t)a.n_parts * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
     if (ws == nullptr || ws_bytes < need) return ALORA_EINVAL;

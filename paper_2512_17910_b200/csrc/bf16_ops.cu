@@ -12,6 +12,8 @@ namespace alora {
 __global__ void embed_bf16_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
                                   const __nv_bfloat16* __restrict__ embed, const float* __restrict__ pos_table, int d,
                                   float* __restrict__ x) {
+  pdl_wait();
+  pdl_trigger();
   const int m = blockIdx.x;
   const __nv_bfloat16* e = embed + (int64_t)tokens[m] * d;
   const float* p = pos_table ? pos_table + (int64_t)positions[m] * d : nullptr;
@@ -24,28 +26,61 @@ __global__ void embed_bf16_kernel(const int32_t* __restrict__ tokens, const int3
 int embed_bf16(const int32_t* tokens, const int32_t* positions, const __nv_bfloat16* embed, const float* pos_table,
                int M, int d, float* x, cudaStream_t st) {
   if (M == 0) return ALORA_OK;
-  embed_bf16_kernel<<<M, 256, 0, st>>>(tokens, positions, embed, pos_table, d, x);
+  ALORA_CUDA_CHECK(launch_pdl(embed_bf16_kernel, dim3(M), dim3(256), 0, st, nullptr, 0, tokens, positions, embed, pos_table, d, x));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
 
 // --------------------------------------------------------------- rmsnorm ---
 // One CTA per row, fp32 sum of squares in a fixed tree order; output bf16.
+// Row cached in registers (float4 per thread per 1024 columns): x is read once, h written with 8-byte stores.
+template <int V>
+__global__ void __launch_bounds__(256) rmsnorm_bf16_vec_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows,
+                                                               int d, const float* __restrict__ w, float eps,
+                                                               __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const int src = rows ? rows[r] : r;
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)src * d);
+  const int n4 = d >> 2;
+  float4 v[V];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * 256;
+    v[j] = i < n4 ? __ldg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss = fmaf(v[j].x, v[j].x, ss); ss = fmaf(v[j].y, v[j].y, ss);
+    ss = fmaf(v[j].z, v[j].z, ss); ss = fmaf(v[j].w, v[j].w, ss);
+  }
+  ss = block_sum(ss, red);
+  const float inv = rsqrtf(ss / (float)d + eps);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)r * d);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * 256;
+    if (i >= n4) break;
+    float4 y = make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv);
+    if (w) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + i);
+      y.x *= g.x; y.y *= g.y; y.z *= g.z; y.w *= g.w;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(y.x, y.y), hi = __floats2bfloat162_rn(y.z, y.w);
+    o[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
 __global__ void rmsnorm_bf16_kernel(const float* __restrict__ x, const int32_t* __restrict__ rows, int d,
                                     const float* __restrict__ w, float eps, __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
   const float* xr = x + (int64_t)src * d;
   float ss = 0.f;
-  if ((d & 3) == 0) {
-    for (int i = threadIdx.x * 4; i < d; i += blockDim.x * 4) {
-      const float4 v = *reinterpret_cast<const float4*>(xr + i);
-      ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-    }
-  } else {
-    for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
-  }
+  for (int i = threadIdx.x; i < d; i += blockDim.x) ss = fmaf(xr[i], xr[i], ss);
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / (float)d + eps);
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
@@ -58,7 +93,207 @@ __global__ void rmsnorm_bf16_kernel(const float* __restrict__ x, const int32_t* 
 int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps,
                  __nv_bfloat16* out, cudaStream_t st) {
   if (n_rows == 0) return ALORA_OK;
-  rmsnorm_bf16_kernel<<<n_rows, 256, 0, st>>>(x, rows, d, w, eps, out);
+  if (d % 4 == 0 && d <= 8192) {
+    const int v = (d / 4 + 255) / 256;
+    if (v <= 1) ALORA_CUDA_CHECK(launch_pdl(rmsnorm_bf16_vec_kernel<1>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, rows, d, w, eps, out));
+    else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(rmsnorm_bf16_vec_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, rows, d, w, eps, out));
+    else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(rmsnorm_bf16_vec_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, rows, d, w, eps, out));
+    else ALORA_CUDA_CHECK(launch_pdl(rmsnorm_bf16_vec_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, rows, d, w, eps, out));
+  } else {
+    ALORA_CUDA_CHECK(launch_pdl(rmsnorm_bf16_kernel, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, rows, d, w, eps, out));
+  }
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+// Sum of up to 8 split-K partials at float4 index i (all loads issued before the adds; split order kept).
+__device__ __forceinline__ float4 sum_parts4(const float* __restrict__ base, int64_t pstride, int nparts) {
+  float4 t[8];
+#pragma unroll
+  for (int p = 0; p < 8; ++p)
+    if (p < nparts) t[p] = __ldcg(reinterpret_cast<const float4*>(base + p * pstride));
+  float4 acc = t[0];
+#pragma unroll
+  for (int p = 1; p < 8; ++p)
+    if (p < nparts) { acc.x += t[p].x; acc.y += t[p].y; acc.z += t[p].z; acc.w += t[p].w; }
+  return acc;
+}
+
+// ------------------------------------------------- deferred split-K consumers ---
+// x[src] (+)= sum_p partials[p][src] in split order (the o-proj / MLP-down epilogue the split-K GEMM
+// deferred), then out[r] = bf16(rmsnorm(x[src]) * w).
+template <int V>
+__global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ part,
+                                                               int nparts, int64_t pstride,
+                                                               const int32_t* __restrict__ rows, int d,
+                                                               const float* __restrict__ w, float eps,
+                                                               __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ float red[32];
+  const int r = blockIdx.x;
+  const int src = rows ? rows[r] : r;
+  float4* xr = reinterpret_cast<float4*>(x + (int64_t)src * d);
+  const int n4 = d >> 2;
+  float4 v[V];
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * 256;
+    if (i < n4) {
+      const float4 acc = sum_parts4(part + (int64_t)src * d + 4 * i, pstride, nparts);
+      float4 xv = xr[i];
+      xv.x += acc.x; xv.y += acc.y; xv.z += acc.z; xv.w += acc.w;
+      xr[i] = xv;
+      v[j] = xv;
+    } else {
+      v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    ss = fmaf(v[j].x, v[j].x, ss); ss = fmaf(v[j].y, v[j].y, ss);
+    ss = fmaf(v[j].z, v[j].z, ss); ss = fmaf(v[j].w, v[j].w, ss);
+  }
+  ss = block_sum(ss, red);
+  const float inv = rsqrtf(ss / (float)d + eps);
+  uint2* o = reinterpret_cast<uint2*>(out + (int64_t)r * d);
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * 256;
+    if (i >= n4) break;
+    float4 y = make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv);
+    if (w) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(w) + i);
+      y.x *= g.x; y.y *= g.y; y.z *= g.z; y.w *= g.w;
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(y.x, y.y), hi = __floats2bfloat162_rn(y.z, y.w);
+    o[i] = make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
+int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, const int32_t* rows, int n_rows, int d,
+                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st) {
+  if (n_rows == 0) return ALORA_OK;
+  if (nparts < 1 || partials == nullptr) return rmsnorm_bf16(x, rows, n_rows, d, w, eps, out, st);
+  if (d % 4 != 0 || d > 8192 || nparts > 8) return ALORA_EINVAL;
+  const int v = (d / 4 + 255) / 256;
+  const int64_t ps = (int64_t)M * d;
+  if (v <= 1) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<1>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
+  else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
+  else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
+  else ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+// Deferred epilogue of a split-K QKV projection: per row, sum the splits (in order), rotate-half RoPE in
+// fp32 on the q and k heads (the kEpiRope math of the GEMM epilogue, one rounding), store q|k|v bf16 and
+// scatter the k and v rows into the paged pool (model.py:217-222) -- the step's kv_write, fused.
+__global__ void __launch_bounds__(256) qkv_finalize_kernel(const float* __restrict__ part, int nparts, int64_t pstride,
+                                                           int Nq, int Nkv, int D,
+                                                           const int32_t* __restrict__ positions,
+                                                           const float* __restrict__ cos_t,
+                                                           const float* __restrict__ sin_t,
+                                                           __nv_bfloat16* __restrict__ qkv, int ldq,
+                                                           const int32_t* __restrict__ slot_mapping,
+                                                           __nv_bfloat16* __restrict__ pool, int n_layers, int layer,
+                                                           int B) {
+  pdl_wait();
+  pdl_trigger();
+  const int m = blockIdx.x;
+  const int N = Nq + 2 * Nkv;
+  const int half = D / 2;
+  const int pos = positions[m];
+  const int slot = slot_mapping[m];
+  __nv_bfloat16* krow = nullptr;
+  __nv_bfloat16* vrow = nullptr;
+  if (slot >= 0) {
+    const int64_t blk = slot / B, r = slot % B;
+    krow = pool + (((blk * n_layers + layer) * 2 + 0) * B + r) * Nkv;
+    vrow = pool + (((blk * n_layers + layer) * 2 + 1) * B + r) * Nkv;
+  }
+  const float* row = part + (int64_t)m * N;
+  auto sum4 = [&](int col) { return sum_parts4(row + col, pstride, nparts); };
+  auto pack4 = [](float a, float b, float c, float d) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
+    return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  };
+  const int rope_q4 = (Nq + Nkv) / 2 / 4;  // 4-wide groups of rotate pairs over the q and k heads
+  const int v4 = Nkv / 4;
+  for (int t = threadIdx.x; t < rope_q4 + v4; t += blockDim.x) {
+    if (t < rope_q4) {
+      const int i = t * 4;                    // pair index
+      const int head = i / half, j = i % half;  // 4 pairs stay inside one head (half % 4 == 0)
+      const int c1 = head * D + j, c2 = c1 + half;
+      const float4 x1 = sum4(c1), x2 = sum4(c2);
+      const float4 cs = __ldg(reinterpret_cast<const float4*>(cos_t + (int64_t)pos * half + j));
+      const float4 sn = __ldg(reinterpret_cast<const float4*>(sin_t + (int64_t)pos * half + j));
+      const uint2 r1 = pack4(x1.x * cs.x - x2.x * sn.x, x1.y * cs.y - x2.y * sn.y, x1.z * cs.z - x2.z * sn.z,
+                             x1.w * cs.w - x2.w * sn.w);
+      const uint2 r2 = pack4(x2.x * cs.x + x1.x * sn.x, x2.y * cs.y + x1.y * sn.y, x2.z * cs.z + x1.z * sn.z,
+                             x2.w * cs.w + x1.w * sn.w);
+      *reinterpret_cast<uint2*>(qkv + (int64_t)m * ldq + c1) = r1;
+      *reinterpret_cast<uint2*>(qkv + (int64_t)m * ldq + c2) = r2;
+      if (krow && c1 >= Nq) {
+        *reinterpret_cast<uint2*>(krow + (c1 - Nq)) = r1;
+        *reinterpret_cast<uint2*>(krow + (c2 - Nq)) = r2;
+      }
+    } else {
+      const int c = Nq + Nkv + (t - rope_q4) * 4;
+      const float4 x = sum4(c);
+      const uint2 r = pack4(x.x, x.y, x.z, x.w);
+      *reinterpret_cast<uint2*>(qkv + (int64_t)m * ldq + c) = r;
+      if (vrow) *reinterpret_cast<uint2*>(vrow + (c - Nq - Nkv)) = r;
+    }
+  }
+}
+
+int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv, int D, const int32_t* positions,
+                      const float* cos_t, const float* sin_t, __nv_bfloat16* qkv, int ldq, const int32_t* slot_mapping,
+                      __nv_bfloat16* kv_pool, int n_layers, int layer, int B, cudaStream_t st) {
+  if (M == 0) return ALORA_OK;
+  if (nparts < 1 || nparts > 8 || !partials || !positions || !cos_t || !sin_t || D % 8 || Nq % D || Nkv % D || ldq % 4)
+    return ALORA_EINVAL;
+  const int64_t ps = (int64_t)M * (Nq + 2 * Nkv);
+  ALORA_CUDA_CHECK(launch_pdl(qkv_finalize_kernel, dim3(M), dim3(256), 0, st, nullptr, 0, partials, nparts, ps, Nq, Nkv,
+                              D, positions, cos_t, sin_t, qkv, ldq, slot_mapping, kv_pool, n_layers, layer, B));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+// Deferred epilogue of a split-K shrink: the kEpiLoraSelect row/slot/target select on the summed splits.
+__global__ void __launch_bounds__(128) lora_select_finalize_kernel(const float* __restrict__ part, int nparts,
+                                                                   int64_t pstride, int M, int SR, int rank,
+                                                                   const int32_t* __restrict__ row_slot,
+                                                                   const uint8_t* __restrict__ row_apply,
+                                                                   const uint8_t* __restrict__ targets,
+                                                                   __nv_bfloat16* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int m = blockIdx.x;
+  const int slot = row_slot[m];
+  const bool takes = slot >= 0 && row_apply[m];
+  const uint32_t tbits = takes ? targets[slot] : 0u;
+  const float* row = part + (int64_t)m * 3 * SR;
+  for (int c = threadIdx.x * 4; c < 3 * SR; c += blockDim.x * 4) {
+    const int t = c / SR, off = c % SR;  // SR % 4 == 0: a 4-column group stays in one plane
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if ((tbits >> t) & 1u) acc = sum_parts4(row + c, pstride, nparts);
+    float e[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if ((off + k) / rank != slot) e[k] = 0.f;
+    __nv_bfloat162 lo = __floats2bfloat162_rn(e[0], e[1]), hi = __floats2bfloat162_rn(e[2], e[3]);
+    *reinterpret_cast<uint2*>(out + ((int64_t)t * M + m) * SR + off) =
+        make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
+  }
+}
+
+int lora_select_finalize_bf16(const float* partials, int nparts, int M, int SR, int rank, const int32_t* row_slot,
+                              const uint8_t* row_apply, const uint8_t* slot_targets, __nv_bfloat16* s,
+                              cudaStream_t st) {
+  if (M == 0) return ALORA_OK;
+  if (nparts < 1 || nparts > 8 || SR % 4 || rank < 1) return ALORA_EINVAL;
+  ALORA_CUDA_CHECK(launch_pdl(lora_select_finalize_kernel, dim3(M), dim3(128), 0, st, nullptr, 0, partials, nparts,
+                              (int64_t)M * 3 * SR, M, SR, rank, row_slot, row_apply, slot_targets, s));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -153,6 +388,8 @@ int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_sl
 // One 32-bit mask per 128-row GEMM tile: bit `slot` set when any row of the tile takes that adapter's delta.
 __global__ void lora_tile_masks_kernel(const int32_t* __restrict__ row_slot, const uint8_t* __restrict__ row_apply,
                                        int M, uint32_t* __restrict__ masks) {
+  pdl_wait();
+  pdl_trigger();
   const int tile = blockIdx.x;
   const int m = tile * 128 + threadIdx.x;
   uint32_t bit = 0;
@@ -174,11 +411,21 @@ void configure_bf16_ops() {
   prefer_max_smem(rope_bf16_kernel);
   prefer_max_smem(lora_shrink_bf16_kernel);
   prefer_max_smem(lora_tile_masks_kernel);
+  prefer_max_smem(rmsnorm_bf16_vec_kernel<1>);
+  prefer_max_smem(rmsnorm_bf16_vec_kernel<2>);
+  prefer_max_smem(rmsnorm_bf16_vec_kernel<4>);
+  prefer_max_smem(rmsnorm_bf16_vec_kernel<8>);
+  prefer_max_smem(residual_rmsnorm_kernel<1>);
+  prefer_max_smem(residual_rmsnorm_kernel<2>);
+  prefer_max_smem(residual_rmsnorm_kernel<4>);
+  prefer_max_smem(residual_rmsnorm_kernel<8>);
+  prefer_max_smem(qkv_finalize_kernel);
+  prefer_max_smem(lora_select_finalize_kernel);
 }
 
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st) {
   if (M == 0) return ALORA_OK;
-  lora_tile_masks_kernel<<<(M + 127) / 128, 128, 0, st>>>(row_slot, row_apply, M, masks);
+  ALORA_CUDA_CHECK(launch_pdl(lora_tile_masks_kernel, dim3((M + 127) / 128), dim3(128), 0, st, nullptr, 0, row_slot, row_apply, M, masks));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }

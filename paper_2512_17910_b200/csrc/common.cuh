@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "../../include/alora_sm100a.h"
 
 #define ALORA_CUDA_CHECK(expr)                  \
@@ -31,6 +34,44 @@ inline void prefer_max_smem(Kernel kernel) {
 }
 
 constexpr int kNumSMs = 148;
+
+// ---- programmatic dependent launch (PDL)
+// Forward-path kernels are launched with programmatic stream serialization: kernel i+1 is scheduled while
+// kernel i drains, runs its prologue (barrier init, TMEM alloc, tensor-map prefetch, weight TMA) and
+// blocks in pdl_wait() until kernel i has completed and its writes are visible. Launched without the
+// attribute, both instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_on() {
+  static const bool on = [] {
+    const char* e = getenv("ALORA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// cudaLaunchKernelEx with the PDL attribute (plus optional extra attributes).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              const cudaLaunchAttribute* extra, int n_extra, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[4];
+  int n = 0;
+  for (int i = 0; i < n_extra && n < 3; ++i) attr[n++] = extra[i];
+  if (pdl_on()) {
+    attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  cfg.attrs = attr;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 constexpr int kGluBlock = 64;  // gate|up interleave granularity of w_in_t (llama)
 
 __device__ __forceinline__ float to_f32(float v) { return v; }

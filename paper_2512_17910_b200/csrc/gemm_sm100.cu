@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_u,
                      const GemmArgs args) {
   using C = Cfg<BN>;
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
@@ -398,26 +400,32 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, con
       return ALORA_ECUDA;
     configured = true;
   }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((args.N + BN - 1) / BN, (args.M + kBM - 1) / kBM, args.splits);
-  cfg.blockDim = dim3(kThreads, 1, 1);
-  cfg.dynamicSmemBytes = C::kSmem;
-  cfg.stream = st;
+  const dim3 grid((args.N + BN - 1) / BN, (args.M + kBM - 1) / kBM, args.splits);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // split-K tiles spin-wait on each other: co-residency required
   attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = args.splits > 1 ? 1 : 0;
   GemmArgs targs = args;
   static unsigned long long* trace_buf = nullptr;
   static const bool tracing = getenv("ALORA_GEMM_TRACE") != nullptr;
-  const int n_ctas = cfg.gridDim.x * cfg.gridDim.y * cfg.gridDim.z;
+  const int n_ctas = grid.x * grid.y * grid.z;
   if (tracing) {
     if (!trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 6 * 65536);
     cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
     targs.trace = trace_buf;
   }
-  if (cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN>, a, b, s, u, targs) != cudaSuccess) return ALORA_ECUDA;
+  if (args.splits > 1) {  // cooperative (co-resident split-K): no programmatic overlap with the previous kernel
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN>, a, b, s, u, targs) != cudaSuccess) return ALORA_ECUDA;
+  } else if (launch_pdl(gemm_bf16_kernel<BN>, grid, dim3(kThreads), C::kSmem, st, nullptr, 0, a, b, s, u, targs) !=
+             cudaSuccess) {
+    return ALORA_ECUDA;
+  }
   ALORA_LAUNCH_CHECK();
   if (tracing) {  // phase timings relative to the earliest CTA start (debug only)
     std::vector<unsigned long long> h(6 * n_ctas);
@@ -443,6 +451,335 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, con
   return ALORA_OK;
 }
 
+
+// ============================================================================================================
+// Weight-streaming GEMM for small M (M <= 256: aLoRA suffix steps, decode).
+//
+// One CTA owns an N tile of BN weight rows and a K slab, and ALL MT (<= 2) 128-row token tiles, so each
+// weight byte enters exactly one SM once and the activations are re-read only N/BN times (the per-SM
+// L2->SM ingest, not HBM, is what bounds narrow tiles). K is split over a thread-block cluster of S CTAs
+// (cluster dims 1x1xS); each parks its fp32 partial tile in its own shared memory and, after a cluster
+// barrier, CTA r reduces token rows [r*M/S, (r+1)*M/S) over distributed shared memory, summing the S
+// partials in rank order (deterministic for a given S), and runs the fused epilogue on them.
+//   warp 0           TMA producer; weight slabs of the first stages are issued BEFORE griddepcontrol.wait
+//                    (weights do not depend on the previous kernel), activations after it
+//   warp 1           TMEM allocator + single-thread tcgen05.mma issuer (MT accumulators of 128 x BN)
+//   warps 2..2+4MT   epilogue: warp w reads TMEM lanes 32*(w%4) of token tile (w-2)/4
+// ============================================================================================================
+#ifndef ALORA_WS_MT2_STAGES
+#define ALORA_WS_MT2_STAGES 4
+#endif
+template <int BN, int MT>
+struct WsCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStage = MT * kABytes + kBBytes;
+  static constexpr int kMaxStages = MT == 2 ? ALORA_WS_MT2_STAGES : 12;
+  static constexpr int kStages = (kSmemBudget / kStage) > kMaxStages ? kMaxStages : (kSmemBudget / kStage);
+  static constexpr int kAcc = MT * BN;
+  static constexpr int kTmemCols = kAcc <= 32 ? 32 : kAcc <= 64 ? 64 : kAcc <= 128 ? 128 : kAcc <= 256 ? 256 : 512;
+  static constexpr int kRedStride = BN + 4;
+  static constexpr int kRedBytes = MT * kBM * kRedStride * 4;
+  static constexpr bool kCanSplit = kRedBytes <= kStages * kStage;
+  static constexpr int kThreads = 64 + 128 * MT;
+  static constexpr int kSmem = 1024 + kStages * kStage + 256;
+};
+
+template <int BN, int MT>
+__global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
+    gemm_ws_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                   const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_u,
+                   const __grid_constant__ CUtensorMap tm_p, const GemmArgs args) {
+  using C = WsCfg<BN, MT>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN;
+  const int S = args.splits;
+  const int split = blockIdx.z;
+  if (threadIdx.x == 0) TRACE(0);
+  const int nkb_all = (args.K + kBK - 1) / kBK;
+  const int per = (nkb_all + S - 1) / S;
+  const int kb0 = min(nkb_all, split * per), kb1 = min(nkb_all, kb0 + per);
+  const int n_base = kb1 - kb0;
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tm_a);
+    sm100::prefetch_tmap(&tm_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    sm100::mbar_init(tmem_full, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  // Producer and MMA warps run their loops warp-converged and elect one lane per operation: a lone lane
+  // looping while the other 31 wait in __syncwarp lets ptxas reuse uniform registers of the diverged
+  // path (observed: the MMA's TMEM operand clobbered -> out-of-range TMEM address).
+  if (warp == 0) {
+    const uint64_t pol_act = sm100::policy_evict_last();
+    const uint64_t pol_w = sm100::policy_evict_first();
+    // weights of the first stages go out before the dependency wait: they overlap the previous kernel
+    const int n_pre = min(C::kStages, n_base);
+    for (int i = 0; i < n_pre; ++i) {
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + i * C::kStage;
+        sm100::mbar_arrive_expect_tx(&full[i], C::kStage);
+        sm100::tma_load_2d(sa + MT * C::kABytes, &tm_b, &full[i], (kb0 + i) * kBK, n0, pol_w);
+      }
+      __syncwarp();
+    }
+    pdl_wait();
+    pdl_trigger();
+    int target = 0, nkl = 0;
+    uint32_t mask = 0;
+    if (args.ks > 0 && split == S - 1) {
+      target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+      nkl = (args.ks + kBK - 1) / kBK;
+      for (int mt = 0; mt < MT; ++mt) mask |= args.tile_slot_mask[mt];
+    }
+    for (int i = 0; i < n_pre; ++i) {
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + i * C::kStage;
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          sm100::tma_load_2d(sa + mt * C::kABytes, &tm_a, &full[i], (kb0 + i) * kBK, mt * kBM, pol_act);
+      }
+      __syncwarp();
+    }
+    int s = n_pre % C::kStages;
+    uint32_t phase = n_pre == C::kStages ? 1u : 0u;
+    auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
+    for (int kb = kb0 + n_pre; kb < kb1; ++kb) {
+      sm100::mbar_wait(&empty[s], phase ^ 1);
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + s * C::kStage;
+        sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
+        sm100::tma_load_2d(sa + MT * C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          sm100::tma_load_2d(sa + mt * C::kABytes, &tm_a, &full[s], kb * kBK, mt * kBM, pol_act);
+      }
+      __syncwarp();
+      next();
+    }
+    for (int j = 0; j < nkl; ++j) {
+      if (!lora_block_present(j, args.rank, mask)) continue;
+      sm100::mbar_wait(&empty[s], phase ^ 1);
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + s * C::kStage;
+        sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
+        sm100::tma_load_2d(sa + MT * C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
+#pragma unroll
+        for (int mt = 0; mt < MT; ++mt)
+          sm100::tma_load_3d(sa + mt * C::kABytes, &tm_s, &full[s], j * kBK, mt * kBM, target, pol_act);
+      }
+      __syncwarp();
+      next();
+    }
+  } else {
+    pdl_wait();
+    if (warp == 1) {
+      int n_iters = n_base;
+      if (args.ks > 0 && split == S - 1) {
+        uint32_t mask = 0;
+        for (int mt = 0; mt < MT; ++mt) mask |= args.tile_slot_mask[mt];
+        const int nkl = (args.ks + kBK - 1) / kBK;
+        for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+      }
+      constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
+      int s = 0;
+      uint32_t phase = 0;
+      for (int it = 0; it < n_iters; ++it) {
+        sm100::mbar_wait(&full[s], phase);
+        sm100::tc_fence_after();
+        if (it == 0 && lane == 0) TRACE(1);
+        if (sm100::elect_one()) {
+          const uint8_t* sa = smem + s * C::kStage;
+          const uint64_t db = sm100::umma_desc_sw128(sa + MT * C::kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {
+              const uint64_t da = sm100::umma_desc_sw128(sa + mt * C::kABytes);
+              sm100::mma_bf16_ss(tmem + mt * BN, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                                 (it > 0 || k > 0) ? 1u : 0u);
+            }
+          }
+          sm100::mma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == C::kStages) { s = 0; phase ^= 1; }
+      }
+      if (sm100::elect_one()) sm100::mma_commit(tmem_full);
+      __syncwarp();
+    } else {
+      // epilogue warps
+      const int ew = warp - 2;
+      const int mt = ew >> 2, quarter = warp & 3;
+      const int trow = mt * kBM + quarter * 32 + lane;  // token row (the CTA spans all token tiles)
+      const bool has_acc = n_base > 0 || (args.ks > 0 && split == S - 1);
+      sm100::mbar_wait(tmem_full, 0);
+      sm100::tc_fence_after();
+      if (threadIdx.x == 64) TRACE(2);
+      const uint32_t taddr = tmem + mt * BN + ((uint32_t)(quarter * 32) << 16);
+      auto tmem_fetch = [&](int c0, float (&v)[32]) {  // warp-collective
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(taddr + c0, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = has_acc ? __uint_as_float(r[i]) : 0.f;
+      };
+      const bool quarter_live = mt * kBM + quarter * 32 < args.M;
+      if (S == 1) {
+        const int units = units_per_row<BN>(args, n0);
+        if (quarter_live)
+          for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, trow, u, tmem_fetch);
+      } else if (quarter_live) {
+        // deferred split-K: this split's fp32 partial rows -> partial[split][row][n]; the consuming kernel
+        // (residual RMSNorm / QKV finalize) sums the splits in order and applies the epilogue
+        // (32 x 32 fp32 boxes staged in the idle stage ring with the 128B swizzle, written by TMA stores;
+        // two staging buffers per warp, rows >= M clipped by the tensor map)
+        uint8_t* stg = smem + ew * 8192;
+        const int row0 = mt * kBM + quarter * 32;
+        int ci = 0;
+        for (int c = 0; c < BN; c += 32, ++ci) {
+          float v[32];
+          tmem_fetch(c, v);
+          uint8_t* buf = stg + (ci & 1) * 4096;
+          if (ci >= 2) {
+            if (lane == 0) sm100::bulk_wait_read<1>();
+            __syncwarp();
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            *reinterpret_cast<float4*>(buf + lane * 128 + ((j ^ (lane & 7)) << 4)) =
+                make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          sm100::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            sm100::tma_store_3d(&tm_p, buf, n0 + c, row0, split);
+            sm100::bulk_commit();
+          }
+          __syncwarp();
+        }
+        if (lane == 0) sm100::bulk_wait<0>();
+        __syncwarp();
+      }
+    }
+  }
+  if (threadIdx.x == 64) TRACE(3);
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  if (threadIdx.x == 64) TRACE(5);
+}
+
+template <int BN, int MT>
+int launch_ws(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, const CUtensorMap& u,
+              const GemmArgs& args, cudaStream_t st) {
+  CUtensorMap p = a;  // deferred split-K partials [splits][M][N] fp32 (TMA-store target)
+  if (args.splits > 1 && !make_tmap_3d_f32(&p, args.partial, args.splits, args.M, args.N, 32)) return ALORA_ECUDA;
+  using C = WsCfg<BN, MT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(gemm_ws_kernel<BN, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  GemmArgs targs = args;
+  static unsigned long long* trace_buf = nullptr;
+  static const bool tracing = getenv("ALORA_GEMM_TRACE") != nullptr;
+  const dim3 grid(args.N / BN, 1, args.splits);
+  const int n_ctas = grid.x * grid.z;
+  if (tracing) {
+    if (!trace_buf) cudaMalloc(&trace_buf, sizeof(unsigned long long) * 6 * 65536);
+    cudaMemsetAsync(trace_buf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
+    targs.trace = trace_buf;
+  }
+  if (launch_pdl(gemm_ws_kernel<BN, MT>, grid, dim3(C::kThreads), C::kSmem, st, nullptr, 0, a, b, s, u, p, targs) !=
+      cudaSuccess)
+    return ALORA_ECUDA;
+  ALORA_LAUNCH_CHECK();
+  if (tracing) {
+    std::vector<unsigned long long> h(6 * n_ctas);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, tend = 0;
+    double ph[5] = {0, 0, 0, 0, 0};
+    for (int c = 0; c < n_ctas; ++c) {
+      t0 = std::min(t0, h[6 * c]);
+      tend = std::max(tend, h[6 * c + 5]);
+      for (int p = 0; p < 5; ++p)
+        if (h[6 * c + p + 1] && h[6 * c + p]) ph[p] += double(h[6 * c + p + 1] - h[6 * c + p]);
+    }
+    fprintf(stderr,
+            "[gemm_ws trace] M=%d N=%d K=%d BN=%d MT=%d splits=%d ctas=%d span %.2f us; mean setup->1st data %.2f, "
+            "mainloop %.2f, epi %.2f, sync %.2f, reduce+exit %.2f us\n",
+            args.M, args.N, args.K, BN, MT, args.splits, n_ctas, (tend - t0) / 1e3, ph[0] / n_ctas / 1e3,
+            ph[1] / n_ctas / 1e3, ph[2] / n_ctas / 1e3, ph[3] / n_ctas / 1e3, ph[4] / n_ctas / 1e3);
+  }
+  return ALORA_OK;
+}
+
+
+struct WsChoice {
+  int bn = 0, splits = 1;
+  double cost = 1e30;
+};
+
+// Modelled time of one weight-streaming launch: per-wave SM ingest (activations + weight slab; at most
+// ~170 GB/s per SM, and no more than the stage ring's bytes in flight per ~1.2 us of loaded latency)
+// against the HBM stream of the weights. K splits (S > 1) are only planned when the caller can defer the
+// reduction to the consuming kernel; that consumer re-reads S fp32 partials from L2.
+template <int BN, int MT>
+void ws_consider(WsChoice& best, int M, int N, int K, bool can_defer, int64_t defer_cap) {
+  using C = WsCfg<BN, MT>;
+  const int nkb = (K + kBK - 1) / kBK;
+  const int tiles = N / BN;
+  for (int S = 1; S <= kMaxSplits; ++S) {
+    if (S > 1 && (!can_defer || (int64_t)S * M * N * 4 > defer_cap)) break;
+    if (S > nkb) break;
+    const int per = (nkb + S - 1) / S;
+    if ((nkb + per - 1) / per != S) continue;  // no empty trailing splits
+    const int waves = (tiles * S + kNumSMs - 1) / kNumSMs;
+    const double ingest = (double)(std::min(M, MT * kBM) + BN) * per * kBK * 2.0;
+    const double inflight = (double)C::kStages * (std::min(M, MT * kBM) + BN) * kBK * 2.0;
+    const double rate = std::min(170e9, inflight / 1.2e-6);
+    double t = waves * (ingest / rate + 1.5e-6);
+    t = std::max(t, (double)N * K * 2.0 / 6.5e12 + 1.5e-6);
+    if (S > 1) t += (double)S * M * N * 4.0 / 8e12 + 0.3e-6;
+    if (t < best.cost) {
+      best.cost = t;
+      best.bn = BN;
+      best.splits = S;
+    }
+  }
+}
+
+template <int MT>
+int dispatch_ws(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, const CUtensorMap& u,
+                GemmArgs& args, int bn, cudaStream_t st) {
+  switch (bn) {
+    case 256: return launch_ws<256, MT>(a, b, s, u, args, st);
+    case 128: return launch_ws<128, MT>(a, b, s, u, args, st);
+    case 64: return launch_ws<64, MT>(a, b, s, u, args, st);
+    default: return launch_ws<32, MT>(a, b, s, u, args, st);
+  }
+}
+
 }  // namespace
 
 void configure_gemm() {
@@ -450,10 +787,20 @@ void configure_gemm() {
   prefer_max_smem(gemm_bf16_kernel<64>);
   prefer_max_smem(gemm_bf16_kernel<128>);
   prefer_max_smem(gemm_bf16_kernel<256>);
+  prefer_max_smem(gemm_ws_kernel<32, 1>);
+  prefer_max_smem(gemm_ws_kernel<64, 1>);
+  prefer_max_smem(gemm_ws_kernel<128, 1>);
+  prefer_max_smem(gemm_ws_kernel<256, 1>);
+  prefer_max_smem(gemm_ws_kernel<32, 2>);
+  prefer_max_smem(gemm_ws_kernel<64, 2>);
+  prefer_max_smem(gemm_ws_kernel<128, 2>);
+  prefer_max_smem(gemm_ws_kernel<256, 2>);
 }
 
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* Cout, int ldc, int M,
-              int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws, int max_splits) {
+              int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws, int max_splits,
+              GemmDefer* defer) {
+  if (defer) defer->splits_out = 1;
   if (M == 0 || N == 0) return ALORA_OK;
   if (M < 0 || N < 0 || K < 1 || lda % 8 || ldb % 8 || ldc % 8) return ALORA_EINVAL;
   const int base_epi = epi & 15;
@@ -521,6 +868,53 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.n_q = lora->n_q;
     args.n_kv = lora->n_kv;
     args.tile_slot_mask = lora->tile_slot_mask;
+  }
+  static const bool no_ws = getenv("ALORA_GEMM_NO_WS") != nullptr;  // A/B switch to the per-tile kernel
+  if (M <= 2 * kBM && !no_ws) {
+    // weight streaming: one CTA per (N tile, K split) covering every token row
+    const int mt = (M + kBM - 1) / kBM;
+    const bool can_defer = defer != nullptr && defer->partial != nullptr && !(epi & 16) &&
+                           (base_epi == kEpiAdd || base_epi == kEpiRope || base_epi == kEpiLoraSelect);
+    const int64_t defer_cap = can_defer ? defer->capacity : 0;
+    WsChoice best;
+    auto consider = [&](int bn) {
+      if (!fits(bn) || mt * bn > 512) return;
+      if (mt == 1) {
+        switch (bn) {
+          case 256: ws_consider<256, 1>(best, M, N, K, can_defer, defer_cap); break;
+          case 128: ws_consider<128, 1>(best, M, N, K, can_defer, defer_cap); break;
+          case 64: ws_consider<64, 1>(best, M, N, K, can_defer, defer_cap); break;
+          default: ws_consider<32, 1>(best, M, N, K, can_defer, defer_cap);
+        }
+      } else {
+        switch (bn) {
+          case 256: ws_consider<256, 2>(best, M, N, K, can_defer, defer_cap); break;
+          case 128: ws_consider<128, 2>(best, M, N, K, can_defer, defer_cap); break;
+          case 64: ws_consider<64, 2>(best, M, N, K, can_defer, defer_cap); break;
+          default: ws_consider<32, 2>(best, M, N, K, can_defer, defer_cap);
+        }
+      }
+    };
+    for (int bn : {256, 128, 64, 32}) consider(bn);
+    static const int force_bn = getenv("ALORA_WS_BN") ? atoi(getenv("ALORA_WS_BN")) : 0;  // debug overrides
+    static const int force_s = getenv("ALORA_WS_S") ? atoi(getenv("ALORA_WS_S")) : 0;
+    if (force_bn > 0 && fits(force_bn) && mt * force_bn <= 512) best.bn = force_bn;
+    if (force_s > 0 && (force_s == 1 || can_defer)) best.splits = force_s;
+    if (best.bn > 0) {
+      if (base_epi == kEpiRope && (lora->rope_cols % best.bn || best.bn % lora->head_dim)) return ALORA_EINVAL;
+      CUtensorMap tb2, tu2 = tu;
+      if (!make_tmap_2d(&tb2, Bt, N, K, ldb, best.bn, kBK)) return ALORA_ECUDA;
+      if (args.ks > 0 && !make_tmap_2d(&tu2, lora->up_t, N, lora->ks, lora->ks, best.bn, kBK)) return ALORA_ECUDA;
+      if (args.ks == 0) tu2 = tb2;
+      args.splits = best.splits;
+      if (best.splits > 1) {
+        if (!can_defer) return ALORA_EINVAL;
+        args.partial = defer->partial;
+        defer->splits_out = best.splits;
+      }
+      return mt == 1 ? dispatch_ws<1>(ta, tb2, ts, tu2, args, best.bn, st)
+                     : dispatch_ws<2>(ta, tb2, ts, tu2, args, best.bn, st);
+    }
   }
   // split K when the tile grid cannot fill the machine (weight-streaming small-M launches): the largest
   // split count with tiles * splits <= 148 (one co-resident CTA per SM) and >= 4 K-blocks per split

@@ -99,10 +99,33 @@ inline GemmWs gemm_ws_from(void* base, int64_t bytes) {
   w.counters = reinterpret_cast<int*>(static_cast<char*>(base) + w.partial_bytes);
   return w;
 }
-// ws enables split-K (max_splits caps it) when the output tiles cannot fill the 148 SMs.
+// Deferred split-K for weight-streaming launches (M <= 256) of the kEpiAdd / kEpiRope epilogues: when the
+// plan splits K, the GEMM writes fp32 partials [splits][M][N] to `partial` (capacity bytes) and skips its
+// epilogue; the consuming kernel (residual_rmsnorm_bf16 / qkv_finalize_bf16) sums the splits in order and
+// applies it. splits_out reports the split count (1 = the epilogue ran inside the GEMM).
+struct GemmDefer {
+  float* partial = nullptr;
+  int64_t capacity = 0;
+  int splits_out = 1;
+};
+// ws enables split-K of the per-tile kernel (M > 256; max_splits caps it) when the output tiles cannot fill
+// the 148 SMs.
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* C, int ldc,
               int M, int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws = nullptr,
-              int max_splits = 8);
+              int max_splits = 8, GemmDefer* defer = nullptr);
+// x[r] (+)= sum_p partials[p][r] (split order), then out[r] = bf16(rmsnorm(x[r]) * w); rows as rmsnorm_bf16.
+int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, const int32_t* rows, int n_rows, int d,
+                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st);
+// qkv[m] = bf16(RoPE(sum_p partials[p][m])) on q/k heads (plain sum on v), and the row's k/v scattered into
+// the paged pool (the kv_write of the step) -- the deferred epilogue of a split-K QKV projection.
+int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv, int D, const int32_t* positions,
+                      const float* cos_t, const float* sin_t, __nv_bfloat16* qkv, int ldq, const int32_t* slot_mapping,
+                      __nv_bfloat16* kv_pool, int n_layers, int layer, int B, cudaStream_t st);
+// Deferred epilogue of a split-K LoRA shrink (kEpiLoraSelect): s[t][m][off] = bf16(sum_p partials[p][m][t*SR+off])
+// where row m takes slot (off / rank)'s delta on target t, else 0.
+int lora_select_finalize_bf16(const float* partials, int nparts, int M, int SR, int rank, const int32_t* row_slot,
+                              const uint8_t* row_apply, const uint8_t* slot_targets, __nv_bfloat16* s,
+                              cudaStream_t st);
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st);
 
 }  // namespace alora

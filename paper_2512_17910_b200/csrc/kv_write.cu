@@ -17,6 +17,8 @@ __global__ void __launch_bounds__(kKvThreads) kv_write_vec_kernel(
     const uint8_t* __restrict__ k, const uint8_t* __restrict__ v, int64_t ld_src_bytes,
     const int32_t* __restrict__ slot_mapping, int M, int row_bytes, uint8_t* __restrict__ pool, int n_layers,
     int layer, int B, int rows_per_cta) {
+  pdl_wait();
+  pdl_trigger();
   const int vec_per_row = row_bytes / 16;
   const int per_row = 2 * vec_per_row;  // K then V
   const int m0 = blockIdx.x * rows_per_cta;
@@ -67,9 +69,10 @@ int kv_write(int dtype, const void* k, const void* v, int64_t ld_src, const int3
     int rows_per_cta = kKvThreads / per_row;
     if (rows_per_cta < 1) rows_per_cta = 1;
     const int grid = (M + rows_per_cta - 1) / rows_per_cta;
-    kv_write_vec_kernel<<<grid, kKvThreads, 0, st>>>(
-        static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v), ld_bytes, slot_mapping, M, row_bytes,
-        static_cast<uint8_t*>(kv_pool), n_layers, layer, B, rows_per_cta);
+    ALORA_CUDA_CHECK(launch_pdl(kv_write_vec_kernel, dim3(grid), dim3(kKvThreads), 0, st, nullptr, 0,
+                                static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v), ld_bytes,
+                                slot_mapping, M, row_bytes, static_cast<uint8_t*>(kv_pool), n_layers, layer, B,
+                                rows_per_cta));
   } else {
     kv_write_scalar_kernel<<<M, 128, 0, st>>>(static_cast<const uint8_t*>(k), static_cast<const uint8_t*>(v),
                                               ld_bytes, slot_mapping, row_bytes, elem,
@@ -82,6 +85,8 @@ int kv_write(int dtype, const void* k, const void* v, int64_t ld_src, const int3
 // ---------------------------------------------------------------- argmax ---
 // Ties -> lowest index: compare (value, -index) lexicographically.
 __global__ void argmax_kernel(const float* __restrict__ logits, int vocab, int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
   __shared__ float sv[32];
   __shared__ int si[32];
   const float* row = logits + (int64_t)blockIdx.x * vocab;
@@ -123,7 +128,7 @@ void configure_kv_ops() {
 int argmax_rows(const float* logits, int rows, int vocab, int32_t* out_ids, cudaStream_t st) {
   if (rows == 0) return ALORA_OK;
   if (vocab <= 0) return ALORA_EINVAL;
-  argmax_kernel<<<rows, 1024, 0, st>>>(logits, vocab, out_ids);
+  ALORA_CUDA_CHECK(launch_pdl(argmax_kernel, dim3(rows), dim3(1024), 0, st, nullptr, 0, logits, vocab, out_ids));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }

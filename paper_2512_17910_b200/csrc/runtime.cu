@@ -5,6 +5,7 @@
 // spans of an engine step are packed into one varlen batch and every layer's
 // kernels are launched from here, on the caller's stream, with no host sync.
 
+#include <algorithm>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -87,7 +88,8 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Workspace carve-up shared by alora_model_workspace_bytes and the executor.
 struct Ws {
-  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, total;
+  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, part, total;
+  int64_t part_bytes;
   int64_t attn_ws_bytes, gemm_ws_bytes;
 };
 
@@ -115,6 +117,9 @@ Ws plan_ws(const AloraModelDesc& d) {
   w.attn_ws = take(w.attn_ws_bytes);
   w.gemm_ws_bytes = d.dtype == ALORA_BF16 ? gemm_bf16_workspace_bytes() : 0;
   w.gemm_ws = take(w.gemm_ws_bytes);  // split-K counters must start zeroed: the caller zero-fills the workspace
+  // deferred split-K partials of the weight-streaming GEMMs (M <= 256): [<= 8 splits][M][max(Nqkv, d)] fp32
+  w.part_bytes = d.dtype == ALORA_BF16 ? 8LL * std::min<int64_t>(T, 256) * std::max<int64_t>(nq + 2 * nkv, d.d_model) * 4 : 0;
+  w.part = take(w.part_bytes);
   w.total = off;
   return w;
 }
@@ -136,9 +141,11 @@ int validate(const AloraModelDesc* d) {
 
 // LoRA shrink for every row against all adapters' stacked down rows [3*SR, K] on the tensor cores, with the
 // per-row slot/target select in the epilogue; the SIMT segmented kernel covers SR that is not a multiple of 64.
+// With a deferral buffer, a weight-streaming shrink may split K; its select epilogue then runs in
+// lora_select_finalize_bf16 (one extra small launch, counted in *extra_launches).
 int shrink(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
            const __nv_bfloat16* down, int n_slots, int R, const uint8_t* targets, __nv_bfloat16* s, cudaStream_t st,
-           const GemmWs* gw) {
+           const GemmWs* gw, float* part = nullptr, int64_t part_bytes = 0, int* extra_launches = nullptr) {
   const int SR = n_slots * R;
   if (SR % 64 != 0) return lora_shrink_bf16(h, M, K, row_slot, row_apply, down, n_slots, R, targets, s, st);
   GemmLora g;
@@ -147,7 +154,13 @@ int shrink(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const 
   g.sel_targets = targets;
   g.sel_sr = SR;
   g.sel_rank = R;
-  return gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, 3 * SR, K, &g, st, gw);
+  GemmDefer df;
+  df.partial = part;
+  df.capacity = part_bytes;
+  const int rc = gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, 3 * SR, K, &g, st, gw, 8, part ? &df : nullptr);
+  if (rc != ALORA_OK || df.splits_out <= 1) return rc;
+  if (extra_launches) ++*extra_launches;
+  return lora_select_finalize_bf16(part, df.splits_out, M, SR, R, row_slot, row_apply, targets, s, st);
 }
 
 int forward_f32(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
@@ -223,7 +236,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   auto* hf = reinterpret_cast<__nv_bfloat16*>(base + w.hf);
   void* aws = base + w.attn_ws;
   const GemmWs gws = gemm_ws_from(base + w.gemm_ws, w.gemm_ws_bytes);
-  const GemmWs* gw = &gws;  // split-K scratch for weight-streaming (small-M) GEMMs
+  const GemmWs* gw = &gws;  // split-K scratch of the per-tile GEMM (M > 256)
+  float* part = reinterpret_cast<float*>(base + w.part);  // deferred split-K partials (M <= 256)
+  int pend = 0;  // splits of the residual update still pending in `part` (applied by the next RMSNorm)
   const int M = s.n_tokens, S = s.n_seqs, dm = d.d_model, F = d.ffn_dim;
   const int H = d.n_heads, Hkv = d.n_kv_heads, D = d.head_dim;
   const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
@@ -245,12 +260,14 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
                                            llama ? nullptr : d.pos_table, M, dm, x, st));
   if (lora) RUN("lora_masks", m_ * 5, 0, lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
   for (int l = 0; l < d.n_layers; ++l) {
-    RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+        residual_rmsnorm_bf16(x, part, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    pend = 0;
     GemmLora gl;
     if (lora) {
       RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
           shrink(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]), d.n_slots,
-                 d.lora_rank, d.slot_targets, sws, st, gw));
+                 d.lora_rank, d.slot_targets, sws, st, gw, part, w.part_bytes, &run.n));
       gl.s = sws;
       gl.up_t = static_cast<const __nv_bfloat16*>(mdl.lora_up_t[l]);
       gl.ks = d.n_slots * d.lora_rank;
@@ -266,29 +283,49 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       gl.rope_cols = Nq + Nkv;
       gl.head_dim = D;
     }
+    GemmDefer dq;
+    dq.partial = part;
+    dq.capacity = w.part_bytes;
     RUN("gemm_qkv", gemm_bytes(m_, Nqkv_, dm_, 2, false) + (lora ? 2.0 * Nqkv_ * ks_ : 0.0), 2.0 * m_ * Nqkv_ * dm_,
         gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
-                  Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st, gw));
-    RUN("kv_write", 2.0 * 2 * m_ * Nkv * 2, 0,
-        kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
-                 d.block_size, st));
+                  Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st, gw, 8, llama ? &dq : nullptr));
+    if (dq.splits_out > 1) {  // split-K QKV: RoPE + bf16 + the paged KV scatter run in the finalize kernel
+      RUN("qkv_finalize", m_ * Nqkv_ * 4.0 * dq.splits_out + 2.0 * m_ * Nqkv_ + 2.0 * 2 * m_ * Nkv * 2, 0,
+          qkv_finalize_bf16(part, dq.splits_out, M, Nq, Nkv, D, s.positions, d.rope_cos, d.rope_sin, qkv, Nqkv,
+                            s.slot_mapping, static_cast<__nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, st));
+    } else {
+      RUN("kv_write", 2.0 * 2 * m_ * Nkv * 2, 0,
+          kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
+                   d.block_size, st));
+    }
     RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
         attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
                   static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
                   aws, w.attn_ws_bytes, st, d.total_blocks));
+    GemmDefer dfo;
+    dfo.partial = part;
+    dfo.capacity = w.part_bytes;
     RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
         gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq, nullptr,
-                  st, gw));
-    RUN("rmsnorm", m_ * dm_ * 6, 0, rmsnorm_bf16(x, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+                  st, gw, 8, &dfo));
+    pend = dfo.splits_out > 1 ? dfo.splits_out : 0;
+    RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+        residual_rmsnorm_bf16(x, part, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    pend = 0;
     const double n_in = llama ? 2 * F_ : F_;
     RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2, 2.0 * m_ * n_in * dm_,
         gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act, F,
                   M, llama ? 2 * F : F, dm, nullptr, st, gw));
+    GemmDefer dfm;
+    dfm.partial = part;
+    dfm.capacity = w.part_bytes;
     RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true), 2.0 * m_ * dm_ * F_,
         gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
-                  st, gw));
+                  st, gw, 8, &dfm));
+    pend = dfm.splits_out > 1 ? dfm.splits_out : 0;
   }
-  RUN("rmsnorm", S_ * dm_ * 6, 0, rmsnorm_bf16(x, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
+  RUN("rmsnorm", S_ * dm_ * (6 + 8.0 * pend), 0,
+      residual_rmsnorm_bf16(x, part, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
   RUN("gemm_lm_head", gemm_bytes(S_, V_, dm_, 4, false), 2.0 * S_ * V_ * dm_,
       gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm, s.logits,
                 d.vocab, S, d.vocab, dm, nullptr, st, gw));

@@ -45,4 +45,11 @@ for _ in range(reps):
     e1.record()
     torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))
-print(f"forward M={p['M']} S={p['S']}: {np.median(ts):.3f} ms (launches {model.last_launches})", flush=True)
+hs = []
+for _ in range(reps):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    model.launch(st)
+    hs.append(time.perf_counter() - t0)
+torch.cuda.synchronize()
+print(f"forward M={p['M']} S={p['S']}: {np.median(ts):.3f} ms device, host launch {1e3*np.median(hs):.3f} ms (launches {model.last_launches})", flush=True)

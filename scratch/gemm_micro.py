@@ -3,12 +3,13 @@ sys.path.insert(0, '.')
 from paper_2512_17910_b200 import _native
 lib = _native.lib
 flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device="cuda")
+ws = torch.zeros(lib.alora_gemm_workspace_bytes(), dtype=torch.uint8, device="cuda")
 def run(M, N, K, split, epi=0, reps=20, label=""):
     A = torch.randn(M, K, device="cuda").to(torch.bfloat16)
     B = (torch.randn(N, K, device="cuda") * 0.05).to(torch.bfloat16)
     C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
-    f = lambda: lib.alora_gemm_bf16(epi, A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, 8 if split else 1, st)
+    f = lambda: lib.alora_gemm_bf16(epi, A.data_ptr(), K, B.data_ptr(), K, C.data_ptr(), N, M, N, K, ws.data_ptr() if split else None, ws.numel() if split else 0, st)
     for _ in range(3): f()
     torch.cuda.synchronize()
     ts = []
