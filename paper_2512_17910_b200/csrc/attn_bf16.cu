@@ -400,9 +400,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (a.trace) a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 6 + (slot)] = gtimer(); \
   } while (0)
 
-// K/V ring depth: D=64 keeps the CTA at ~98 KB of smem so two CTAs (two independent softmax chains) share an SM
+// K/V ring depth. The ring cycle of a stage is TMA latency + S MMA + softmax + PV (~2-3 us under load), so
+// the per-tile period is that over kNS; D=64 keeps the CTA at ~98 KB of smem (4 stages, one P buffer) so
+// two CTAs (two independent softmax chains) share an SM.
 template <int D>
-constexpr int kNS = D == 64 ? 3 : 4;
+constexpr int kNS = 4;
 constexpr int kThreads = 192;   // 4 softmax + 1 producer + 1 MMA warps
 constexpr float kRescaleLog2 = 8.f;
 
@@ -415,7 +417,7 @@ struct Smem {
   static constexpr int kK = kQ + kQBytes;
   static constexpr int kV = kK + kNS<D> * kKVBytes;
   static constexpr int kP = kV + kNS<D> * kKVBytes;
-  static constexpr int kBar = kP + 2 * kPBytes;
+  static constexpr int kBar = kP + kPBytes;  // one P buffer: P_{t+1} is written after PV_t has read P_t
   static constexpr int kTotal = kBar + 256 + 1024;  // barriers + TMEM slot + alignment slack
 };
 
@@ -435,9 +437,9 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   uint64_t* kv_full = bars + 1;        // kNS<D>
   uint64_t* kv_empty = kv_full + kNS<D>;  // kNS<D>
   uint64_t* s_full = kv_empty + kNS<D>;   // 2
-  uint64_t* p_full = s_full + 2;       // 2
-  uint64_t* pv_done = p_full + 2;      // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* p_full = s_full + 2;       // 1
+  uint64_t* pv_done = p_full + 1;      // 1 (completes once per tile)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
   __shared__ int s_last;
 
   const int G = a.H / a.Hkv;
@@ -459,17 +461,17 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) ATTN_TRACE(0);
   constexpr int CH = D / 8;
+  const int live_warps = (rows_here + 31) / 32;  // softmax warps with at least one live packed row
   if (tid == 0) {
     sm100::mbar_init(q_full, 32);
     for (int i = 0; i < kNS<D>; ++i) {
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&s_full[i], 1);
-      sm100::mbar_init(&p_full[i], 128);
-      sm100::mbar_init(&pv_done[i], 1);
-    }
+    sm100::mbar_init(&s_full[0], 1);
+    sm100::mbar_init(&s_full[1], 1);
+    sm100::mbar_init(p_full, 32 * live_warps);
+    sm100::mbar_init(pv_done, 1);
     sm100::fence_barrier_init();
   }
   if (warp == 5) sm100::tmem_alloc<256>(tmem_slot);
@@ -477,13 +479,44 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  pdl_wait();  // q, the block table and this layer's fresh K/V rows come from the kernels before
-  pdl_trigger();
   const uint32_t tS[2] = {tmem, tmem + 64};
   const uint32_t tO = tmem + 128;
 
+  // Producer and MMA loops run warp-converged with one elected lane per operation (see gemm_ws_kernel).
   if (warp == 4) {
     // ------------------------------------------------------------------ producer warp
+    const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;  // step metadata: uploaded before the forward
+    const int last_blk = (key_end - 1) / a.B;
+    const int per_tile = kKT / a.B;
+    const uint64_t pol = sm100::policy_evict_last();  // a conversation's prefix is read by each adapter's request
+    auto issue_kv = [&](int t) {  // K/V tile t: TMA boxes of [B keys x 64 dims], page by page via the block table
+      const int st = t % kNS<D>;
+      sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
+      uint8_t* dk = sm + L::kK + st * L::kKVBytes;
+      uint8_t* dv = sm + L::kV + st * L::kKVBytes;
+      const int b0 = (key_begin + t * kKT) / a.B;
+      for (int j = 0; j < per_tile; ++j) {
+        const int64_t blk = bt[min(b0 + j, last_blk)];  // past the end: a valid duplicate, masked later
+        const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+#pragma unroll
+        for (int sub = 0; sub < D / 64; ++sub) {
+          sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk, pol);
+          sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
+                             rowk + a.B, pol);
+        }
+      }
+    };
+    // Tiles made only of pages wholly before this sequence's start position hold cached KV that no kernel of
+    // this step writes: they stream in before the dependency wait, overlapping the kernels before.
+    const int cached_end = (start / a.B) * a.B;
+    int t = 0;
+    for (; t < min(n_tiles, kNS<D>); ++t) {
+      if (key_begin + (t + 1) * kKT > cached_end) break;
+      if (sm100::elect_one()) issue_kv(t);
+      __syncwarp();
+    }
+    pdl_wait();  // q and this step's fresh K/V rows come from the kernels before
+    pdl_trigger();
     // Q: the 32 lanes gather the 128 GQA-packed rows (4 each) with cp.async into the swizzled layout
     for (int p = lane; p < kQT; p += 32) {
       const bool valid = p < rows_here;
@@ -496,45 +529,25 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     cp_async_wait<0>();
     sm100::fence_proxy_async_smem();
     sm100::mbar_arrive(q_full);
-    // K/V: one lane issues TMA boxes of [B keys x 64 dims] page by page (the block table is the gather index)
-    if (lane == 0) {
-      const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;
-      const int last_blk = (key_end - 1) / a.B;
-      const int per_tile = kKT / a.B;
-      const uint64_t pol = sm100::policy_evict_last();  // prefix blocks are shared by requests of the step
-      for (int t = 0; t < n_tiles; ++t) {
-        const int st = t % kNS<D>;
-        if (t >= kNS<D>) sm100::mbar_wait(&kv_empty[st], ((t / kNS<D>) - 1) & 1);
-        sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
-        uint8_t* dk = sm + L::kK + st * L::kKVBytes;
-        uint8_t* dv = sm + L::kV + st * L::kKVBytes;
-        const int b0 = (key_begin + t * kKT) / a.B;
-        for (int j = 0; j < per_tile; ++j) {
-          const int64_t blk = bt[min(b0 + j, last_blk)];  // past the end: a valid duplicate, masked later
-          const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
-#pragma unroll
-          for (int sub = 0; sub < D / 64; ++sub) {
-            sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk,
-                               pol);
-            sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
-                               rowk + a.B, pol);
-          }
-        }
-      }
+    for (; t < n_tiles; ++t) {
+      const int st = t % kNS<D>;
+      if (t >= kNS<D>) sm100::mbar_wait(&kv_empty[st], ((t / kNS<D>) - 1) & 1);
+      if (sm100::elect_one()) issue_kv(t);
+      __syncwarp();
     }
-    __syncwarp();
   } else if (warp == 5) {
     // ------------------------------------------------------------------ MMA issuer
-    if (sm100::elect_one()) {
-      constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
-      constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
-      sm100::mbar_wait(q_full, 0);
-      ATTN_TRACE(1);
+    pdl_wait();
+    constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
+    constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
+    sm100::mbar_wait(q_full, 0);
+    if (lane == 0) ATTN_TRACE(1);
+    sm100::tc_fence_after();
+    auto issue_s = [&](int t) {
+      const int st = t % kNS<D>;
+      sm100::mbar_wait(&kv_full[st], (t / kNS<D>) & 1);
       sm100::tc_fence_after();
-      auto issue_s = [&](int t) {
-        const int st = t % kNS<D>;
-        sm100::mbar_wait(&kv_full[st], (t / kNS<D>) & 1);
-        sm100::tc_fence_after();
+      if (sm100::elect_one()) {
         const uint8_t* qb = sm + L::kQ;
         const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
 #pragma unroll
@@ -544,13 +557,16 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
           sm100::mma_bf16_ss(tS[t & 1], da, db, idesc_s, ks > 0 ? 1u : 0u);
         }
         sm100::mma_commit(&s_full[t & 1]);
-      };
-      issue_s(0);
-      for (int t = 0; t < n_tiles; ++t) {
-        if (t + 1 < n_tiles) issue_s(t + 1);  // S buffer (t+1)&1 was drained: p_full for t-1 was awaited
-        sm100::mbar_wait(&p_full[t & 1], (t >> 1) & 1);
-        sm100::tc_fence_after();
-        const uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
+      }
+      __syncwarp();
+    };
+    issue_s(0);
+    for (int t = 0; t < n_tiles; ++t) {
+      if (t + 1 < n_tiles) issue_s(t + 1);  // S buffer (t+1)&1 was drained: p_full for t-1 was awaited
+      sm100::mbar_wait(p_full, t & 1);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint8_t* pb = sm + L::kP;
         const uint8_t* vb = sm + L::kV + (t % kNS<D>) * L::kKVBytes;
 #pragma unroll
         for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
@@ -558,19 +574,23 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
           const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
           sm100::mma_bf16_ss(tO, da, db, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
         }
-        sm100::mma_commit(&pv_done[t & 1]);
+        sm100::mma_commit(pv_done);
         sm100::mma_commit(&kv_empty[t % kNS<D>]);
       }
+      __syncwarp();
     }
-    __syncwarp();
-  } else {
-    // ------------------------------------------------------------------ softmax (warps 0-3)
+  } else if (warp < live_warps) {
+    // ------------------------------------------------------------------ softmax (live warps of 0-3)
+    // Scores stay raw (unscaled): the max commutes with the positive scale, and each probability is one
+    // FFMA + ex2: p = 2^(s * scale_log2 - m * scale_log2). m_run is kept raw; partials store it scaled.
+    pdl_wait();
     const int r = tid;  // TMEM lane == packed row
     const bool live = r < rows_here;
-    const bool warp_live = warp * 32 < rows_here;
     const int pos = live ? start + (qt * kQT + r) / G : -1;
     const int lim = min(pos, key_end - 1);
     const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    const float sc = a.scale_log2;
+    const float thr = kRescaleLog2 / sc;  // rescale threshold in raw score units
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < n_tiles; ++t) {
       const int k0 = key_begin + t * kKT;
@@ -578,19 +598,16 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::tc_fence_after();
       if (t == 0 && tid == 0) ATTN_TRACE(2);
       float sv[kKT];
-      if (warp_live) {
+      {
         uint32_t r0[32], r1[32];
         sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base, r0);
         sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base + 32, r1);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
-          sv[j] = __uint_as_float(r0[j]) * a.scale_log2;
-          sv[j + 32] = __uint_as_float(r1[j]) * a.scale_log2;
+          sv[j] = __uint_as_float(r0[j]);
+          sv[j + 32] = __uint_as_float(r1[j]);
         }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kKT; ++j) sv[j] = -INFINITY;
       }
       const bool need_mask = k0 + kKT - 1 > lim;
       float mt = -INFINITY;
@@ -601,10 +618,10 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       }
       const float m_new = fmaxf(m_run, mt);
       // lazy rescale: only when the max grew by more than 2^8 (or on the first finite max)
-      const bool grow = m_new > m_run + kRescaleLog2 || (m_run == -INFINITY && m_new != -INFINITY);
-      if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY) && warp_live) {
-        const float corr = grow && m_run != -INFINITY ? fast_exp2(m_run - m_new) : 1.f;
-        sm100::mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV_{t-1}
+      const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
+      if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
+        const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
+        sm100::mbar_wait(pv_done, (t - 1) & 1);  // O holds PV_{t-1}
         sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
@@ -619,16 +636,17 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
         l_run *= corr;
       }
       if (grow) m_run = m_new;
-      const float base = m_run == -INFINITY ? 0.f : m_run;
+      const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
       float rs = 0.f;
-      if (t >= 2) sm100::mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);  // P buffer t&1 drained by PV_{t-2}
-      uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
+      if (t >= 1) sm100::mbar_wait(pv_done, (t - 1) & 1);  // the P buffer was read by PV_{t-1}
+      uint8_t* pb = sm + L::kP;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // 8 keys -> one 16-byte swizzled chunk at a time (few live registers)
         uint32_t pk[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(sv[c * 8 + 2 * e] - base), p1 = fast_exp2(sv[c * 8 + 2 * e + 1] - base);
+          const float p0 = fast_exp2(fmaf(sv[c * 8 + 2 * e], sc, nb));
+          const float p1 = fast_exp2(fmaf(sv[c * 8 + 2 * e + 1], sc, nb));
           rs += p0 + p1;
           pk[e] = pack_bf16(p0, p1);
         }
@@ -637,13 +655,13 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       l_run += rs;
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&p_full[t & 1]);
+      sm100::mbar_arrive(p_full);
     }
     if (tid == 0) ATTN_TRACE(3);
     // final O
-    sm100::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    sm100::mbar_wait(pv_done, (n_tiles - 1) & 1);
     sm100::tc_fence_after();
-    if (warp_live) {
+    {
       const int pr = qt * kQT + r;
       const int tok = live ? pr / G : 0, head = kvh * G + (live ? pr % G : 0);
       const int64_t grow_ = row0 + tok;
@@ -674,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
             __stcg(reinterpret_cast<float4*>(dst + q * 4),
                    make_float4(__uint_as_float(ov[q * 4]), __uint_as_float(ov[q * 4 + 1]),
                                __uint_as_float(ov[q * 4 + 2]), __uint_as_float(ov[q * 4 + 3])));
-          if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run, l_run));
+          if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run * sc, l_run));
         }
       }
     }

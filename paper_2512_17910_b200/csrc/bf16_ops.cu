@@ -127,12 +127,14 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
                                                                int nparts, int64_t pstride,
                                                                const int32_t* __restrict__ rows, int d,
                                                                const float* __restrict__ w, float eps,
-                                                               __nv_bfloat16* __restrict__ out) {
+                                                               __nv_bfloat16* __restrict__ out,
+                                                               unsigned long long* __restrict__ zero_rows) {
   pdl_wait();
   pdl_trigger();
   __shared__ float red[32];
   const int r = blockIdx.x;
   const int src = rows ? rows[r] : r;
+  if (zero_rows && threadIdx.x == 0) zero_rows[r] = 0ull;  // the lm_head's fused argmax accumulates here
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)src * d);
   const int n4 = d >> 2;
   float4 v[V];
@@ -141,10 +143,12 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
   for (int j = 0; j < V; ++j) {
     const int i = threadIdx.x + j * 256;
     if (i < n4) {
-      const float4 acc = sum_parts4(part + (int64_t)src * d + 4 * i, pstride, nparts);
       float4 xv = xr[i];
-      xv.x += acc.x; xv.y += acc.y; xv.z += acc.z; xv.w += acc.w;
-      xr[i] = xv;
+      if (nparts > 0) {
+        const float4 acc = sum_parts4(part + (int64_t)src * d + 4 * i, pstride, nparts);
+        xv.x += acc.x; xv.y += acc.y; xv.z += acc.z; xv.w += acc.w;
+        xr[i] = xv;
+      }
       v[j] = xv;
     } else {
       v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -170,16 +174,21 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
 }
 
 int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, const int32_t* rows, int n_rows, int d,
-                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st) {
+                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st,
+                          unsigned long long* zero_rows) {
   if (n_rows == 0) return ALORA_OK;
-  if (nparts < 1 || partials == nullptr) return rmsnorm_bf16(x, rows, n_rows, d, w, eps, out, st);
-  if (d % 4 != 0 || d > 8192 || nparts > 8) return ALORA_EINVAL;
+  if (partials == nullptr) nparts = 0;
+  if (d % 4 != 0 || d > 8192) {
+    if (nparts > 0 || zero_rows) return ALORA_EINVAL;
+    return rmsnorm_bf16(x, rows, n_rows, d, w, eps, out, st);
+  }
+  if (nparts > 8) return ALORA_EINVAL;
   const int v = (d / 4 + 255) / 256;
   const int64_t ps = (int64_t)M * d;
-  if (v <= 1) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<1>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
-  else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
-  else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
-  else ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out));
+  if (v <= 1) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<1>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
+  else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
+  else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
+  else ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }

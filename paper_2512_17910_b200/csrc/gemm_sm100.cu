@@ -65,6 +65,7 @@ struct GemmArgs {
   const uint8_t* sel_row_apply;
   const uint8_t* sel_targets;
   int sel_sr, sel_rank;
+  unsigned long long* argmax;  // fused greedy argmax of the fp32-store epilogue (ws kernel, S == 1)
   int splits;                 // K splits (blockIdx.z); grid <= SM count, cooperative launch
   float* partial;             // [splits][m_tiles*128][N] fp32 when splits > 1
   int* counters;              // 2 per output tile (arrive, depart); zero between launches
@@ -644,8 +645,26 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
       const bool quarter_live = mt * kBM + quarter * 32 < args.M;
       if (S == 1) {
         const int units = units_per_row<BN>(args, n0);
-        if (quarter_live)
-          for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, trow, u, tmem_fetch);
+        if (quarter_live) {
+          if (args.argmax != nullptr) {
+            unsigned long long best = 0ull;
+            auto fetch_am = [&](int c0, float (&v)[32]) {
+              tmem_fetch(c0, v);
+#pragma unroll
+              for (int j = 0; j < 32; ++j) {
+                uint32_t u32 = __float_as_uint(v[j]);
+                u32 = (u32 & 0x80000000u) ? ~u32 : (u32 | 0x80000000u);
+                const unsigned long long key =
+                    ((unsigned long long)u32 << 32) | (0xFFFFFFFFu - (uint32_t)(n0 + c0 + j));
+                best = key > best ? key : best;
+              }
+            };
+            for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, trow, u, fetch_am);
+            if (trow < args.M) atomicMax(args.argmax + trow, best);
+          } else {
+            for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, trow, u, tmem_fetch);
+          }
+        }
       } else if (quarter_live) {
         // deferred split-K: this split's fp32 partial rows -> partial[split][row][n]; the consuming kernel
         // (residual RMSNorm / QKV finalize) sums the splits in order and applies the epilogue
@@ -740,28 +759,34 @@ struct WsChoice {
   double cost = 1e30;
 };
 
-// Modelled time of one weight-streaming launch: per-wave SM ingest (activations + weight slab; at most
-// ~170 GB/s per SM, and no more than the stage ring's bytes in flight per ~1.2 us of loaded latency)
-// against the HBM stream of the weights. K splits (S > 1) are only planned when the caller can defer the
-// reduction to the consuming kernel; that consumer re-reads S fp32 partials from L2.
+// Modelled time of one weight-streaming launch. A CTA moves weight bytes at most at
+//   min(SM ingest ~170 GB/s, stage-ring bytes in flight / ~1.2 us loaded latency) x BN / (BN + token rows)
+// capped at the ~60 GB/s a CTA was measured to sustain; the launch is further bounded by HBM. K splits (S > 1) are only planned when the caller can defer the
+// reduction to the consuming kernel, which then re-reads S fp32 partials from L2.
 template <int BN, int MT>
 void ws_consider(WsChoice& best, int M, int N, int K, bool can_defer, int64_t defer_cap) {
   using C = WsCfg<BN, MT>;
   const int nkb = (K + kBK - 1) / kBK;
   const int tiles = N / BN;
+  const double mrows = std::min(M, MT * kBM);
   for (int S = 1; S <= kMaxSplits; ++S) {
     if (S > 1 && (!can_defer || (int64_t)S * M * N * 4 > defer_cap)) break;
     if (S > nkb) break;
     const int per = (nkb + S - 1) / S;
     if ((nkb + per - 1) / per != S) continue;  // no empty trailing splits
-    const int waves = (tiles * S + kNumSMs - 1) / kNumSMs;
-    const double ingest = (double)(std::min(M, MT * kBM) + BN) * per * kBK * 2.0;
-    const double inflight = (double)C::kStages * (std::min(M, MT * kBM) + BN) * kBK * 2.0;
-    const double rate = std::min(170e9, inflight / 1.2e-6);
-    double t = waves * (ingest / rate + 1.5e-6);
-    t = std::max(t, (double)N * K * 2.0 / 6.5e12 + 1.5e-6);
+    const int ctas = tiles * S;
+    const int waves = (ctas + kNumSMs - 1) / kNumSMs;
+    const int active = std::min(ctas, kNumSMs);
+    const double inflight = (double)C::kStages * (mrows + BN) * kBK * 2.0;
+    const double ingest_rate = std::min(170e9, inflight / 1.2e-6);
+    // measured on the B200: a lone weight-streaming CTA sustains ~30-60 GB/s of weights, so the SM count
+    // engaged matters more than the tile shape
+    const double w_rate = std::min(ingest_rate * BN / (BN + mrows), 60e9);
+    const double wbytes = (double)N * K * 2.0;
+    (void)active;
+    double t = std::max(waves * ((double)BN * per * kBK * 2.0 / w_rate), wbytes / 6.5e12) + waves * 1.5e-6;
     if (S > 1) t += (double)S * M * N * 4.0 / 8e12 + 0.3e-6;
-    if (t < best.cost) {
+    if (t < best.cost * 0.97) {  // prefer the first (wider) tile unless clearly faster
       best.cost = t;
       best.bn = BN;
       best.splits = S;
@@ -843,6 +868,10 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.rope_sin = lora->rope_sin;
     args.rope_cols = lora->rope_cols;
     args.head_dim = lora->head_dim;
+  }
+  if (lora && lora->argmax) {
+    if (epi != (kEpiStore | 16) || M > 2 * kBM) return ALORA_EINVAL;
+    args.argmax = lora->argmax;
   }
   if (base_epi == kEpiLoraSelect) {
     if (!lora || !lora->sel_row_slot || !lora->sel_row_apply || !lora->sel_targets || lora->sel_sr % 32 ||

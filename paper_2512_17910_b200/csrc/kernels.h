@@ -79,6 +79,9 @@ struct GemmLora {
   const uint8_t* sel_targets = nullptr;
   int sel_sr = 0;
   int sel_rank = 0;
+  // fp32-store epilogue of a weight-streaming launch: per row, atomicMax of (orderable logit << 32 | ~col),
+  // i.e. the greedy token with ties to the lowest id (model.py:190-195), fused into the lm_head
+  unsigned long long* argmax = nullptr;
 };
 // Split-K scratch: fp32 partial rows + 2 arrival counters per output tile (zeroed once, self-resetting).
 constexpr int kGemmCounters = 16384;
@@ -114,8 +117,11 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
               int M, int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws = nullptr,
               int max_splits = 8, GemmDefer* defer = nullptr);
 // x[r] (+)= sum_p partials[p][r] (split order), then out[r] = bf16(rmsnorm(x[r]) * w); rows as rmsnorm_bf16.
+// zero_rows (optional, [n_rows]) is cleared: the packed argmax accumulator of the lm_head that follows.
 int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, const int32_t* rows, int n_rows, int d,
-                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st);
+                          const float* w, float eps, __nv_bfloat16* out, cudaStream_t st,
+                          unsigned long long* zero_rows = nullptr);
+int argmax_unpack(const unsigned long long* packed, int rows, int32_t* out_ids, cudaStream_t st);
 // qkv[m] = bf16(RoPE(sum_p partials[p][m])) on q/k heads (plain sum on v), and the row's k/v scattered into
 // the paged pool (the kv_write of the step) -- the deferred epilogue of a split-K QKV projection.
 int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv, int D, const int32_t* positions,

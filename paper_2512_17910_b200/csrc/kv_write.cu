@@ -125,6 +125,22 @@ void configure_kv_ops() {
   prefer_max_smem(argmax_kernel);
 }
 
+// next_ids[r] from the packed (orderable value, ~index) maxima the lm_head epilogue accumulated.
+__global__ void argmax_unpack_kernel(const unsigned long long* __restrict__ packed, int rows, int32_t* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r < rows) out[r] = (int32_t)(0xFFFFFFFFu - (uint32_t)(packed[r] & 0xFFFFFFFFull));
+}
+
+int argmax_unpack(const unsigned long long* packed, int rows, int32_t* out_ids, cudaStream_t st) {
+  if (rows <= 0) return ALORA_OK;
+  ALORA_CUDA_CHECK(launch_pdl(argmax_unpack_kernel, dim3((rows + 127) / 128), dim3(128), 0, st, nullptr, 0, packed,
+                              rows, out_ids));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
 int argmax_rows(const float* logits, int rows, int vocab, int32_t* out_ids, cudaStream_t st) {
   if (rows == 0) return ALORA_OK;
   if (vocab <= 0) return ALORA_EINVAL;

@@ -88,7 +88,7 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Workspace carve-up shared by alora_model_workspace_bytes and the executor.
 struct Ws {
-  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, part, total;
+  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, part, amax, total;
   int64_t part_bytes;
   int64_t attn_ws_bytes, gemm_ws_bytes;
 };
@@ -120,6 +120,7 @@ Ws plan_ws(const AloraModelDesc& d) {
   // deferred split-K partials of the weight-streaming GEMMs (M <= 256): [<= 8 splits][M][max(Nqkv, d)] fp32
   w.part_bytes = d.dtype == ALORA_BF16 ? 8LL * std::min<int64_t>(T, 256) * std::max<int64_t>(nq + 2 * nkv, d.d_model) * 4 : 0;
   w.part = take(w.part_bytes);
+  w.amax = take(S * 8);  // packed greedy argmax per span (fused into the lm_head epilogue)
   w.total = off;
   return w;
 }
@@ -324,12 +325,21 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
                   st, gw, 8, &dfm));
     pend = dfm.splits_out > 1 ? dfm.splits_out : 0;
   }
+  // greedy argmax fused into the lm_head epilogue (weight-streaming path: S <= 256 spans, vocab % 32 == 0)
+  auto* amax = reinterpret_cast<unsigned long long*>(base + w.amax);
+  const bool fused_argmax = S <= 256 && d.vocab % 32 == 0;
   RUN("rmsnorm", S_ * dm_ * (6 + 8.0 * pend), 0,
-      residual_rmsnorm_bf16(x, part, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st));
+      residual_rmsnorm_bf16(x, part, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st,
+                            fused_argmax ? amax : nullptr));
+  GemmLora glm;
+  glm.argmax = fused_argmax ? amax : nullptr;
   RUN("gemm_lm_head", gemm_bytes(S_, V_, dm_, 4, false), 2.0 * S_ * V_ * dm_,
       gemm_bf16(kEpiStore + 16 /* fp32 out */, hf, dm, static_cast<const __nv_bfloat16*>(d.unembed_t), dm, s.logits,
-                d.vocab, S, d.vocab, dm, nullptr, st, gw));
-  RUN("argmax", S_ * V_ * 4, 0, argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
+                d.vocab, S, d.vocab, dm, fused_argmax ? &glm : nullptr, st, gw));
+  if (fused_argmax)
+    RUN("argmax", S_ * 12.0, 0, argmax_unpack(amax, S, s.next_ids, st));
+  else
+    RUN("argmax", S_ * V_ * 4, 0, argmax_rows(s.logits, S, d.vocab, s.next_ids, st));
 #undef RUN
   mdl.last_launches = run.n;
   return ALORA_OK;
