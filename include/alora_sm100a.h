@@ -129,6 +129,12 @@ int alora_argmax(const float* logits, int32_t rows, int32_t vocab, int32_t* out_
 
 /* ------------------------------------------------------ native executor ---- */
 
+/* Tensor-parallel all-reduce hook (sum, in place) of `count` fp32 values at device pointer `buf`,
+ * stream-ordered on `stream`. alora_model_forward calls it twice per layer when tp_size > 1: on the
+ * row-parallel O-projection output and on the MLP-down output, before the residual add + RMSNorm
+ * (reference model.py:269-271, sharded as in SURVEY.md §8(e)). Returns 0 on success. */
+typedef int32_t (*alora_allreduce_fn)(void* ctx, float* buf, int64_t count, void* stream);
+
 /* Model description: shapes plus device pointers (caller-owned). Per-layer
  * pointers are arrays of n_layers device pointers living in HOST memory. */
 typedef struct AloraModelDesc {
@@ -161,6 +167,11 @@ typedef struct AloraModelDesc {
   /* workspace (caller-owned device memory, >= alora_model_workspace_bytes) */
   void* workspace;
   int64_t workspace_bytes;
+  /* tensor parallelism (bf16 tier): this rank holds n_heads / n_kv_heads / ffn_dim of a tp_size-way
+   * sharded model (column-parallel q|k|v and gate|up, row-parallel o and down); 0 or 1 = unsharded */
+  int32_t tp_size;
+  void* tp_ctx;
+  alora_allreduce_fn tp_allreduce;
 } AloraModelDesc;
 
 /* One engine step: all spans packed back to back (varlen). Device arrays. */

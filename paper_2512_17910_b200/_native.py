@@ -53,7 +53,12 @@ class AloraModelDesc(ctypes.Structure):
         ("slot_targets", c_void_p),
         ("kv_pool", c_void_p), ("total_blocks", c_i32), ("block_size", c_i32),
         ("workspace", c_void_p), ("workspace_bytes", c_i64),
+        ("tp_size", c_i32), ("tp_ctx", c_void_p), ("tp_allreduce", c_void_p),
     ]
+
+
+# int32_t (*alora_allreduce_fn)(void* ctx, float* buf, int64_t count, void* stream)
+ALLREDUCE_FN = ctypes.CFUNCTYPE(c_i32, c_void_p, c_void_p, c_i64, c_void_p)
 
 
 class AloraStepDesc(ctypes.Structure):

@@ -2,6 +2,8 @@
 // embedding gather, RMSNorm -> bf16 GEMM operand, RoPE, the segmented LoRA
 // shrink and the per-tile adapter masks that let the GEMM skip absent adapters.
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -189,6 +191,24 @@ int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, co
   else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
   else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
   else ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+__global__ void __launch_bounds__(256) sum_partials_kernel(const float* __restrict__ part, int nparts, int64_t n4,
+                                                           float* __restrict__ out) {
+  pdl_wait();
+  pdl_trigger();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x)
+    reinterpret_cast<float4*>(out)[i] = sum_parts4(part + 4 * i, 4 * n4, nparts);
+}
+
+int sum_partials_f32(const float* partials, int nparts, int64_t n, float* out, cudaStream_t st) {
+  if (n == 0) return ALORA_OK;
+  if (nparts < 1 || nparts > 8 || n % 4) return ALORA_EINVAL;
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 4 * kNumSMs);
+  ALORA_CUDA_CHECK(launch_pdl(sum_partials_kernel, dim3(grid), dim3(256), 0, st, nullptr, 0, partials, nparts, n4, out));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -430,6 +450,7 @@ void configure_bf16_ops() {
   prefer_max_smem(residual_rmsnorm_kernel<8>);
   prefer_max_smem(qkv_finalize_kernel);
   prefer_max_smem(lora_select_finalize_kernel);
+  prefer_max_smem(sum_partials_kernel);
 }
 
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st) {

@@ -121,6 +121,8 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
 int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, const int32_t* rows, int n_rows, int d,
                           const float* w, float eps, __nv_bfloat16* out, cudaStream_t st,
                           unsigned long long* zero_rows = nullptr);
+// out[i] = sum_p partials[p * n + i] in split order (n % 4 == 0): the local split-K sum before a TP all-reduce.
+int sum_partials_f32(const float* partials, int nparts, int64_t n, float* out, cudaStream_t st);
 int argmax_unpack(const unsigned long long* packed, int rows, int32_t* out_ids, cudaStream_t st);
 // qkv[m] = bf16(RoPE(sum_p partials[p][m])) on q/k heads (plain sum on v), and the row's k/v scattered into
 // the paged pool (the kv_write of the step) -- the deferred epilogue of a split-K QKV projection.

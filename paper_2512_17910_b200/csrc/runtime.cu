@@ -88,7 +88,7 @@ inline int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
 
 // Workspace carve-up shared by alora_model_workspace_bytes and the executor.
 struct Ws {
-  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, part, amax, total;
+  int64_t x, h, qkv, attn, gu, act, s, masks, hf, attn_ws, gemm_ws, part, amax, tpd, total;
   int64_t part_bytes;
   int64_t attn_ws_bytes, gemm_ws_bytes;
 };
@@ -121,6 +121,7 @@ Ws plan_ws(const AloraModelDesc& d) {
   w.part_bytes = d.dtype == ALORA_BF16 ? 8LL * std::min<int64_t>(T, 256) * std::max<int64_t>(nq + 2 * nkv, d.d_model) * 4 : 0;
   w.part = take(w.part_bytes);
   w.amax = take(S * 8);  // packed greedy argmax per span (fused into the lm_head epilogue)
+  w.tpd = take(d.tp_size > 1 ? T * d.d_model * 4 : 0);  // TP: this rank's residual delta, all-reduced in place
   w.total = off;
   return w;
 }
@@ -137,6 +138,7 @@ int validate(const AloraModelDesc* d) {
     return ALORA_EINVAL;
   if (d->n_slots < 0 || d->lora_rank < 0 || (d->n_slots > 0 && d->lora_rank < 1)) return ALORA_EINVAL;
   if (d->dtype == ALORA_BF16 && d->n_slots > 32) return ALORA_EINVAL;  // tile slot masks are 32-bit
+  if (d->tp_size > 1 && (d->dtype != ALORA_BF16 || d->tp_allreduce == nullptr)) return ALORA_EINVAL;
   return ALORA_OK;
 }
 
@@ -239,13 +241,38 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const GemmWs gws = gemm_ws_from(base + w.gemm_ws, w.gemm_ws_bytes);
   const GemmWs* gw = &gws;  // split-K scratch of the per-tile GEMM (M > 256)
   float* part = reinterpret_cast<float*>(base + w.part);  // deferred split-K partials (M <= 256)
-  int pend = 0;  // splits of the residual update still pending in `part` (applied by the next RMSNorm)
+  int pend = 0;  // splits of the residual update still pending in `pend_buf` (applied by the next RMSNorm)
+  const float* pend_buf = part;
+
   const int M = s.n_tokens, S = s.n_seqs, dm = d.d_model, F = d.ffn_dim;
   const int H = d.n_heads, Hkv = d.n_kv_heads, D = d.head_dim;
   const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
   const bool llama = d.arch == ALORA_ARCH_LLAMA;
   const bool lora = d.n_slots > 0;
   Launcher run{mdl, st};
+  const bool tp = d.tp_size > 1;
+  float* tpd = reinterpret_cast<float*>(base + w.tpd);
+  // Residual-producing GEMM (O-projection, MLP-down). Unsharded: x += A.W^T fused in the epilogue, or the
+  // split-K partials are left for the next RMSNorm. Tensor parallel: this rank's partial product is
+  // materialised in tpd (split-K summed in order), all-reduced by the caller's hook, then applied by the
+  // RMSNorm as a single pending partial (row-parallel linear layer + all-reduce).
+  auto residual_gemm = [&](const __nv_bfloat16* A, int K, const void* W, int ldw) -> int {
+    GemmDefer df;
+    df.partial = part;
+    df.capacity = w.part_bytes;
+    if (!tp) {
+      const int rc = gemm_bf16(kEpiAdd, A, K, static_cast<const __nv_bfloat16*>(W), ldw, x, dm, M, dm, K, nullptr,
+                               st, gw, 8, &df);
+      pend = df.splits_out > 1 ? df.splits_out : 0;
+      pend_buf = part;
+      return rc;
+    }
+    int rc = gemm_bf16(kEpiStore | 16, A, K, static_cast<const __nv_bfloat16*>(W), ldw, tpd, dm, M, dm, K, nullptr,
+                       st, gw, 8, nullptr);
+    pend = 1;
+    pend_buf = tpd;
+    return rc;
+  };
   int rc;
   const double m_ = M, dm_ = dm, F_ = F, Nqkv_ = Nqkv, Nq_ = Nq, V_ = d.vocab, S_ = S, ks_ = (double)d.n_slots * d.lora_rank;
   // algorithmic bytes of a bf16 GEMM: A + B read once, C written (and read for +=)
@@ -262,7 +289,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   if (lora) RUN("lora_masks", m_ * 5, 0, lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
   for (int l = 0; l < d.n_layers; ++l) {
     RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
-        residual_rmsnorm_bf16(x, part, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+        residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     pend = 0;
     GemmLora gl;
     if (lora) {
@@ -303,33 +330,25 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
         attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
                   static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
                   aws, w.attn_ws_bytes, st, d.total_blocks));
-    GemmDefer dfo;
-    dfo.partial = part;
-    dfo.capacity = w.part_bytes;
     RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
-        gemm_bf16(kEpiAdd, attn, Nq, static_cast<const __nv_bfloat16*>(mdl.w_o_t[l]), Nq, x, dm, M, dm, Nq, nullptr,
-                  st, gw, 8, &dfo));
-    pend = dfo.splits_out > 1 ? dfo.splits_out : 0;
+        residual_gemm(attn, Nq, mdl.w_o_t[l], Nq));
+    if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
     RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
-        residual_rmsnorm_bf16(x, part, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+        residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
     pend = 0;
     const double n_in = llama ? 2 * F_ : F_;
     RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2, 2.0 * m_ * n_in * dm_,
         gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act, F,
                   M, llama ? 2 * F : F, dm, nullptr, st, gw));
-    GemmDefer dfm;
-    dfm.partial = part;
-    dfm.capacity = w.part_bytes;
     RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true), 2.0 * m_ * dm_ * F_,
-        gemm_bf16(kEpiAdd, act, F, static_cast<const __nv_bfloat16*>(mdl.w_out_t[l]), F, x, dm, M, dm, F, nullptr,
-                  st, gw, 8, &dfm));
-    pend = dfm.splits_out > 1 ? dfm.splits_out : 0;
+        residual_gemm(act, F, mdl.w_out_t[l], F));
+    if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
   }
   // greedy argmax fused into the lm_head epilogue (weight-streaming path: S <= 256 spans, vocab % 32 == 0)
   auto* amax = reinterpret_cast<unsigned long long*>(base + w.amax);
   const bool fused_argmax = S <= 256 && d.vocab % 32 == 0;
   RUN("rmsnorm", S_ * dm_ * (6 + 8.0 * pend), 0,
-      residual_rmsnorm_bf16(x, part, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st,
+      residual_rmsnorm_bf16(x, pend_buf, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st,
                             fused_argmax ? amax : nullptr));
   GemmLora glm;
   glm.argmax = fused_argmax ? amax : nullptr;

@@ -287,6 +287,9 @@ class Model:
         bank = self._bank
         D.n_slots = 0 if bank is None else bank["n"]
         D.lora_rank = 0 if bank is None else bank["rank"]
+        tp = getattr(self, "_tp", None)  # (size, allreduce hook address): set by tp.TPModel
+        if tp is not None:
+            D.tp_size, D.tp_allreduce = tp
         if probe:
             return D
         D.embed, D.unembed_t = self.embed.data_ptr(), self.unembed_t.data_ptr()
