@@ -22,6 +22,7 @@ from .model import (BaseWeights, LayerWeights, Model, ModelConfig, SeqInput, gen
 from .pipeline import (PipelineSpec, build_engine, end_of_turn_token, invocation_for, random_conversation,
                        run_sync_pipeline)
 from .scheduler import Request, RequestState, ScheduledSpan, Scheduler, SchedulerConfig
+from .replicas import gather_replica_rows, replica_instances, run_replica_pipeline
 from .tp import ThreadGroup, TorchDistGroup, TPModel, shard_adapter, shard_config, shard_weights
 
 __version__ = "0.1.0"

@@ -92,26 +92,32 @@ def run_phase(engine: Engine, submits) -> None:
     engine.run_until_idle()
 
 
-def pipeline_phases(spec: PipelineSpec, engine: Engine, rid_prefix: str = ""):
-    """Yield (stage, submits) per phase; each phase's prompts depend on the previous phase's outputs."""
+def pipeline_phases(spec: PipelineSpec, engine: Engine, rid_prefix: str = "", instances=None):
+    """Yield (stage, submits) per phase; each phase's prompts depend on the previous phase's outputs.
+
+    `instances` (replicas.py) restricts the run to a subset of the spec's pipeline instances; the
+    conversations are still drawn for all `spec.batch` instances, so instance i is the same on every
+    replica count.
+    """
     base_first, has_final, n_eval = pipeline_shape(spec)
     V = engine.config.model.vocab_size
     eot = end_of_turn_token(V)
     rng = np.random.default_rng(spec.seed)
     convs = [random_conversation(rng, spec.prompt_len, V) for _ in range(spec.batch)]
+    mine = list(range(spec.batch)) if instances is None else [int(i) for i in instances]
     meta = lambda stage, i: {"pipeline": spec.pipeline, "mode": spec.mode, "stage": stage, "instance": i}
     inv = {k: np.asarray(engine.adapters[f"adapter{k}"].invocation_tokens, dtype=np.int64) for k in range(n_eval)}
     if base_first:
         yield "base", [(_rid(rid_prefix, i, "base"), convs[i], None, spec.gen_len, meta("base", i))
-                       for i in range(spec.batch)]
-        for i in range(spec.batch):
+                       for i in mine]
+        for i in mine:
             gen = engine.finished[_rid(rid_prefix, i, "base")].generated
             convs[i] = np.concatenate([convs[i], np.asarray(gen, dtype=np.int64), [eot]])
     yield "eval", [(_rid(rid_prefix, i, f"eval{k}"), np.concatenate([convs[i], inv[k]]), f"adapter{k}",
-                    spec.adapter_gen_len, meta("eval", i)) for i in range(spec.batch) for k in range(n_eval)]
+                    spec.adapter_gen_len, meta("eval", i)) for i in mine for k in range(n_eval)]
     if has_final:
         finals = []
-        for i in range(spec.batch):
+        for i in mine:
             parts = [convs[i]]
             for k in range(n_eval):
                 out = np.asarray(engine.finished[_rid(rid_prefix, i, f"eval{k}")].generated, dtype=np.int64)
