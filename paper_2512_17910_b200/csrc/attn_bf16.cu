@@ -60,6 +60,7 @@ struct AttnArgs {
   int* counters; // [n_seqs * Hkv * n_qtiles], zero between launches
   unsigned long long* trace;  // optional per-CTA %globaltimer stamps (ALORA_ATTN_TRACE=1)
   int M;
+  int exp;  // debug experiments (ALORA_ATTN_EXP): 3 = softmax skips its math (timing only)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
@@ -404,7 +405,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // the per-tile period is that over kNS; D=64 keeps the CTA at ~98 KB of smem (4 stages, one P buffer) so
 // two CTAs (two independent softmax chains) share an SM.
 template <int D>
-constexpr int kNS = 4;
+constexpr int kNS = 3;
+// S runs two tiles ahead of the softmax (three S buffers in TMEM) and P is double-buffered in smem, so
+// neither the softmax nor the MMA warp waits on the other's previous step (the per-tile chain was the
+// bound: S MMA -> commit -> softmax -> P -> PV -> commit, ~1 us per 64-key tile with one buffer each).
+constexpr int kSBuf = 3;
 constexpr int kThreads = 192;   // 4 softmax + 1 producer + 1 MMA warps
 constexpr float kRescaleLog2 = 8.f;
 
@@ -417,7 +422,7 @@ struct Smem {
   static constexpr int kK = kQ + kQBytes;
   static constexpr int kV = kK + kNS<D> * kKVBytes;
   static constexpr int kP = kV + kNS<D> * kKVBytes;
-  static constexpr int kBar = kP + kPBytes;  // one P buffer: P_{t+1} is written after PV_t has read P_t
+  static constexpr int kBar = kP + 2 * kPBytes;  // two P buffers
   static constexpr int kTotal = kBar + 256 + 1024;  // barriers + TMEM slot + alignment slack
 };
 
@@ -436,10 +441,10 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   uint64_t* q_full = bars;             // 1
   uint64_t* kv_full = bars + 1;        // kNS<D>
   uint64_t* kv_empty = kv_full + kNS<D>;  // kNS<D>
-  uint64_t* s_full = kv_empty + kNS<D>;   // 2
-  uint64_t* p_full = s_full + 2;       // 1
-  uint64_t* pv_done = p_full + 1;      // 1 (completes once per tile)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 1);
+  uint64_t* s_full = kv_empty + kNS<D>;   // kSBuf
+  uint64_t* p_full = s_full + kSBuf;   // 2
+  uint64_t* pv_done = p_full + 2;      // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
   __shared__ int s_last;
 
   const int G = a.H / a.Hkv;
@@ -468,19 +473,21 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
     }
-    sm100::mbar_init(&s_full[0], 1);
-    sm100::mbar_init(&s_full[1], 1);
-    sm100::mbar_init(p_full, 32 * live_warps);
-    sm100::mbar_init(pv_done, 1);
+    for (int i = 0; i < kSBuf; ++i) sm100::mbar_init(&s_full[i], 1);
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&p_full[i], 32 * live_warps);
+      sm100::mbar_init(&pv_done[i], 1);
+    }
     sm100::fence_barrier_init();
   }
-  if (warp == 5) sm100::tmem_alloc<256>(tmem_slot);
+  if (warp == 5) sm100::tmem_alloc<(D == 64 ? 256 : 512)>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tS[2] = {tmem, tmem + 64};
-  const uint32_t tO = tmem + 128;
+  // TMEM: D=64 -> S0 | S1 | O | S2 in 256 columns; D=128 -> S0 | S1 | S2 | - | O in 512
+  const uint32_t tO = tmem + (D == 64 ? 128 : 256);
+  const uint32_t tS[kSBuf] = {tmem, tmem + 64, tmem + (D == 64 ? 192 : 128)};
 
   // Producer and MMA loops run warp-converged with one elected lane per operation (see gemm_ws_kernel).
   if (warp == 4) {
@@ -543,41 +550,58 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     sm100::mbar_wait(q_full, 0);
     if (lane == 0) ATTN_TRACE(1);
     sm100::tc_fence_after();
-    auto issue_s = [&](int t) {
-      const int st = t % kNS<D>;
-      sm100::mbar_wait(&kv_full[st], (t / kNS<D>) & 1);
-      sm100::tc_fence_after();
-      if (sm100::elect_one()) {
-        const uint8_t* qb = sm + L::kQ;
-        const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
+    // Event-driven issue (no head-of-line blocking): S_ts needs its K tile and a free S buffer (ts%3 was read by
+    // softmax_{ts-3}, observed as p_full when PV_{ts-3} was issued: ts <= tp + 2); PV_tp needs P_tp.
+    int ts = 0, tp = 0;
+    while (tp < n_tiles) {
+      bool did = false;
+      if (ts < n_tiles && ts <= tp + 2) {
+        const int st = ts % kNS<D>;
+        uint32_t ready = 0;
+        if (lane == 0) ready = sm100::mbar_test(&kv_full[st], (ts / kNS<D>) & 1) ? 1u : 0u;
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready) {
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+            const uint8_t* qb = sm + L::kQ;
+            const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks) {  // K = D in 16-wide steps; sub-tile every 4 steps
-          const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
-          const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
-          sm100::mma_bf16_ss(tS[t & 1], da, db, idesc_s, ks > 0 ? 1u : 0u);
+            for (int ks = 0; ks < D / 16; ++ks) {  // K = D in 16-wide steps; sub-tile every 4 steps
+              const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
+              const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
+              sm100::mma_bf16_ss(tS[ts % kSBuf], da, db, idesc_s, ks > 0 ? 1u : 0u);
+            }
+            sm100::mma_commit(&s_full[ts % kSBuf]);
+          }
+          __syncwarp();
+          ++ts;
+          did = true;
         }
-        sm100::mma_commit(&s_full[t & 1]);
       }
-      __syncwarp();
-    };
-    issue_s(0);
-    for (int t = 0; t < n_tiles; ++t) {
-      if (t + 1 < n_tiles) issue_s(t + 1);  // S buffer (t+1)&1 was drained: p_full for t-1 was awaited
-      sm100::mbar_wait(p_full, t & 1);
-      sm100::tc_fence_after();
-      if (sm100::elect_one()) {
-        const uint8_t* pb = sm + L::kP;
-        const uint8_t* vb = sm + L::kV + (t % kNS<D>) * L::kKVBytes;
+      if (tp < ts) {
+        uint32_t ready = 0;
+        if (lane == 0) ready = sm100::mbar_test(&p_full[tp & 1], (tp >> 1) & 1) ? 1u : 0u;
+        ready = __shfl_sync(0xffffffffu, ready, 0);
+        if (ready) {
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+            const uint8_t* pb = sm + L::kP + (tp & 1) * L::kPBytes;
+            const uint8_t* vb = sm + L::kV + (tp % kNS<D>) * L::kKVBytes;
 #pragma unroll
-        for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
-          const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
-          const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
-          sm100::mma_bf16_ss(tO, da, db, idesc_o, (t > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
+              const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
+              const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
+              sm100::mma_bf16_ss(tO, da, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
+            }
+            sm100::mma_commit(&pv_done[tp & 1]);
+            sm100::mma_commit(&kv_empty[tp % kNS<D>]);
+          }
+          __syncwarp();
+          ++tp;
+          did = true;
         }
-        sm100::mma_commit(pv_done);
-        sm100::mma_commit(&kv_empty[t % kNS<D>]);
       }
-      __syncwarp();
+      if (!did) __nanosleep(32);
     }
   } else if (warp < live_warps) {
     // ------------------------------------------------------------------ softmax (live warps of 0-3)
@@ -594,14 +618,19 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < n_tiles; ++t) {
       const int k0 = key_begin + t * kKT;
-      sm100::mbar_wait(&s_full[t & 1], (t >> 1) & 1);
+      sm100::mbar_wait(&s_full[t % kSBuf], (t / kSBuf) & 1);
       sm100::tc_fence_after();
+      if (a.exp == 3) {  // timing experiment: no softmax work at all
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&p_full[t & 1]);
+        continue;
+      }
       if (t == 0 && tid == 0) ATTN_TRACE(2);
       float sv[kKT];
       {
         uint32_t r0[32], r1[32];
-        sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base, r0);
-        sm100::tmem_ld_32x32b_x32(tS[t & 1] + lane_base + 32, r1);
+        sm100::tmem_ld_32x32b_x32(tS[t % kSBuf] + lane_base, r0);
+        sm100::tmem_ld_32x32b_x32(tS[t % kSBuf] + lane_base + 32, r1);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
@@ -609,19 +638,26 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
           sv[j + 32] = __uint_as_float(r1[j]);
         }
       }
-      const bool need_mask = k0 + kKT - 1 > lim;
-      float mt = -INFINITY;
+      if (__any_sync(0xffffffffu, k0 + kKT - 1 > lim)) {  // causal / partition-end mask: warp-uniform branch
 #pragma unroll
-      for (int j = 0; j < kKT; ++j) {
-        if (need_mask && k0 + j > lim) sv[j] = -INFINITY;
-        mt = fmaxf(mt, sv[j]);
+        for (int j = 0; j < kKT; ++j)
+          if (k0 + j > lim) sv[j] = -INFINITY;
       }
+      float mx[8];  // 8 independent max chains, then a tree
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mx[q] = fmaxf(sv[q], sv[q + 8]);
+#pragma unroll
+      for (int j = 16; j < kKT; j += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], sv[j + q]);
+      }
+      const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
       const float m_new = fmaxf(m_run, mt);
       // lazy rescale: only when the max grew by more than 2^8 (or on the first finite max)
       const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
       if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
         const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
-        sm100::mbar_wait(pv_done, (t - 1) & 1);  // O holds PV_{t-1}
+        sm100::mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV_{t-1}
         sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
@@ -637,9 +673,9 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       }
       if (grow) m_run = m_new;
       const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
-      float rs = 0.f;
-      if (t >= 1) sm100::mbar_wait(pv_done, (t - 1) & 1);  // the P buffer was read by PV_{t-1}
-      uint8_t* pb = sm + L::kP;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      if (t >= 2) sm100::mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);  // P buffer t&1 was read by PV_{t-2}
+      uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
 #pragma unroll
       for (int c = 0; c < 8; ++c) {  // 8 keys -> one 16-byte swizzled chunk at a time (few live registers)
         uint32_t pk[4];
@@ -647,19 +683,19 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
         for (int e = 0; e < 4; ++e) {
           const float p0 = fast_exp2(fmaf(sv[c * 8 + 2 * e], sc, nb));
           const float p1 = fast_exp2(fmaf(sv[c * 8 + 2 * e + 1], sc, nb));
-          rs += p0 + p1;
+          rs4[e] += p0 + p1;
           pk[e] = pack_bf16(p0, p1);
         }
         *reinterpret_cast<int4*>(pb + sw_off(r, c, kQT)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
       }
-      l_run += rs;
+      l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
-      sm100::mbar_arrive(p_full);
+      sm100::mbar_arrive(&p_full[t & 1]);
     }
     if (tid == 0) ATTN_TRACE(3);
     // final O
-    sm100::mbar_wait(pv_done, (n_tiles - 1) & 1);
+    sm100::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
     sm100::tc_fence_after();
     {
       const int pr = qt * kQT + r;
@@ -699,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 5) sm100::tmem_dealloc<256>(tmem);
+  if (warp == 5) sm100::tmem_dealloc<(D == 64 ? 256 : 512)>(tmem);
   if (tid == 0) ATTN_TRACE(4);
   if (parts_here > 1) merge_partials<D>(a, s, kvh, qt, row0, start, rows_here, parts_here, G, &s_last);
   if (tid == 0) ATTN_TRACE(5);
@@ -755,6 +791,8 @@ int launch_attn(const AttnArgs& a, int n_seqs, int64_t kv_rows, cudaStream_t st)
     static unsigned long long* tbuf = nullptr;
     const int n_ctas = grid.x * grid.y * grid.z;
     AttnArgs ta = a;
+    static const int exp_mode = getenv("ALORA_ATTN_EXP") ? atoi(getenv("ALORA_ATTN_EXP")) : 0;
+    ta.exp = exp_mode;
     if (tracing) {
       if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 6 * 65536);
       cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 6 * n_ctas, st);
