@@ -57,6 +57,9 @@ def parse():
     ap.add_argument("--lora-steps", type=int, default=2, help="timed LoRA-recompute eval turns")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write per-kernel profile here")
+    ap.add_argument("--sweep", choices=["c4"], default=None,
+                    help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k)")
+    ap.add_argument("--contexts", default="4096,8192,16384,32768")
     return ap.parse_args()
 
 
@@ -165,11 +168,76 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ C4 sweep ---
+C4 = dict(arch="llama", n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, ffn_dim=14336,
+          vocab_size=128256, seed=0)
+
+
+def run_sweep_c4(args):
+    """BASELINE.json configs[3]: Llama-3-8B, one base->adapter pipeline per context length; the eval turn's TTFT
+    with base-aligned reuse (aLoRA) vs standard-LoRA full recompute (budget 8192, chunked like vLLM)."""
+    import torch
+    import paper_2512_17910_b200 as P
+
+    torch.cuda.set_device(0)
+    rows = []
+    for ctx in [int(c) for c in args.contexts.split(",")]:
+        y = 256
+        x = ctx - y - 4
+        mcfg = P.ModelConfig(**C4, max_seq_len=ctx + 64, dtype="bf16")
+        model = P.Model(mcfg, init="device", max_tokens=8192, max_seqs=16)
+        res = {"context": ctx}
+        for mode in ("alora", "lora"):
+            spec = P.PipelineSpec(pipeline="base_adapter", mode=mode, prompt_len=x, gen_len=y, adapter_gen_len=16,
+                                  n_adapters=1, batch=1)
+            cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=8192, max_batch_requests=8),
+                                 pool_blocks=2 * (-(-(ctx + 64) // 16)) * 3 + 64, block_size=16,
+                                 adapters=(P.AdapterSpec(adapter_id="adapter0", rank=32, seed=0,
+                                                         invocation_tokens=P.invocation_for(mcfg.vocab_size, 0)),),
+                                 comparison_mode=mode)
+            eng = P.Engine(cfg, clock=P.WallClock(), model=model)
+            ttft, e2e, comp, base_tps = [], [], [], []
+            for i in range(1 + max(1, args.lora_steps)):  # first pipeline is warm-up
+                sp = P.PipelineSpec(**{**spec.__dict__, "seed": i})
+                ph = P.pipeline.pipeline_phases(sp, eng, rid_prefix=f"{mode}{i}-")
+                _, sub = next(ph)
+                n0 = len(eng.metrics)
+                P.pipeline.run_phase(eng, sub)
+                b = eng.metrics[n0]
+                _, sub = next(ph)
+                torch.cuda.synchronize()
+                n0 = len(eng.metrics)
+                P.pipeline.run_phase(eng, sub)
+                r = eng.metrics[n0]
+                if i > 0:
+                    ttft.append(r.ttft_s)
+                    e2e.append(r.e2e_s)
+                    comp.append(r.computed_tokens)
+                    base_tps.append(b.prompt_len / b.prefill_s)
+            res[mode] = {"ttft_ms": 1e3 * statistics.mean(ttft), "e2e_ms": 1e3 * statistics.mean(e2e),
+                         "computed_tokens": int(statistics.mean(comp)),
+                         "base_prefill_tok_s": statistics.mean(base_tps)}
+            del eng
+            torch.cuda.empty_cache()
+        res["ttft_speedup"] = res["lora"]["ttft_ms"] / res["alora"]["ttft_ms"]
+        res["e2e_speedup"] = res["lora"]["e2e_ms"] / res["alora"]["e2e_ms"]
+        rows.append(res)
+        print(json.dumps(res), flush=True)
+        del model
+        torch.cuda.empty_cache()
+    print(json.dumps({"metric": "C4 eval-turn TTFT aLoRA vs LoRA recompute (Llama-3-8B geometry, bf16, 1 B200)",
+                      "config": {"workload": "base_adapter pipeline, y=256, eval gen 16, B=16, budget 8192",
+                                 **{k: v for k, v in C4.items() if k != "seed"}},
+                      "data": "synthetic (random-init weights in HBM)", "sweep": rows}), flush=True)
+
+
 # --------------------------------------------------------------------- ours ---
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.sweep == "c4":
+        return run_sweep_c4(args)
     import torch
     import torch.distributed as dist
 
