@@ -216,7 +216,7 @@ int sum_partials_f32(const float* partials, int nparts, int64_t n, float* out, c
 // Deferred epilogue of a split-K QKV projection: per row, sum the splits (in order), rotate-half RoPE in
 // fp32 on the q and k heads (the kEpiRope math of the GEMM epilogue, one rounding), store q|k|v bf16 and
 // scatter the k and v rows into the paged pool (model.py:217-222) -- the step's kv_write, fused.
-__global__ void __launch_bounds__(256) qkv_finalize_kernel(const float* __restrict__ part, int nparts, int64_t pstride,
+__global__ void __launch_bounds__(512) qkv_finalize_kernel(const float* __restrict__ part, int nparts, int64_t pstride,
                                                            int Nq, int Nkv, int D,
                                                            const int32_t* __restrict__ positions,
                                                            const float* __restrict__ cos_t,
@@ -282,7 +282,7 @@ int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv,
   if (nparts < 1 || nparts > 8 || !partials || !positions || !cos_t || !sin_t || D % 8 || Nq % D || Nkv % D || ldq % 4)
     return ALORA_EINVAL;
   const int64_t ps = (int64_t)M * (Nq + 2 * Nkv);
-  ALORA_CUDA_CHECK(launch_pdl(qkv_finalize_kernel, dim3(M), dim3(256), 0, st, nullptr, 0, partials, nparts, ps, Nq, Nkv,
+  ALORA_CUDA_CHECK(launch_pdl(qkv_finalize_kernel, dim3(M), dim3(512), 0, st, nullptr, 0, partials, nparts, ps, Nq, Nkv,
                               D, positions, cos_t, sin_t, qkv, ldq, slot_mapping, kv_pool, n_layers, layer, B));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;

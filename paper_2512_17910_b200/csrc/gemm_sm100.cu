@@ -102,7 +102,8 @@ __device__ __forceinline__ bool lora_block_present(int j, int rank, uint32_t mas
   return false;
 }
 
-__device__ __forceinline__ float silu(float g) { return g / (1.0f + __expf(-g)); }
+// fast SiLU: __fdividef (MUFU.RCP + FMUL, no IEEE-division slow path / divergence); -> 0 for very negative g
+__device__ __forceinline__ float silu(float g) { return __fdividef(g, 1.0f + __expf(-g)); }
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* dst, const float (&v)[32], bool relu) {
 #pragma unroll
