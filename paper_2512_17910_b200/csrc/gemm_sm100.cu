@@ -755,6 +755,235 @@ int launch_ws(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, 
 }
 
 
+// ============================================================================================================
+// Decode GEMM (M <= 32 token rows): swap-AB weight streaming. The MMA's 128-row A operand is a tile of 128
+// WEIGHT rows and the B operand the (zero-padded) token rows, N = MN in {16, 32}, so a stage is 16 KB of
+// weights + MN*128 B of activations: ~11 stages (~176 KB of weights in flight per SM) instead of the
+// half-empty 128-row token tiles of gemm_ws_kernel. TMEM lane = output column, TMEM column = token.
+//   warp 0 TMA producer (weights of the first stages before griddepcontrol.wait), warp 1 MMA issuer,
+//   warps 2..5 epilogue. Epilogues: fp32 split-K partials [split][M][N] (consumed by residual RMSNorm /
+//   QKV finalize / LoRA select), C(fp32) += acc, fp32 store (+ fused greedy argmax), SwiGLU.
+// ============================================================================================================
+enum DecEpi : int { kDecPartial = 0, kDecAdd = 1, kDecStoreF32 = 2, kDecSwiglu = 3 };
+
+template <int MN>
+struct DecCfg {
+  static constexpr int kWBytes = kBM * kBK * 2;   // 128 weight rows x 64 K
+  static constexpr int kXBytes = MN * kBK * 2;    // MN token rows x 64 K
+  static constexpr int kStage = kWBytes + kXBytes;
+  static constexpr int kStages = (kSmemBudget / kStage) > 12 ? 12 : (kSmemBudget / kStage);
+  static constexpr int kSmem = 1024 + kStages * kStage + 256 + 128 * 33 * 4;  // + SwiGLU exchange tile
+};
+
+struct DecArgs {
+  int M, N, K, splits, mode;
+  float* out;          // partial base / C (fp32) / logits
+  int ldc;
+  __nv_bfloat16* out_bf16;  // SwiGLU output [M, N/2]
+  int ld_bf16;
+  unsigned long long* argmax;
+  int ks, rank, n_q, n_kv;  // LoRA expand as extra K (last split)
+  const uint32_t* tile_slot_mask;
+};
+
+template <int MN>
+__global__ void __launch_bounds__(192, 1)
+    gemm_dec_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
+                    const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_s,
+                    const DecArgs args) {
+  using C = DecCfg<MN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  float* xch = reinterpret_cast<float*>(smem + C::kStages * C::kStage + 256);  // [128][33]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * kBM;
+  const int S = args.splits, split = blockIdx.z;
+  const int nkb_all = (args.K + kBK - 1) / kBK;
+  const int per = (nkb_all + S - 1) / S;
+  const int kb0 = min(nkb_all, split * per), kb1 = min(nkb_all, kb0 + per);
+  const int n_base = kb1 - kb0;
+  const bool lora_here = args.ks > 0 && split == S - 1;
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tm_w);
+    sm100::prefetch_tmap(&tm_x);
+    for (int i = 0; i < C::kStages; ++i) {
+      sm100::mbar_init(&full[i], 1);
+      sm100::mbar_init(&empty[i], 1);
+    }
+    sm100::mbar_init(tmem_full, 1);
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<32>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    const uint64_t pol_act = sm100::policy_evict_last();
+    const uint64_t pol_w = sm100::policy_evict_first();
+    const int n_pre = min(C::kStages, n_base);
+    for (int i = 0; i < n_pre; ++i) {  // weights first: they do not depend on the previous kernel
+      if (sm100::elect_one()) {
+        sm100::mbar_arrive_expect_tx(&full[i], C::kStage);
+        sm100::tma_load_2d(smem + i * C::kStage, &tm_w, &full[i], (kb0 + i) * kBK, n0, pol_w);
+      }
+      __syncwarp();
+    }
+    pdl_wait();
+    pdl_trigger();
+    int target = 0, nkl = 0;
+    uint32_t mask = 0;
+    if (lora_here) {
+      target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+      nkl = (args.ks + kBK - 1) / kBK;
+      mask = args.tile_slot_mask[0];
+    }
+    for (int i = 0; i < n_pre; ++i) {
+      if (sm100::elect_one())
+        sm100::tma_load_2d(smem + i * C::kStage + C::kWBytes, &tm_x, &full[i], (kb0 + i) * kBK, 0, pol_act);
+      __syncwarp();
+    }
+    int st = n_pre % C::kStages;
+    uint32_t phase = n_pre == C::kStages ? 1u : 0u;
+    auto next = [&] { if (++st == C::kStages) { st = 0; phase ^= 1; } };
+    for (int kb = kb0 + n_pre; kb < kb1; ++kb) {
+      sm100::mbar_wait(&empty[st], phase ^ 1);
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + st * C::kStage;
+        sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
+        sm100::tma_load_2d(sa, &tm_w, &full[st], kb * kBK, n0, pol_w);
+        sm100::tma_load_2d(sa + C::kWBytes, &tm_x, &full[st], kb * kBK, 0, pol_act);
+      }
+      __syncwarp();
+      next();
+    }
+    for (int j = 0; j < nkl; ++j) {
+      if (!lora_block_present(j, args.rank, mask)) continue;
+      sm100::mbar_wait(&empty[st], phase ^ 1);
+      if (sm100::elect_one()) {
+        uint8_t* sa = smem + st * C::kStage;
+        sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
+        sm100::tma_load_2d(sa, &tm_u, &full[st], j * kBK, n0, pol_w);
+        sm100::tma_load_3d(sa + C::kWBytes, &tm_s, &full[st], j * kBK, 0, target, pol_act);
+      }
+      __syncwarp();
+      next();
+    }
+  } else if (warp == 1) {
+    pdl_wait();
+    int n_iters = n_base;
+    if (lora_here) {
+      const uint32_t mask = args.tile_slot_mask[0];
+      const int nkl = (args.ks + kBK - 1) / kBK;
+      for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+    }
+    constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, MN);
+    int st = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < n_iters; ++it) {
+      sm100::mbar_wait(&full[st], phase);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint8_t* sa = smem + st * C::kStage;
+        const uint64_t da = sm100::umma_desc_sw128(sa);
+        const uint64_t db = sm100::umma_desc_sw128(sa + C::kWBytes);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+          sm100::mma_bf16_ss(tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (it > 0 || k > 0) ? 1u : 0u);
+        sm100::mma_commit(&empty[st]);
+      }
+      __syncwarp();
+      if (++st == C::kStages) { st = 0; phase ^= 1; }
+    }
+    if (sm100::elect_one()) sm100::mma_commit(tmem_full);
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int quarter = warp & 3;
+    const int ncol = n0 + quarter * 32 + lane;  // this thread's output column (TMEM lane)
+    const bool has_acc = n_base > 0 || lora_here;
+    sm100::mbar_wait(tmem_full, 0);
+    sm100::tc_fence_after();
+    uint32_t r[32];
+    sm100::tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16), r);
+    sm100::tmem_ld_wait();
+    float v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = has_acc ? __uint_as_float(r[j]) : 0.f;
+    const int M = args.M;
+    if (args.mode == kDecPartial) {
+      float* dst = args.out + (int64_t)split * M * args.N + ncol;
+#pragma unroll
+      for (int m = 0; m < MN; ++m)
+        if (m < M) dst[(int64_t)m * args.N] = v[m];
+    } else if (args.mode == kDecAdd) {
+#pragma unroll
+      for (int m = 0; m < MN; ++m)
+        if (m < M) args.out[(int64_t)m * args.ldc + ncol] += v[m];
+    } else if (args.mode == kDecStoreF32) {
+#pragma unroll
+      for (int m = 0; m < MN; ++m)
+        if (m < M) args.out[(int64_t)m * args.ldc + ncol] = v[m];
+      if (args.argmax) {
+#pragma unroll
+        for (int m = 0; m < MN; ++m) {
+          if (m >= M) break;
+          uint32_t u32 = __float_as_uint(v[m]);
+          u32 = (u32 & 0x80000000u) ? ~u32 : (u32 | 0x80000000u);
+          unsigned long long key = ((unsigned long long)u32 << 32) | (0xFFFFFFFFu - (uint32_t)ncol);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+            key = other > key ? other : key;
+          }
+          if (lane == 0) atomicMax(args.argmax + m, key);
+        }
+      }
+    } else {  // kDecSwiglu: lanes 0-63 of the 128-row tile are gate rows, 64-127 the matching up rows
+      const int row = quarter * 32 + lane;
+#pragma unroll
+      for (int m = 0; m < MN; ++m) xch[row * 33 + m] = v[m];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      if (quarter < 2) {
+        const int j = row;  // output column n0/2 + j
+#pragma unroll
+        for (int m = 0; m < MN; ++m)
+          if (m < M)
+            args.out_bf16[(int64_t)m * args.ld_bf16 + n0 / 2 + j] =
+                __float2bfloat16_rn(silu(xch[j * 33 + m]) * xch[(j + 64) * 33 + m]);
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) sm100::tmem_dealloc<32>(tmem);
+}
+
+template <int MN>
+int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& u, const CUtensorMap& sm,
+               const DecArgs& args, cudaStream_t st) {
+  using C = DecCfg<MN>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(gemm_dec_kernel<MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  const dim3 grid(args.N / kBM, 1, args.splits);
+  if (launch_pdl(gemm_dec_kernel<MN>, grid, dim3(192), C::kSmem, st, nullptr, 0, w, x, u, sm, args) != cudaSuccess)
+    return ALORA_ECUDA;
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
 struct WsChoice {
   int bn = 0, splits = 1;
   double cost = 1e30;
@@ -821,12 +1050,17 @@ void configure_gemm() {
   prefer_max_smem(gemm_ws_kernel<64, 2>);
   prefer_max_smem(gemm_ws_kernel<128, 2>);
   prefer_max_smem(gemm_ws_kernel<256, 2>);
+  prefer_max_smem(gemm_dec_kernel<16>);
+  prefer_max_smem(gemm_dec_kernel<32>);
 }
 
 int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt, int ldb, void* Cout, int ldc, int M,
               int N, int K, const GemmLora* lora, cudaStream_t st, const GemmWs* ws, int max_splits,
               GemmDefer* defer) {
-  if (defer) defer->splits_out = 1;
+  if (defer) {
+    defer->splits_out = 1;
+    defer->deferred = false;
+  }
   if (M == 0 || N == 0) return ALORA_OK;
   if (M < 0 || N < 0 || K < 1 || lda % 8 || ldb % 8 || ldc % 8) return ALORA_EINVAL;
   const int base_epi = epi & 15;
@@ -899,6 +1133,54 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.n_kv = lora->n_kv;
     args.tile_slot_mask = lora->tile_slot_mask;
   }
+  static const bool no_dec = getenv("ALORA_GEMM_NO_DEC") != nullptr;  // A/B switch off the swap-AB decode GEMM
+  if (M <= 32 && !no_dec && N % kBM == 0 && K % kBK == 0) {
+    const bool defer_ok = defer != nullptr && defer->partial != nullptr;
+    int mode = -1;
+    if (base_epi == kEpiAdd && !(epi & 16)) mode = defer_ok ? kDecPartial : kDecAdd;
+    else if ((base_epi == kEpiRope || base_epi == kEpiLoraSelect) && defer_ok) mode = kDecPartial;
+    else if (epi == (kEpiStore | 16)) mode = kDecStoreF32;
+    else if (base_epi == kEpiSwiglu) mode = kDecSwiglu;
+    if (mode >= 0) {
+      DecArgs da{};
+      da.M = M; da.N = N; da.K = K; da.mode = mode; da.splits = 1;
+      const int tiles = N / kBM, nkb = K / kBK;
+      if (mode == kDecPartial) {
+        int sp = std::max(1, std::min({8, (2 * kNumSMs + tiles - 1) / tiles / 2 > 0 ? kNumSMs / tiles : 1, nkb / 4}));
+        while (sp > 1 && (int64_t)sp * M * N * 4 > defer->capacity) --sp;
+        const int per = (nkb + sp - 1) / sp;
+        sp = (nkb + per - 1) / per;  // no empty trailing splits
+        da.splits = sp;
+        da.out = defer->partial;
+        defer->splits_out = sp;
+        defer->deferred = true;
+      } else if (mode == kDecSwiglu) {
+        da.out_bf16 = static_cast<__nv_bfloat16*>(Cout);
+        da.ld_bf16 = ldc;
+      } else {
+        da.out = static_cast<float*>(Cout);
+        da.ldc = ldc;
+        da.argmax = lora ? lora->argmax : nullptr;
+      }
+      const int MN = M <= 16 ? 16 : 32;
+      CUtensorMap tw, tx, tu, tsm;
+      if (!make_tmap_2d(&tw, Bt, N, K, ldb, kBM, kBK)) return ALORA_ECUDA;
+      if (!make_tmap_2d(&tx, A, M, K, lda, MN, kBK)) return ALORA_ECUDA;
+      tu = tw;
+      tsm = tx;
+      if (lora != nullptr && lora->s != nullptr && lora->ks > 0) {
+        if (lora->ks % 8 || (lora->n_q % kBM) || (lora->n_kv % kBM) || lora->rank < 1) return ALORA_EINVAL;
+        if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks, lora->ks, kBM, kBK)) return ALORA_ECUDA;
+        if (!make_tmap_3d(&tsm, lora->s, 3, M, lora->ks, MN, kBK)) return ALORA_ECUDA;
+        da.ks = lora->ks;
+        da.rank = lora->rank;
+        da.n_q = lora->n_q;
+        da.n_kv = lora->n_kv;
+        da.tile_slot_mask = lora->tile_slot_mask;
+      }
+      return MN == 16 ? launch_dec<16>(tw, tx, tu, tsm, da, st) : launch_dec<32>(tw, tx, tu, tsm, da, st);
+    }
+  }
   static const bool no_ws = getenv("ALORA_GEMM_NO_WS") != nullptr;  // A/B switch to the per-tile kernel
   if (M <= 2 * kBM && !no_ws) {
     // weight streaming: one CTA per (N tile, K split) covering every token row
@@ -941,6 +1223,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
         if (!can_defer) return ALORA_EINVAL;
         args.partial = defer->partial;
         defer->splits_out = best.splits;
+        defer->deferred = true;
       }
       return mt == 1 ? dispatch_ws<1>(ta, tb2, ts, tu2, args, best.bn, st)
                      : dispatch_ws<2>(ta, tb2, ts, tu2, args, best.bn, st);

@@ -110,6 +110,7 @@ struct GemmDefer {
   float* partial = nullptr;
   int64_t capacity = 0;
   int splits_out = 1;
+  bool deferred = false;  // partials [splits_out][M][N] were written and the epilogue is the consumer's job
 };
 // ws enables split-K of the per-tile kernel (M > 256; max_splits caps it) when the output tiles cannot fill
 // the 148 SMs.

@@ -161,7 +161,7 @@ int shrink(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const 
   df.partial = part;
   df.capacity = part_bytes;
   const int rc = gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, 3 * SR, K, &g, st, gw, 8, part ? &df : nullptr);
-  if (rc != ALORA_OK || df.splits_out <= 1) return rc;
+  if (rc != ALORA_OK || !df.deferred) return rc;
   if (extra_launches) ++*extra_launches;
   return lora_select_finalize_bf16(part, df.splits_out, M, SR, R, row_slot, row_apply, targets, s, st);
 }
@@ -263,7 +263,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     if (!tp) {
       const int rc = gemm_bf16(kEpiAdd, A, K, static_cast<const __nv_bfloat16*>(W), ldw, x, dm, M, dm, K, nullptr,
                                st, gw, 8, &df);
-      pend = df.splits_out > 1 ? df.splits_out : 0;
+      pend = df.deferred ? df.splits_out : 0;
       pend_buf = part;
       return rc;
     }
@@ -317,7 +317,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     RUN("gemm_qkv", gemm_bytes(m_, Nqkv_, dm_, 2, false) + (lora ? 2.0 * Nqkv_ * ks_ : 0.0), 2.0 * m_ * Nqkv_ * dm_,
         gemm_bf16(llama ? kEpiRope : kEpiStore, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_qkv_t[l]), dm, qkv,
                   Nqkv, M, Nqkv, dm, (lora || llama) ? &gl : nullptr, st, gw, 8, llama ? &dq : nullptr));
-    if (dq.splits_out > 1) {  // split-K QKV: RoPE + bf16 + the paged KV scatter run in the finalize kernel
+    if (dq.deferred) {  // split-K / decode QKV: RoPE + bf16 + the paged KV scatter run in the finalize kernel
       RUN("qkv_finalize", m_ * Nqkv_ * 4.0 * dq.splits_out + 2.0 * m_ * Nqkv_ + 2.0 * 2 * m_ * Nkv * 2, 0,
           qkv_finalize_bf16(part, dq.splits_out, M, Nq, Nkv, D, s.positions, d.rope_cos, d.rope_sin, qkv, Nqkv,
                             s.slot_mapping, static_cast<__nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, st));
