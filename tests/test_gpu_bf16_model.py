@@ -146,6 +146,28 @@ def test_forward_bf16_vs_oracle_with_adapters(dims):
             margin = np.sort(want[k])[-1] - np.sort(want[k])[-2]
             if margin > 2 * LOGIT_TOL:
                 assert int(np.argmax(got[k])) == int(np.argmax(want[k])), k
+    # two decode steps (M = 3 rows: the swap-AB decode GEMM path, LoRA expand as extra K, deferred RoPE /
+    # LoRA select / residual consumers); every request feeds the oracle's greedy token of the previous step
+    nxt = {k: int(np.argmax(want[k])) for k in want}
+    lens = [len(t) for t in toks]
+    for step in range(2):
+        oseqs, pseqs = [], []
+        for r in range(3):
+            tk, pos = np.array([nxt[f"r{r}"]]), lens[r] + step
+            if r == 1:
+                oseqs.append(O.OracleSpan(f"r{r}", tk, pos, tables[r], oa, np.array([False])))
+                pseqs.append(P.SeqInput(f"r{r}", tk, pos, tables[r], pa, np.array([False])))
+            elif r == 2:
+                oseqs.append(O.OracleSpan(f"r{r}", tk, pos, tables[r], oa_std, None))
+                pseqs.append(P.SeqInput(f"r{r}", tk, pos, tables[r], pa_std, None))
+            else:
+                oseqs.append(O.OracleSpan(f"r{r}", tk, pos, tables[r]))
+                pseqs.append(P.SeqInput(f"r{r}", tk, pos, tables[r]))
+        want = om.forward_step(oseqs, okv)
+        got = pm.forward_step(pseqs, pool.kv)
+        for k in want:
+            worst = max(worst, float(np.max(np.abs(got[k] - want[k]))))
+            nxt[k] = int(np.argmax(want[k]))
     kv = pool.kv.float().cpu().numpy()
     rel = float(np.linalg.norm(kv - okv) / np.linalg.norm(okv))
     print(f"[parity] bf16 forward {dims.get('arch', 'ref')}: max |dlogit| {worst:.3g}, KV rel-L2 {rel:.3g}, "
