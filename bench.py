@@ -57,8 +57,9 @@ def parse():
     ap.add_argument("--lora-steps", type=int, default=2, help="timed LoRA-recompute eval turns")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-json", default=None, help="write per-kernel profile here")
-    ap.add_argument("--sweep", choices=["c4"], default=None,
-                    help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k)")
+    ap.add_argument("--sweep", choices=["c3", "c4"], default=None,
+                    help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k); "
+                         "c3: Llama-3-8B + 8 aLoRA adapters, 64 eval requests over 8k contexts (one replica)")
     ap.add_argument("--contexts", default="4096,8192,16384,32768")
     return ap.parse_args()
 
@@ -231,6 +232,57 @@ def run_sweep_c4(args):
                       "data": "synthetic (random-init weights in HBM)", "sweep": rows}), flush=True)
 
 
+def run_c3(args):
+    """BASELINE.json configs[2] on one replica: Llama-3-8B bf16 + 8 activated adapters (r=32), a multi_adapter
+    pipeline over 8 conversations of 8k tokens -> 64 concurrent eval requests (8 adapters x 8 instances),
+    aLoRA (base-aligned reuse) vs LoRA recompute (budget 8192). Replicas scale it weakly (replicas.py)."""
+    import torch
+    import paper_2512_17910_b200 as P
+
+    torch.cuda.set_device(0)
+    ctx, y, n_ad, batch = 8192, 256, 8, 8
+    x = ctx - y - 4
+    mcfg = P.ModelConfig(**C4, max_seq_len=ctx + 64, dtype="bf16")
+    model = P.Model(mcfg, init="device", max_tokens=8192, max_seqs=96)
+    out = {}
+    for mode in ("alora", "lora"):
+        spec = P.PipelineSpec(pipeline="multi_adapter", mode=mode, prompt_len=x, gen_len=y, adapter_gen_len=16,
+                              n_adapters=n_ad, batch=batch)
+        blocks = -(-(ctx + 64) // 16)
+        cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=8192, max_batch_requests=96),
+                             pool_blocks=(batch * (n_ad + 1) + 8) * blocks, block_size=16,
+                             adapters=tuple(P.AdapterSpec(adapter_id=f"adapter{k}", rank=32, seed=k,
+                                                          invocation_tokens=P.invocation_for(mcfg.vocab_size, k))
+                                            for k in range(n_ad)),
+                             comparison_mode=mode)
+        eng = P.Engine(cfg, clock=P.WallClock(), model=model)
+        ph = P.pipeline.pipeline_phases(spec, eng, rid_prefix=f"{mode}-")
+        _, sub = next(ph)
+        P.pipeline.run_phase(eng, sub)
+        _, sub = next(ph)
+        torch.cuda.synchronize()
+        n0 = len(eng.metrics)
+        t0 = time.perf_counter()
+        P.pipeline.run_phase(eng, sub)
+        wall = time.perf_counter() - t0
+        rows = eng.metrics[n0:]
+        out[mode] = {"requests": len(rows), "ttft_ms_mean": 1e3 * statistics.mean(r.ttft_s for r in rows),
+                     "turn_ttft_ms": 1e3 * max(r.ttft_s for r in rows),
+                     "e2e_ms_mean": 1e3 * statistics.mean(r.e2e_s for r in rows), "turn_wall_ms": 1e3 * wall,
+                     "hit_tokens_per_request": statistics.mean(r.hit_tokens for r in rows),
+                     "computed_tokens": int(sum(r.computed_tokens for r in rows)),
+                     "eval_prompt_tok_s": sum(r.prompt_len for r in rows) / max(r.ttft_s for r in rows)}
+        del eng
+        torch.cuda.empty_cache()
+    out["turn_ttft_speedup"] = out["lora"]["turn_ttft_ms"] / out["alora"]["turn_ttft_ms"]
+    out["e2e_speedup"] = out["lora"]["e2e_ms_mean"] / out["alora"]["e2e_ms_mean"]
+    print(json.dumps({"metric": "C3 eval turn, 64 requests: TTFT/E2E aLoRA vs LoRA recompute (1 replica, 1 B200)",
+                      "config": {"workload": "multi_adapter, 8 conversations x 8 adapters, 8k context, y=256, "
+                                             "eval gen 16, B=16, budget 8192",
+                                 **{k: v for k, v in C4.items() if k != "seed"}},
+                      "data": "synthetic (random-init weights in HBM)", **out}), flush=True)
+
+
 # --------------------------------------------------------------------- ours ---
 def main():
     args = parse()
@@ -238,6 +290,8 @@ def main():
         return run_reference(args)
     if args.sweep == "c4":
         return run_sweep_c4(args)
+    if args.sweep == "c3":
+        return run_c3(args)
     import torch
     import torch.distributed as dist
 
