@@ -106,6 +106,24 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+def eval_split(args, B=16):
+    """(cached, computed) prompt tokens of an aLoRA eval request: hits ((x+y-1)//B)*B, SURVEY.md Appendix B."""
+    total = args.prompt_len + args.gen_len + 4  # conversation + base output + EOT + 3-token invocation
+    cached = ((args.prompt_len + args.gen_len - 1) // B) * B
+    return cached, total - cached
+
+
+def c2_config(args, world):
+    """The workload both arms report (BASELINE.json configs[1])."""
+    return {"workload": "C2: Llama-3.2-1B geometry + 3 aLoRA adapters r=32, multi_adapter pipeline "
+                        f"(x={args.prompt_len}, y={args.gen_len}, eval gen {args.adapter_gen}), "
+                        f"{args.batch} instances x 3 adapters per eval turn, B=16, budget 8192; metric = eval "
+                        "prompt tokens (cached + computed) per second of the TTFT-defining forward",
+            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+            "l2": "working set (2.5 GB weights + KV) exceeds the 126 MB L2; no flush needed",
+            **{k: v for k, v in C2.items() if k != "seed"}}
+
+
 # --------------------------------------------------------------- reference ---
 def oracle_c2(n_layers=None):
     """C2 geometry in the numpy oracle; random fp32 weights (values do not change CPU time)."""
@@ -137,7 +155,7 @@ def cpu_sample(O, cfg, model, ad, prefix, suffix, B=16):
     n_blocks = -(-(prefix + suffix) // B)
     kv = np.random.default_rng(1).standard_normal((n_blocks, cfg.n_layers, 2, B, cfg.kv_width)).astype(np.float32)
     toks = np.random.default_rng(2).integers(0, cfg.vocab_size - 32, suffix)
-    mask = np.arange(prefix, prefix + suffix) < prefix + 1  # EOT before the invocation, adapted after
+    mask = np.arange(prefix, prefix + suffix) < prefix + suffix - 3  # the base path up to the invocation
     span = O.OracleSpan("r", toks, prefix, list(range(n_blocks)), ad, mask)
     t0 = time.perf_counter()
     model.forward_step([span], kv)
@@ -148,8 +166,7 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    prefix = args.prompt_len + args.gen_len  # cached conversation (x + y), suffix = EOT + invocation
-    suffix = 4
+    prefix, suffix = eval_split(args)
     O, cfg, model, ad = oracle_c2()
     for _ in range(args.warmup):
         cpu_sample(O, cfg, model, ad, prefix, suffix)
@@ -160,11 +177,12 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": {"workload": "C2 aLoRA eval request: 4-token suffix over a 2048-token cached prefix",
-                       **{k: v for k, v in C2.items() if k != "seed"}},
+            "config": c2_config(args, int(os.environ.get("WORLD_SIZE", "1"))),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"1 eval request per step ({suffix}-token suffix over {prefix} cached tokens), "
-                                       "oracle/model_oracle.py fp64 numpy (OpenBLAS threads = cores)"},
+                             "sample": f"1 of the turn's eval requests per step ({suffix}-token suffix over {prefix} "
+                                       "cached tokens; the reference forward loops over spans, model.py:243, so "
+                                       "tok/s per request is the turn's), oracle/model_oracle.py fp64 numpy "
+                                       "(OpenBLAS threads = cores)"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -490,7 +508,7 @@ def main():
     if world == 1 and not args.no_cpu_baseline:
         try:
             O, ocfg, om, oad = oracle_c2()
-            prefix, suffix = args.prompt_len + args.gen_len, 4
+            prefix, suffix = eval_split(args)
             cpu_sample(O, ocfg, om, oad, prefix, suffix)
             t = min(cpu_sample(O, ocfg, om, oad, prefix, suffix) for _ in range(2))
             cpu = {"value": (prefix + suffix) / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
@@ -504,12 +522,7 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": fwd_max * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights in HBM, random conversations)",
-        "config": {"workload": "C2: Llama-3.2-1B geometry bf16 + 3 aLoRA adapters r=32, multi_adapter pipeline "
-                               f"(x={args.prompt_len}, y={args.gen_len}, eval gen {args.adapter_gen}), "
-                               f"{args.batch} instances x 3 adapters per eval turn, B=16, budget {budget}",
-                   "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                   "l2": "working set (2.5 GB weights + KV) exceeds the 126 MB L2; no flush needed",
-                   "eval_requests_per_step": int(tokens / (args.prompt_len + args.gen_len + 4)),
+        "config": {**c2_config(args, world), "eval_requests_per_step": int(tokens / (args.prompt_len + args.gen_len + 4)),
                    "forward_rows": ra["fwd_rows"]},
         "e2e": {"value": tokens_all / ttft_max, "unit": UNIT, "h2d_bytes_per_step": ra["h2d"],
                 "d2h_bytes_per_step": ra["d2h"],
