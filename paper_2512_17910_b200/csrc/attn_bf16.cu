@@ -338,22 +338,78 @@ __device__ void merge_partials(const AttnArgs& a, int s, int kvh, int qt, int ro
   __syncthreads();
   if (!*s_last) return;
   constexpr int G8 = D / 8;
-  for (int i = tid; i < rows_here * G8; i += nthr) {
+  const int n_items = rows_here * G8;
+  if (parts_here <= 4) {
+  // two work items per thread per round: all partial loads of both are in flight before any is consumed
+  // (the merge is a chain of L2 round trips on the kernel's tail)
+  for (int i0 = tid; i0 < n_items; i0 += 2 * nthr) {
+    float2 ml[2][4];
+    float4 x0[2][4], x1[2][4];
+    int64_t grow2[2];
+    int head2[2], c82[2], np2[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int i = i0 + u * nthr;
+      np2[u] = 0;
+      if (i >= n_items) continue;
+      const int r = i / G8, c8 = (i % G8) * 8;
+      const int pr = qt * kQT + r;
+      const int tok = pr / G, head = kvh * G + pr % G;
+      const int64_t grow = row0 + tok;
+      const int np_row = min(parts_here, (start + tok) / a.part_size + 1);
+      grow2[u] = grow;
+      head2[u] = head;
+      c82[u] = c8;
+      np2[u] = np_row;
+      const int64_t slot0 = (int64_t)grow * a.H + head, pstride = (int64_t)a.M * a.H;
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {
+        if (p < np_row) {
+          ml[u][p] = __ldcg(reinterpret_cast<const float2*>(a.ws_ml + (slot0 + p * pstride) * 2));
+          x0[u][p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8));
+          x1[u][p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8 + 4));
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int np_row = np2[u];
+      if (np_row == 0) continue;
+      float mx = -INFINITY;
+#pragma unroll
+      for (int p = 0; p < 4; ++p)
+        if (p < np_row) mx = fmaxf(mx, ml[u][p].x);
+      float l = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int p = 0; p < 4; ++p) {  // partition order: deterministic
+        if (p >= np_row) break;
+        const float w = fast_exp2(ml[u][p].x - mx);
+        l += w * ml[u][p].y;
+        acc[0] += w * x0[u][p].x; acc[1] += w * x0[u][p].y; acc[2] += w * x0[u][p].z; acc[3] += w * x0[u][p].w;
+        acc[4] += w * x1[u][p].x; acc[5] += w * x1[u][p].y; acc[6] += w * x1[u][p].z; acc[7] += w * x1[u][p].w;
+      }
+      const float inv = __fdividef(1.f, l);
+      __align__(16) __nv_bfloat162 ov[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) ov[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+      *reinterpret_cast<int4*>(a.out + grow2[u] * a.ld_out + head2[u] * D + c82[u]) = *reinterpret_cast<int4*>(ov);
+    }
+  }
+    return;
+  }
+  for (int i = tid; i < n_items; i += nthr) {
     const int r = i / G8, c8 = (i % G8) * 8;
     const int pr = qt * kQT + r;
     const int tok = pr / G, head = kvh * G + pr % G;
     const int64_t grow = row0 + tok;
     const int np_row = min(parts_here, (start + tok) / a.part_size + 1);
-    // all loads of a round are issued before any is consumed: two L2 round trips per item, not 2 * np
     const int64_t slot0 = (int64_t)grow * a.H + head, pstride = (int64_t)a.M * a.H;
     float2 ml[kMaxParts];
-#pragma unroll
-    for (int p = 0; p < kMaxParts; ++p)
-      ml[p] = p < np_row ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml + (slot0 + p * pstride) * 2))
-                         : make_float2(-INFINITY, 0.f);
     float4 x0[kMaxParts], x1[kMaxParts];
 #pragma unroll
     for (int p = 0; p < kMaxParts; ++p) {
+      ml[p] = p < np_row ? __ldcg(reinterpret_cast<const float2*>(a.ws_ml + (slot0 + p * pstride) * 2))
+                         : make_float2(-INFINITY, 0.f);
       if (p < np_row) {
         x0[p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8));
         x1[p] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8 + 4));
@@ -371,7 +427,7 @@ __device__ void merge_partials(const AttnArgs& a, int s, int kvh, int qt, int ro
       acc[0] += w * x0[p].x; acc[1] += w * x0[p].y; acc[2] += w * x0[p].z; acc[3] += w * x0[p].w;
       acc[4] += w * x1[p].x; acc[5] += w * x1[p].y; acc[6] += w * x1[p].z; acc[7] += w * x1[p].w;
     }
-    const float inv = 1.f / l;
+    const float inv = __fdividef(1.f, l);
     __align__(16) __nv_bfloat162 ov[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) ov[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
