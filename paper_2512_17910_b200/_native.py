@@ -10,7 +10,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libalora_sm100a.so")
+# ALORA_LIB (developer A/B switch) loads another in-tree build of the same library
+LIB_PATH = os.environ.get("ALORA_LIB") or os.path.join(_HERE, "libalora_sm100a.so")
 
 ALORA_OK = 0
 ALORA_EINVAL = -1
