@@ -199,6 +199,13 @@ int alora_model_destroy(void* handle);
 /* Run every layer for one packed step: embed -> L x [norm, masked QKV (+LoRA),
  * KV write, paged attention, O-proj, MLP] -> last-row logits -> argmax. */
 int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream);
+/* alora_model_forward captured as a CUDA graph (with its programmatic-launch edges) and replayed: the first
+ * call for a step shape (n_tokens, n_seqs, max_blocks, max_q, max_ctx) captures on `stream` (which must not
+ * be the legacy default stream), later calls with the same shape AND the same staged step buffers replay it.
+ * Kernels read every per-step length from the device arrays, so one capture serves all decode steps whose
+ * padded block-table width and context bound fall in the same bucket. Falls back to alora_model_forward
+ * while profiling. */
+int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream);
 /* Count of kernel launches issued by the last alora_model_forward. */
 int32_t alora_model_last_launches(void* handle);
 

@@ -104,6 +104,8 @@ EXPORTS = {
                                ctypes.POINTER(c_void_p)),
     "alora_model_destroy": _sig("alora_model_destroy", c_i32, c_void_p),
     "alora_model_forward": _sig("alora_model_forward", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc), c_void_p),
+    "alora_model_forward_graph": _sig("alora_model_forward_graph", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc),
+                                      c_void_p),
     "alora_model_last_launches": _sig("alora_model_last_launches", c_i32, c_void_p),
     "alora_model_set_profiling": _sig("alora_model_set_profiling", c_i32, c_void_p, c_i32),
     "alora_model_profile_read": _sig("alora_model_profile_read", c_i32, c_void_p, c_i32, c_void_p, c_void_p,

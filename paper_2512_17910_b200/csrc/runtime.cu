@@ -8,8 +8,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
+#include <tuple>
 #include <vector>
 
 #include "common.cuh"
@@ -57,12 +59,27 @@ struct Profiler {
   }
 };
 
+// A captured forward: valid for steps with the same shape and the same staged device buffers.
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  AloraStepDesc step{};
+  int32_t launches = 0;
+  uint64_t last_use = 0;
+};
+using GraphKey = std::tuple<int, int, int, int, int>;  // n_tokens, n_seqs, max_blocks, max_q, max_ctx
+
 struct Model {
   AloraModelDesc d;
   std::vector<const void*> w_qkv_t, w_o_t, w_in_t, w_out_t, lora_down, lora_up_t;
   std::vector<const float*> attn_norm, mlp_norm;
   int32_t last_launches = 0;
   Profiler prof;
+  std::map<GraphKey, GraphEntry> graphs;
+  uint64_t graph_clock = 0;
+  ~Model() {
+    for (auto& kv : graphs)
+      if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  }
 };
 
 // Runs one launcher; counts it and, when profiling, brackets it with events and tags its algorithmic cost.
@@ -535,6 +552,56 @@ int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream) {
     return ALORA_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   return m.d.dtype == ALORA_F32 ? forward_f32(m, *step, st) : forward_bf16(m, *step, st);
+}
+
+static bool same_step_buffers(const AloraStepDesc& a, const AloraStepDesc& b) {
+  return a.tokens == b.tokens && a.positions == b.positions && a.slot_mapping == b.slot_mapping &&
+         a.row_slot == b.row_slot && a.row_apply == b.row_apply && a.cu_q == b.cu_q && a.start_pos == b.start_pos &&
+         a.block_table == b.block_table && a.last_row == b.last_row && a.logits == b.logits && a.next_ids == b.next_ids;
+}
+
+int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream) {
+  if (!handle || !step) return ALORA_EINVAL;
+  Model& m = *static_cast<Model*>(handle);
+  if (m.d.dtype != ALORA_BF16 || m.prof.on) return alora_model_forward(handle, step, stream);
+  if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
+    return ALORA_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const GraphKey key{step->n_tokens, step->n_seqs, step->max_blocks, step->max_q, step->max_ctx};
+  auto it = m.graphs.find(key);
+  if (it != m.graphs.end() && !same_step_buffers(it->second.step, *step)) {
+    cudaGraphExecDestroy(it->second.exec);
+    m.graphs.erase(it);
+    it = m.graphs.end();
+  }
+  if (it == m.graphs.end()) {
+    if (m.graphs.size() >= 32) {  // evict the least recently used capture
+      auto lru = m.graphs.begin();
+      for (auto j = m.graphs.begin(); j != m.graphs.end(); ++j)
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      cudaGraphExecDestroy(lru->second.exec);
+      m.graphs.erase(lru);
+    }
+    cudaGraph_t g = nullptr;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return ALORA_ECUDA;
+    const int rc = forward_bf16(m, *step, st);
+    const cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (rc != ALORA_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess || g == nullptr) return ALORA_ECUDA;
+    GraphEntry e;
+    const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
+    cudaGraphDestroy(g);
+    if (ie != cudaSuccess) return ALORA_ECUDA;
+    e.step = *step;
+    e.launches = m.last_launches;
+    it = m.graphs.emplace(key, e).first;
+  }
+  it->second.last_use = ++m.graph_clock;
+  m.last_launches = it->second.launches;
+  return cudaGraphLaunch(it->second.exec, st) == cudaSuccess ? ALORA_OK : ALORA_ECUDA;
 }
 
 int32_t alora_model_last_launches(void* handle) {

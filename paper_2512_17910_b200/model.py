@@ -116,10 +116,16 @@ class _StepBuffers:
 class Model:
     """Weights on the device plus the native step executor."""
 
+    GRAPH_BLOCK_BUCKET = 32  # decode steps pad the block table to a multiple of this many blocks
+
     def __init__(self, config: ModelConfig | None = None, weights: BaseWeights | None = None, init: str = "philox",
-                 max_tokens: int = 2048, max_seqs: int = 256):
+                 max_tokens: int = 2048, max_seqs: int = 256, graphs: bool = True):
         torch = _native.require_cuda()
         self._torch = torch
+        # decode steps (one row per span, bf16) replay a captured CUDA graph of the whole forward
+        self._graphs = bool(graphs) and (config or ModelConfig()).dtype == "bf16"
+        self._graph_stream = torch.cuda.Stream() if self._graphs else None
+        self._staged_graphable = False
         self.config = cfg = config or ModelConfig()
         if init == "philox" or weights is not None:
             self.weights = weights if weights is not None else generate_weights(cfg)
@@ -387,6 +393,10 @@ class Model:
             tables.append(np.asarray(seq.block_ids[:need], dtype=np.int64))
         M = int(sum(lens))
         maxb = max(len(tb) for tb in tables)
+        graphable = self._graphs and max(lens) == 1  # a decode step: replay a captured graph
+        if graphable:  # bucket the table width (and the context bound below) so one capture serves many steps
+            bb = self.GRAPH_BLOCK_BUCKET
+            maxb = -(-maxb // bb) * bb
         cu = np.zeros(S + 1, dtype=np.int32)
         np.cumsum(lens, out=cu[1:])
         positions = np.concatenate([np.arange(s, s + n, dtype=np.int32) for s, n in zip(starts, lens)])
@@ -400,7 +410,8 @@ class Model:
             "attn_kv_tokens": float(sum(s + n for s, n in zip(starts, lens))),
             "attn_qk_pairs": float(sum(n * (s + (n + 1) / 2) for s, n in zip(starts, lens))),
             "M": M, "S": S, "maxb": maxb, "max_q": int(max(lens)),
-            "max_ctx": int(max(s + n for s, n in zip(starts, lens))),
+            "max_ctx": maxb * block_size if graphable else int(max(s + n for s, n in zip(starts, lens))),
+            "graphable": graphable,
             "tokens": np.concatenate(toks).astype(np.int32), "positions": positions, "slot_mapping": slot_map,
             "row_slot": np.concatenate(slots), "row_apply": np.concatenate(applies),
             "cu_q": cu, "start_pos": np.asarray(starts, dtype=np.int32), "last_row": (cu[1:] - 1).astype(np.int32),
@@ -422,10 +433,18 @@ class Model:
         return self._ids_host[:S].numpy().copy(), logits
 
     def launch(self, st) -> None:
-        """Enqueue one staged step (alora_model_forward) on the current stream; no host sync."""
-        stream = self._torch.cuda.current_stream().cuda_stream
-        _native.check(_native.lib.alora_model_forward(self._handle, ctypes.byref(st), ctypes.c_void_p(stream)),
-                      "alora_model_forward")
+        """Enqueue one staged step on the current stream (decode steps: a CUDA-graph replay); no host sync."""
+        cur = self._torch.cuda.current_stream()
+        if self._staged_graphable and not getattr(self, "_profiling", False):
+            gs = self._graph_stream  # capture/replay needs a non-legacy stream; ordered against the caller's
+            gs.wait_stream(cur)
+            _native.check(_native.lib.alora_model_forward_graph(self._handle, ctypes.byref(st),
+                                                                ctypes.c_void_p(gs.cuda_stream)),
+                          "alora_model_forward_graph")
+            cur.wait_stream(gs)
+        else:
+            _native.check(_native.lib.alora_model_forward(self._handle, ctypes.byref(st),
+                                                          ctypes.c_void_p(cur.cuda_stream)), "alora_model_forward")
         self.last_launches = _native.lib.alora_model_last_launches(self._handle)
 
     def stage(self, p: dict, kv):
@@ -456,6 +475,7 @@ class Model:
         st.row_apply = base + 4 * int(offs[len(self._FIELDS)])
         st.logits, st.next_ids = self._logits.data_ptr(), self._ids.data_ptr()
         st.attn_kv_tokens, st.attn_qk_pairs = p.get("attn_kv_tokens", 0.0), p.get("attn_qk_pairs", 0.0)
+        self._staged_graphable = bool(p.get("graphable", False))
         self.last_h2d_bytes = 4 * total
         return st
 
