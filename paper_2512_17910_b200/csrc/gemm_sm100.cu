@@ -791,17 +791,21 @@ __global__ void __launch_bounds__(192, 1)
     gemm_dec_kernel(const __grid_constant__ CUtensorMap tm_w, const __grid_constant__ CUtensorMap tm_x,
                     const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_s,
                     const DecArgs args) {
+  // Persistent over N tiles (tile = blockIdx.x + j * gridDim.x): the stage ring runs on across tiles and two
+  // TMEM accumulators alternate, so tile j's epilogue overlaps tile j+1's weight stream (no wave tail on
+  // the 128256-row lm_head).
   using C = DecCfg<MN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
   uint64_t* empty = full + C::kStages;
-  uint64_t* tmem_full = empty + C::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* tmem_full = empty + C::kStages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
   float* xch = reinterpret_cast<float*>(smem + C::kStages * C::kStage + 256);  // [128][33]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * kBM;
+  const int n_tiles = args.N / kBM;
   const int S = args.splits, split = blockIdx.z;
   const int nkb_all = (args.K + kBK - 1) / kBK;
   const int per = (nkb_all + S - 1) / S;
@@ -816,10 +820,13 @@ __global__ void __launch_bounds__(192, 1)
       sm100::mbar_init(&full[i], 1);
       sm100::mbar_init(&empty[i], 1);
     }
-    sm100::mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&tmem_full[b], 1);
+      sm100::mbar_init(&tmem_empty[b], 128);
+    }
     sm100::fence_barrier_init();
   }
-  if (warp == 1) sm100::tmem_alloc<32>(tmem_slot);
+  if (warp == 1) sm100::tmem_alloc<64>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -829,22 +836,19 @@ __global__ void __launch_bounds__(192, 1)
     const uint64_t pol_act = sm100::policy_evict_last();
     const uint64_t pol_w = sm100::policy_evict_first();
     const int n_pre = min(C::kStages, n_base);
-    for (int i = 0; i < n_pre; ++i) {  // weights first: they do not depend on the previous kernel
+    const int first = blockIdx.x;
+    for (int i = 0; i < n_pre; ++i) {  // first tile's weights before the dependency wait
       if (sm100::elect_one()) {
         sm100::mbar_arrive_expect_tx(&full[i], C::kStage);
-        sm100::tma_load_2d(smem + i * C::kStage, &tm_w, &full[i], (kb0 + i) * kBK, n0, pol_w);
+        sm100::tma_load_2d(smem + i * C::kStage, &tm_w, &full[i], (kb0 + i) * kBK, first * kBM, pol_w);
       }
       __syncwarp();
     }
     pdl_wait();
     pdl_trigger();
-    int target = 0, nkl = 0;
     uint32_t mask = 0;
-    if (lora_here) {
-      target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
-      nkl = (args.ks + kBK - 1) / kBK;
-      mask = args.tile_slot_mask[0];
-    }
+    const int nkl = lora_here ? (args.ks + kBK - 1) / kBK : 0;
+    if (lora_here) mask = args.tile_slot_mask[0];
     for (int i = 0; i < n_pre; ++i) {
       if (sm100::elect_one())
         sm100::tma_load_2d(smem + i * C::kStage + C::kWBytes, &tm_x, &full[i], (kb0 + i) * kBK, 0, pol_act);
@@ -853,28 +857,32 @@ __global__ void __launch_bounds__(192, 1)
     int st = n_pre % C::kStages;
     uint32_t phase = n_pre == C::kStages ? 1u : 0u;
     auto next = [&] { if (++st == C::kStages) { st = 0; phase ^= 1; } };
-    for (int kb = kb0 + n_pre; kb < kb1; ++kb) {
-      sm100::mbar_wait(&empty[st], phase ^ 1);
-      if (sm100::elect_one()) {
-        uint8_t* sa = smem + st * C::kStage;
-        sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
-        sm100::tma_load_2d(sa, &tm_w, &full[st], kb * kBK, n0, pol_w);
-        sm100::tma_load_2d(sa + C::kWBytes, &tm_x, &full[st], kb * kBK, 0, pol_act);
+    for (int tile = first; tile < n_tiles; tile += gridDim.x) {
+      const int n0 = tile * kBM;
+      for (int kb = (tile == first ? kb0 + n_pre : kb0); kb < kb1; ++kb) {
+        sm100::mbar_wait(&empty[st], phase ^ 1);
+        if (sm100::elect_one()) {
+          uint8_t* sa = smem + st * C::kStage;
+          sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
+          sm100::tma_load_2d(sa, &tm_w, &full[st], kb * kBK, n0, pol_w);
+          sm100::tma_load_2d(sa + C::kWBytes, &tm_x, &full[st], kb * kBK, 0, pol_act);
+        }
+        __syncwarp();
+        next();
       }
-      __syncwarp();
-      next();
-    }
-    for (int j = 0; j < nkl; ++j) {
-      if (!lora_block_present(j, args.rank, mask)) continue;
-      sm100::mbar_wait(&empty[st], phase ^ 1);
-      if (sm100::elect_one()) {
-        uint8_t* sa = smem + st * C::kStage;
-        sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
-        sm100::tma_load_2d(sa, &tm_u, &full[st], j * kBK, n0, pol_w);
-        sm100::tma_load_3d(sa + C::kWBytes, &tm_s, &full[st], j * kBK, 0, target, pol_act);
+      const int target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+      for (int j = 0; j < nkl; ++j) {
+        if (!lora_block_present(j, args.rank, mask)) continue;
+        sm100::mbar_wait(&empty[st], phase ^ 1);
+        if (sm100::elect_one()) {
+          uint8_t* sa = smem + st * C::kStage;
+          sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
+          sm100::tma_load_2d(sa, &tm_u, &full[st], j * kBK, n0, pol_w);
+          sm100::tma_load_3d(sa + C::kWBytes, &tm_s, &full[st], j * kBK, 0, target, pol_act);
+        }
+        __syncwarp();
+        next();
       }
-      __syncwarp();
-      next();
     }
   } else if (warp == 1) {
     pdl_wait();
@@ -887,83 +895,99 @@ __global__ void __launch_bounds__(192, 1)
     constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, MN);
     int st = 0;
     uint32_t phase = 0;
-    for (int it = 0; it < n_iters; ++it) {
-      sm100::mbar_wait(&full[st], phase);
-      sm100::tc_fence_after();
-      if (sm100::elect_one()) {
-        const uint8_t* sa = smem + st * C::kStage;
-        const uint64_t da = sm100::umma_desc_sw128(sa);
-        const uint64_t db = sm100::umma_desc_sw128(sa + C::kWBytes);
-#pragma unroll
-        for (int k = 0; k < kBK / 16; ++k)
-          sm100::mma_bf16_ss(tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (it > 0 || k > 0) ? 1u : 0u);
-        sm100::mma_commit(&empty[st]);
+    int j = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+      const int b = j & 1;
+      if (j >= 2) {  // the epilogue has drained this accumulator (tile j-2)
+        sm100::mbar_wait(&tmem_empty[b], ((j - 2) >> 1) & 1);
+        sm100::tc_fence_after();
       }
+      for (int it = 0; it < n_iters; ++it) {
+        sm100::mbar_wait(&full[st], phase);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint8_t* sa = smem + st * C::kStage;
+          const uint64_t da = sm100::umma_desc_sw128(sa);
+          const uint64_t db = sm100::umma_desc_sw128(sa + C::kWBytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            sm100::mma_bf16_ss(tmem + b * 32, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                               (it > 0 || k > 0) ? 1u : 0u);
+          sm100::mma_commit(&empty[st]);
+        }
+        __syncwarp();
+        if (++st == C::kStages) { st = 0; phase ^= 1; }
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&tmem_full[b]);
       __syncwarp();
-      if (++st == C::kStages) { st = 0; phase ^= 1; }
     }
-    if (sm100::elect_one()) sm100::mma_commit(tmem_full);
-    __syncwarp();
   } else {
     pdl_wait();
     const int quarter = warp & 3;
-    const int ncol = n0 + quarter * 32 + lane;  // this thread's output column (TMEM lane)
     const bool has_acc = n_base > 0 || lora_here;
-    sm100::mbar_wait(tmem_full, 0);
-    sm100::tc_fence_after();
-    uint32_t r[32];
-    sm100::tmem_ld_32x32b_x32(tmem + ((uint32_t)(quarter * 32) << 16), r);
-    sm100::tmem_ld_wait();
-    float v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = has_acc ? __uint_as_float(r[j]) : 0.f;
     const int M = args.M;
-    if (args.mode == kDecPartial) {
-      float* dst = args.out + (int64_t)split * M * args.N + ncol;
+    int j = 0;
+    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++j) {
+      const int b = j & 1;
+      const int n0 = tile * kBM;
+      const int ncol = n0 + quarter * 32 + lane;  // this thread's output column (TMEM lane)
+      sm100::mbar_wait(&tmem_full[b], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      uint32_t r[32];
+      sm100::tmem_ld_32x32b_x32(tmem + b * 32 + ((uint32_t)(quarter * 32) << 16), r);
+      sm100::tmem_ld_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&tmem_empty[b]);  // the accumulator may be reused while the stores below run
+      float v[32];
 #pragma unroll
-      for (int m = 0; m < MN; ++m)
-        if (m < M) dst[(int64_t)m * args.N] = v[m];
-    } else if (args.mode == kDecAdd) {
-#pragma unroll
-      for (int m = 0; m < MN; ++m)
-        if (m < M) args.out[(int64_t)m * args.ldc + ncol] += v[m];
-    } else if (args.mode == kDecStoreF32) {
-#pragma unroll
-      for (int m = 0; m < MN; ++m)
-        if (m < M) args.out[(int64_t)m * args.ldc + ncol] = v[m];
-      if (args.argmax) {
-#pragma unroll
-        for (int m = 0; m < MN; ++m) {
-          if (m >= M) break;
-          uint32_t u32 = __float_as_uint(v[m]);
-          u32 = (u32 & 0x80000000u) ? ~u32 : (u32 | 0x80000000u);
-          unsigned long long key = ((unsigned long long)u32 << 32) | (0xFFFFFFFFu - (uint32_t)ncol);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
-            key = other > key ? other : key;
-          }
-          if (lane == 0) atomicMax(args.argmax + m, key);
-        }
-      }
-    } else {  // kDecSwiglu: lanes 0-63 of the 128-row tile are gate rows, 64-127 the matching up rows
-      const int row = quarter * 32 + lane;
-#pragma unroll
-      for (int m = 0; m < MN; ++m) xch[row * 33 + m] = v[m];
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      if (quarter < 2) {
-        const int j = row;  // output column n0/2 + j
+      for (int q = 0; q < 32; ++q) v[q] = has_acc ? __uint_as_float(r[q]) : 0.f;
+      if (args.mode == kDecPartial) {
+        float* dst = args.out + (int64_t)split * M * args.N + ncol;
 #pragma unroll
         for (int m = 0; m < MN; ++m)
-          if (m < M)
-            args.out_bf16[(int64_t)m * args.ld_bf16 + n0 / 2 + j] =
-                __float2bfloat16_rn(silu(xch[j * 33 + m]) * xch[(j + 64) * 33 + m]);
+          if (m < M) dst[(int64_t)m * args.N] = v[m];
+      } else if (args.mode == kDecAdd) {
+#pragma unroll
+        for (int m = 0; m < MN; ++m)
+          if (m < M) args.out[(int64_t)m * args.ldc + ncol] += v[m];
+      } else if (args.mode == kDecStoreF32) {
+#pragma unroll
+        for (int m = 0; m < MN; ++m)
+          if (m < M) args.out[(int64_t)m * args.ldc + ncol] = v[m];
+        if (args.argmax) {
+#pragma unroll
+          for (int m = 0; m < MN; ++m) {
+            if (m >= M) break;
+            uint32_t u32 = __float_as_uint(v[m]);
+            u32 = (u32 & 0x80000000u) ? ~u32 : (u32 | 0x80000000u);
+            unsigned long long key = ((unsigned long long)u32 << 32) | (0xFFFFFFFFu - (uint32_t)ncol);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+              key = other > key ? other : key;
+            }
+            if (lane == 0) atomicMax(args.argmax + m, key);
+          }
+        }
+      } else {  // kDecSwiglu: lanes 0-63 of the 128-row tile are gate rows, 64-127 the matching up rows
+        const int row = quarter * 32 + lane;
+#pragma unroll
+        for (int m = 0; m < MN; ++m) xch[row * 33 + m] = v[m];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (quarter < 2) {
+#pragma unroll
+          for (int m = 0; m < MN; ++m)
+            if (m < M)
+              args.out_bf16[(int64_t)m * args.ld_bf16 + n0 / 2 + row] =
+                  __float2bfloat16_rn(silu(xch[row * 33 + m]) * xch[(row + 64) * 33 + m]);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // xch is rewritten by the next tile
       }
     }
   }
   sm100::tc_fence_before();
   __syncthreads();
-  if (warp == 1) sm100::tmem_dealloc<32>(tmem);
+  if (warp == 1) sm100::tmem_dealloc<64>(tmem);
 }
 
 template <int MN>
@@ -977,7 +1001,9 @@ int launch_dec(const CUtensorMap& w, const CUtensorMap& x, const CUtensorMap& u,
       return ALORA_ECUDA;
     configured = true;
   }
-  const dim3 grid(args.N / kBM, 1, args.splits);
+  const int tiles = args.N / kBM;
+  const int per_split = std::max(1, kNumSMs / args.splits);  // persistent: at most one CTA per SM
+  const dim3 grid(std::min(tiles, per_split), 1, args.splits);
   if (launch_pdl(gemm_dec_kernel<MN>, grid, dim3(192), C::kSmem, st, nullptr, 0, w, x, u, sm, args) != cudaSuccess)
     return ALORA_ECUDA;
   ALORA_LAUNCH_CHECK();
