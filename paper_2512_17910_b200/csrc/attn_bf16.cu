@@ -551,7 +551,9 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;  // step metadata: uploaded before the forward
     const int last_blk = (key_end - 1) / a.B;
     const int per_tile = kKT / a.B;
-    const uint64_t pol = sm100::policy_evict_last();  // a conversation's prefix is read by each adapter's request
+    // KV streams through L2 with evict_first: keeping it (evict_last) pushed the next kernels' weights and
+    // split-K partials out of L2 and cost ~3.5% of the forward (measured A/B)
+    const uint64_t pol = sm100::policy_evict_first();
     auto issue_kv = [&](int t) {  // K/V tile t: TMA boxes of [B keys x 64 dims], page by page via the block table
       const int st = t % kNS<D>;
       sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
