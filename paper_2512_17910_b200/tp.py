@@ -177,6 +177,8 @@ class TPModel(Model):
 
         self._tp_cb = _native.ALLREDUCE_FN(_cb)  # kept alive for the handle's lifetime
         self._tp = (group.size, ctypes.cast(self._tp_cb, ctypes.c_void_p).value) if group.size > 1 else None
+        # the all-reduce hook is a host callback (stream syncs / host barriers): not capturable in a CUDA graph
+        kw.setdefault("graphs", group.size <= 1)
         super().__init__(scfg, weights=weights, init=init, **kw)
         self.pool_kv_width = scfg.kv_width
 
