@@ -77,6 +77,7 @@ struct Blake2b {
     v[c] = v[c] + v[d];              \
     v[b] = rotr(v[b] ^ v[c], 63);    \
   } while (0)
+#pragma GCC unroll 12
     for (int r = 0; r < 12; ++r) {
       const uint8_t* s = kSigma[r];
       G(0, 4, 8, 12, m[s[0]], m[s[1]]);
