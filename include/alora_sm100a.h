@@ -40,6 +40,8 @@ extern "C" {
 #define ALORA_EINVAL (-1)
 #define ALORA_ECUDA (-2)
 #define ALORA_EUNSUPPORTED (-3)
+#define ALORA_ENOSPC (-4) /* block pool: not enough free blocks (PoolExhaustedError) */
+#define ALORA_ESTATE (-5) /* block pool: an invariant the call relies on does not hold */
 
 #define ALORA_F32 0
 #define ALORA_BF16 1
@@ -63,6 +65,48 @@ int alora_hash_block(const uint8_t* parent, const uint32_t* tokens, int32_t bloc
 int alora_hash_chain(const uint8_t* parent, const uint32_t* tokens, int64_t n_blocks,
                      int32_t block_size, const char* key_blob, const int64_t* key_off,
                      uint8_t* out_digests);
+
+/* n_chains independent alora_hash_chain calls (arguments per chain, parents
+ * may be NULL = every chain starts fresh), spread over up to n_threads host
+ * threads. Replaces the per-request chain walks of one scheduler step
+ * (kv_cache.py:166-182 called from scheduler.py admission, 253-260 at retire). */
+int alora_hash_chains(int32_t n_chains, const uint8_t* const* parents, const uint32_t* const* tokens,
+                      const int64_t* n_blocks, int32_t block_size, const char* const* key_blobs,
+                      const int64_t* const* key_offs, uint8_t* const* out_digests, int32_t n_threads);
+
+/* The admission lookup chains of n_req requests in one call: request r's prompt
+ * (int64 token ids, validated < 2^32) gives n_blocks[r] digests; blocks
+ * [0, n_base[r]) carry the base key "" and the rest keys[r] (compute_block_keys,
+ * kv_cache.py:72-96). Digests land back to back in out_digests (sum n_blocks * 16). */
+int alora_hash_requests(int32_t n_req, const int64_t* const* tokens, const int64_t* n_blocks, const int64_t* n_base,
+                        const char* const* keys, const int32_t* key_lens, int32_t block_size,
+                        uint8_t* out_digests, int32_t n_threads);
+
+/* ------------------------------------------------------- block manager ---- */
+/* Per-block state of the paged KV pool and its digest index (kv_cache.py:126-326
+ * BlockPool; the per-request maps stay with the caller). Digests are 16 bytes. */
+void* alora_pool_create(int32_t n_blocks, int32_t block_size);
+void alora_pool_destroy(void* pool);
+/* Host pointers to the pool's own arrays: ref_count[nb], fill[nb], has_hash[nb], hash[nb*16]. */
+int alora_pool_views(void* pool, int32_t** ref, int32_t** fill, uint8_t** has_hash, uint8_t** hash);
+int32_t alora_pool_num_free(void* pool);
+/* find_cached_prefix walk (kv_cache.py:154-183): pins and returns the hit count (>= 0). */
+int64_t alora_pool_lookup(void* pool, const uint8_t* digests, int64_t n, int32_t* out_ids);
+/* allocate (kv_cache.py:192-218): ALORA_ENOSPC and no change when n > free blocks. */
+int alora_pool_allocate(void* pool, int64_t n, int32_t* out_ids);
+/* release of a request's blocks, tail first (kv_cache.py:258-270). */
+int alora_pool_release(void* pool, const int32_t* ids, int64_t n);
+/* commit: digest i -> block ids[i] (full blocks only), index overwritten (kv_cache.py:250-257). */
+int alora_pool_publish(void* pool, const int32_t* ids, const uint8_t* digests, int64_t n);
+/* set_fill (kv_cache.py:220-223) for the n blocks ids[0..n) of a request that hold its
+ * block positions first .. first+n-1. */
+int alora_pool_set_fill(void* pool, const int32_t* ids, int64_t n, int64_t first, int64_t n_tokens);
+/* Free blocks in eviction order (least recently released first); returns the count. */
+int64_t alora_pool_free_list(void* pool, int32_t* out, int64_t cap);
+/* Block id indexed under `digest`, or -1. */
+int32_t alora_pool_index_get(void* pool, const uint8_t* digest);
+/* Index entries (cap <= 0: just the count). */
+int64_t alora_pool_index_dump(void* pool, uint8_t* digests, int32_t* ids, int64_t cap);
 
 /* ------------------------------------------------------ hot-path kernels ---- */
 

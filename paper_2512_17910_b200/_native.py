@@ -17,6 +17,8 @@ ALORA_OK = 0
 ALORA_EINVAL = -1
 ALORA_ECUDA = -2
 ALORA_EUNSUPPORTED = -3
+ALORA_ENOSPC = -4
+ALORA_ESTATE = -5
 ALORA_F32 = 0
 ALORA_BF16 = 1
 ALORA_ARCH_REF = 0
@@ -85,6 +87,22 @@ EXPORTS = {
     "alora_hash_block": _sig("alora_hash_block", c_i32, c_void_p, c_void_p, c_i32, ctypes.c_char_p, c_i32, c_void_p),
     "alora_hash_chain": _sig("alora_hash_chain", c_i32, c_void_p, c_void_p, c_i64, c_i32, ctypes.c_char_p,
                              c_void_p, c_void_p),
+    "alora_hash_chains": _sig("alora_hash_chains", c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_i32, c_void_p,
+                              c_void_p, c_void_p, c_i32),
+    "alora_hash_requests": _sig("alora_hash_requests", c_i32, c_i32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_i32, c_void_p, c_i32),
+    "alora_pool_create": _sig("alora_pool_create", c_void_p, c_i32, c_i32),
+    "alora_pool_destroy": _sig("alora_pool_destroy", None, c_void_p),
+    "alora_pool_views": _sig("alora_pool_views", c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p),
+    "alora_pool_num_free": _sig("alora_pool_num_free", c_i32, c_void_p),
+    "alora_pool_lookup": _sig("alora_pool_lookup", c_i64, c_void_p, c_void_p, c_i64, c_void_p),
+    "alora_pool_allocate": _sig("alora_pool_allocate", c_i32, c_void_p, c_i64, c_void_p),
+    "alora_pool_release": _sig("alora_pool_release", c_i32, c_void_p, c_void_p, c_i64),
+    "alora_pool_publish": _sig("alora_pool_publish", c_i32, c_void_p, c_void_p, c_void_p, c_i64),
+    "alora_pool_set_fill": _sig("alora_pool_set_fill", c_i32, c_void_p, c_void_p, c_i64, c_i64, c_i64),
+    "alora_pool_free_list": _sig("alora_pool_free_list", c_i64, c_void_p, c_void_p, c_i64),
+    "alora_pool_index_get": _sig("alora_pool_index_get", c_i32, c_void_p, c_void_p),
+    "alora_pool_index_dump": _sig("alora_pool_index_dump", c_i64, c_void_p, c_void_p, c_void_p, c_i64),
     "alora_qkv_proj": _sig("alora_qkv_proj", c_i32, c_i32, c_void_p, c_i32, c_i32, c_void_p, c_i32, c_i32,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                            c_i32, c_void_p),
@@ -118,6 +136,8 @@ def check(rc: int, what: str) -> None:
         return
     if rc == ALORA_EINVAL:
         raise ValueError(f"{what}: invalid argument (ALORA_EINVAL)")
+    if rc == ALORA_ESTATE:
+        raise AssertionError(f"{what}: block pool invariant violated (ALORA_ESTATE)")
     if rc == ALORA_EUNSUPPORTED:
         raise RuntimeError(f"{what}: unsupported configuration (ALORA_EUNSUPPORTED)")
     raise RuntimeError(f"{what}: CUDA error (status {rc})")

@@ -11,7 +11,9 @@
 // BLAKE2b is RFC 7693 with digest length 16, no key, no salt/personal.
 
 #include <cstdint>
+#include <atomic>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "../../include/alora_sm100a.h"
@@ -174,6 +176,97 @@ int alora_hash_chain(const uint8_t* parent, const uint32_t* tokens, int64_t n_bl
     prev = out_digests + 16 * i;
   }
   return ALORA_OK;
+}
+
+int alora_hash_requests(int32_t n_req, const int64_t* const* tokens, const int64_t* n_blocks, const int64_t* n_base,
+                        const char* const* keys, const int32_t* key_lens, int32_t block_size,
+                        uint8_t* out_digests, int32_t n_threads) {
+  if (n_req < 0 || block_size < 1) return ALORA_EINVAL;
+  if (n_req == 0) return ALORA_OK;
+  if (tokens == nullptr || n_blocks == nullptr || n_base == nullptr || keys == nullptr || key_lens == nullptr ||
+      out_digests == nullptr)
+    return ALORA_EINVAL;
+  std::vector<int64_t> first(static_cast<size_t>(n_req) + 1, 0);  // digest offset of each request
+  for (int32_t r = 0; r < n_req; ++r) {
+    if (n_blocks[r] < 0 || key_lens[r] < 0 || (key_lens[r] > 0 && keys[r] == nullptr)) return ALORA_EINVAL;
+    first[r + 1] = first[r] + n_blocks[r];
+  }
+  const int64_t total = first[n_req];
+  int64_t want = total / 192;  // a thread pays for its spawn above a few hundred blocks
+  if (want > n_threads) want = n_threads;
+  if (want > n_req) want = n_req;
+  std::atomic<int32_t> next{0};
+  std::atomic<int> status{ALORA_OK};
+  auto work = [&]() {
+    std::vector<uint32_t> blk(static_cast<size_t>(block_size));
+    for (int32_t r; (r = next.fetch_add(1)) < n_req;) {
+      const uint8_t* prev = nullptr;
+      uint8_t* out = out_digests + 16 * first[r];
+      for (int64_t i = 0; i < n_blocks[r]; ++i) {
+        const int64_t* t = tokens[r] + i * block_size;
+        for (int32_t j = 0; j < block_size; ++j) {
+          if (t[j] < 0 || t[j] > 0xffffffffLL) {
+            status.store(ALORA_EINVAL);
+            return;
+          }
+          blk[j] = static_cast<uint32_t>(t[j]);
+        }
+        // blocks [0, n_base) carry the base key "", the rest the request's key (compute_block_keys)
+        const bool base = i < n_base[r];
+        hash_one(prev, blk.data(), block_size, base ? "" : keys[r], base ? 0 : key_lens[r], out + 16 * i);
+        prev = out + 16 * i;
+      }
+    }
+  };
+  if (want <= 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    for (int64_t t = 1; t < want; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  }
+  return status.load();
+}
+
+int alora_hash_chains(int32_t n_chains, const uint8_t* const* parents, const uint32_t* const* tokens,
+                      const int64_t* n_blocks, int32_t block_size, const char* const* key_blobs,
+                      const int64_t* const* key_offs, uint8_t* const* out_digests, int32_t n_threads) {
+  if (n_chains < 0 || block_size < 1) return ALORA_EINVAL;
+  if (n_chains == 0) return ALORA_OK;
+  if (tokens == nullptr || n_blocks == nullptr || key_blobs == nullptr || key_offs == nullptr ||
+      out_digests == nullptr)
+    return ALORA_EINVAL;
+  int64_t total = 0;
+  for (int32_t c = 0; c < n_chains; ++c) {
+    if (n_blocks[c] < 0) return ALORA_EINVAL;
+    total += n_blocks[c];
+  }
+  // chains are independent; each is sequential (block i hashes digest i-1). Threads take whole chains
+  // from a shared counter; a thread is worth its ~20 us spawn only above a few hundred blocks.
+  const int64_t kBlocksPerThread = 192;
+  int64_t want = total / kBlocksPerThread;
+  if (want > n_threads) want = n_threads;
+  if (want > n_chains) want = n_chains;
+  std::atomic<int32_t> next{0};
+  std::atomic<int> status{ALORA_OK};
+  auto work = [&]() {
+    for (int32_t c; (c = next.fetch_add(1)) < n_chains;) {
+      int rc = alora_hash_chain(parents ? parents[c] : nullptr, tokens[c], n_blocks[c], block_size, key_blobs[c],
+                                key_offs[c], out_digests[c]);
+      if (rc != ALORA_OK) status.store(rc);
+    }
+  };
+  if (want <= 1) {
+    work();
+  } else {
+    std::vector<std::thread> pool;
+    pool.reserve(static_cast<size_t>(want - 1));
+    for (int64_t t = 1; t < want; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  }
+  return status.load();
 }
 
 }  // extern "C"

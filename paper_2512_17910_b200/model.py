@@ -360,61 +360,68 @@ class Model:
             raise ValueError("no spans")
         if S > self._max_seqs:
             raise ValueError(f"{S} spans exceed max_seqs {self._max_seqs}")
-        lens, starts, slots, applies, toks, tables = [], [], [], [], [], []
-        for seq in seqs:
+        lens, starts, slot_ids, masked, toks, tables = [], [], [], [], [], []
+        const_apply = []
+        for i, seq in enumerate(seqs):
             tk = np.asarray(seq.tokens, dtype=np.int64).reshape(-1)
             n = len(tk)
             if n == 0:
                 raise ValueError("empty span")
             if seq.start_pos < 0 or seq.start_pos + n > cfg.max_seq_len:
                 raise ValueError("span exceeds max_seq_len")
-            if tk.min() < 0 or tk.max() >= cfg.vocab_size:
-                raise ValueError("token id outside the vocabulary")
             need = -(-(seq.start_pos + n) // block_size)
             if len(seq.block_ids) < need:
                 raise ValueError(f"block table has {len(seq.block_ids)} blocks, need {need}")
             ad = seq.adapter
             if ad is None:
-                apply = np.zeros(n, dtype=np.uint8)
+                const_apply.append(0)
             elif ad.mode == MODE_ACTIVATED:
                 if seq.mask is None:
                     raise ValueError(f"activated adapter span for {seq.request_id} is missing its mask")
                 m = np.asarray(seq.mask, dtype=bool)
                 if m.shape != (n,):
                     raise ValueError(f"mask shape {m.shape} does not match {n} rows")
-                apply = (~m).astype(np.uint8)
+                const_apply.append(0)
+                masked.append((i, m))
             else:  # standard LoRA: adapted on every row (model.py:260-261)
-                apply = np.ones(n, dtype=np.uint8)
-            slots.append(np.full(n, self._slot_for(ad), dtype=np.int32))
-            applies.append(apply)
+                const_apply.append(1)
+            slot_ids.append(self._slot_for(ad))
             lens.append(n)
             starts.append(int(seq.start_pos))
             toks.append(tk)
-            tables.append(np.asarray(seq.block_ids[:need], dtype=np.int64))
+            tables.append(seq.block_ids[:need])
+        tokens = np.concatenate(toks) if S > 1 else toks[0]
+        if tokens.min() < 0 or tokens.max() >= cfg.vocab_size:
+            raise ValueError("token id outside the vocabulary")
         M = int(sum(lens))
+        lens_a = np.asarray(lens, dtype=np.int64)
+        starts_a = np.asarray(starts, dtype=np.int64)
+        cu = np.zeros(S + 1, dtype=np.int32)
+        np.cumsum(lens_a, out=cu[1:])
+        row_seq = np.repeat(np.arange(S), lens_a)
+        positions = (np.arange(M, dtype=np.int64) - np.repeat(cu[:-1] - starts_a, lens_a)).astype(np.int32)
+        row_apply = np.repeat(np.asarray(const_apply, dtype=np.uint8), lens_a)
+        for i, m in masked:
+            row_apply[cu[i]:cu[i + 1]] = ~m
         maxb = max(len(tb) for tb in tables)
         graphable = self._graphs and max(lens) == 1  # a decode step: replay a captured graph
         if graphable:  # bucket the table width (and the context bound below) so one capture serves many steps
             bb = self.GRAPH_BLOCK_BUCKET
             maxb = -(-maxb // bb) * bb
-        cu = np.zeros(S + 1, dtype=np.int32)
-        np.cumsum(lens, out=cu[1:])
-        positions = np.concatenate([np.arange(s, s + n, dtype=np.int32) for s, n in zip(starts, lens)])
         bt = np.zeros((S, maxb), dtype=np.int32)
-        slot_map = np.empty(M, dtype=np.int32)
         for i, tb in enumerate(tables):
             bt[i, :len(tb)] = tb
-            p = positions[cu[i]:cu[i + 1]]
-            slot_map[cu[i]:cu[i + 1]] = tb[p // block_size] * block_size + p % block_size
+        slot_map = (bt[row_seq, positions // block_size] * block_size + positions % block_size).astype(np.int32)
+        ends = starts_a + lens_a
         return {
-            "attn_kv_tokens": float(sum(s + n for s, n in zip(starts, lens))),
-            "attn_qk_pairs": float(sum(n * (s + (n + 1) / 2) for s, n in zip(starts, lens))),
-            "M": M, "S": S, "maxb": maxb, "max_q": int(max(lens)),
-            "max_ctx": maxb * block_size if graphable else int(max(s + n for s, n in zip(starts, lens))),
+            "attn_kv_tokens": float(ends.sum()),
+            "attn_qk_pairs": float((lens_a * (starts_a + (lens_a + 1) / 2)).sum()),
+            "M": M, "S": S, "maxb": maxb, "max_q": int(lens_a.max()),
+            "max_ctx": maxb * block_size if graphable else int(ends.max()),
             "graphable": graphable,
-            "tokens": np.concatenate(toks).astype(np.int32), "positions": positions, "slot_mapping": slot_map,
-            "row_slot": np.concatenate(slots), "row_apply": np.concatenate(applies),
-            "cu_q": cu, "start_pos": np.asarray(starts, dtype=np.int32), "last_row": (cu[1:] - 1).astype(np.int32),
+            "tokens": tokens.astype(np.int32), "positions": positions, "slot_mapping": slot_map,
+            "row_slot": np.repeat(np.asarray(slot_ids, dtype=np.int32), lens_a), "row_apply": row_apply,
+            "cu_q": cu, "start_pos": starts_a.astype(np.int32), "last_row": (cu[1:] - 1).astype(np.int32),
             "block_table": bt,
         }
 

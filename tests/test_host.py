@@ -52,6 +52,50 @@ def test_native_hash_long_keys_and_multiblock_messages():
                 assert P.hash_block(p, toks, key, B) == O.hash_block(p, toks, key, B)
 
 
+def test_batched_chains_and_commit_digest_reuse_match_oracle():
+    from paper_2512_17910_b200 import kv_cache as K
+
+    rng = np.random.default_rng(11)
+    B = 16
+    chains = []
+    for n_tok, split in ((4096, 100), (17, 0), (15, 0), (700, 30), (2052, 128)):
+        toks = rng.integers(0, 2**32, n_tok, dtype=np.uint64).astype(np.int64)
+        nb = -(-n_tok // B)
+        chains.append((toks, n_tok // B, [""] * split + ["adapter0"] * (nb - split)))
+    got = K.hash_chains(chains, B, n_threads=4)
+    for (toks, n, keys), dg in zip(chains, got):
+        want, parent = [], None
+        for i in range(n):
+            parent = O.hash_block(parent, toks[i * B:(i + 1) * B].tolist(), keys[i], B)
+            want.append(parent)
+        assert dg == want
+    # the scheduler's batched admission hashing (two-run keys) equals the per-request chain
+    items, want = [], []
+    for n_tok, adapter, inv in ((2052, None, None), (33, "std", None), (2052, "act", 2040), (48, "act", 32),
+                                (47, "act", 0), (17, "act", 17), (5, None, None)):
+        toks = rng.integers(0, 2**32, n_tok, dtype=np.uint64).astype(np.int64)
+        keys = P.compute_block_keys(toks, B, adapter_id=adapter, inv_start=inv)
+        n = max(0, (n_tok - 1) // B)
+        n_base = n if adapter is None else (0 if inv is None else min(-(-n_tok // B), inv // B))
+        items.append((toks, n, n_base, adapter or ""))
+        want.append(b"".join(P.hash_chain(toks, n, B, keys)))
+    assert K.hash_requests(items, B, n_threads=3) == want
+    with pytest.raises(ValueError):
+        K.hash_requests([(np.array([-1] * 32), 2, 2, "")], B)
+    # commit_and_free reuses the admission chain for the unchanged prefix and hashes the rest
+    pool = P.BlockPool(64, B, 1, 8, storage="numpy")
+    prompt = rng.integers(0, 1000, 70)
+    keys = P.compute_block_keys(prompt, B)
+    pool.find_cached_prefix("r", prompt, keys)
+    pool.allocate("r", 5)
+    seq = np.concatenate([prompt, rng.integers(0, 1000, 10)])
+    pool.set_fill("r", len(seq))
+    pool.commit_and_free("r", seq, P.compute_block_keys(seq, B))
+    ref = P.hash_chain(seq, len(seq) // B, B, P.compute_block_keys(seq, B))
+    assert [pool.blocks[pool._index[d]].hash for d in ref] == ref
+    pool.check_conservation()
+
+
 def test_hash_validation_errors():
     with pytest.raises(ValueError):
         P.hash_block(None, [1, 2], "", 3)
