@@ -12,7 +12,10 @@
 
 #include <cstdint>
 #include <atomic>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -130,6 +133,66 @@ struct Blake2b {
 
 const char kDomain[] = "aloraserve.block.v1";
 
+// Persistent helper threads for the batched hashes: spawning threads inside a process that has torch /
+// the CUDA runtime loaded costs ~100 us each (per-thread TLS set-up), more than the hashing they would
+// share, so the helpers are created once and parked on a condition variable. run(k, f) runs f on the
+// caller plus k-1 helpers; f pulls work from its own atomic counter, so a helper that finds none returns.
+class Helpers {
+ public:
+  void run(int k, const std::function<void()>& f) {
+    if (k <= 1) {
+      f();
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);  // one batched call at a time
+    {
+      std::lock_guard<std::mutex> l(mu_);
+      while (static_cast<int>(threads_.size()) < k - 1) {
+        threads_.emplace_back([this] { loop(); });
+        threads_.back().detach();
+      }
+      job_ = &f;
+      want_ = k - 1;
+      pending_ = k - 1;
+      ++gen_;
+    }
+    cv_.notify_all();
+    f();
+    std::unique_lock<std::mutex> l(mu_);
+    done_.wait(l, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void()>* j = nullptr;
+      {
+        std::unique_lock<std::mutex> l(mu_);
+        cv_.wait(l, [&] { return gen_ != seen && want_ > 0; });
+        seen = gen_;
+        --want_;
+        j = job_;
+      }
+      (*j)();
+      std::lock_guard<std::mutex> l(mu_);
+      if (--pending_ == 0) done_.notify_all();
+    }
+  }
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_;
+  std::vector<std::thread> threads_;
+  const std::function<void()>* job_ = nullptr;
+  uint64_t gen_ = 0;
+  int want_ = 0, pending_ = 0;
+};
+
+Helpers& helpers() {
+  static Helpers* h = new Helpers();  // never destroyed: parked helpers die with the process
+  return *h;
+}
+
 void hash_one(const uint8_t* parent, const uint32_t* tokens, int32_t block_size, const char* key,
               int32_t key_len, uint8_t* out) {
   Blake2b b(16);
@@ -191,41 +254,75 @@ int alora_hash_requests(int32_t n_req, const int64_t* const* tokens, const int64
     if (n_blocks[r] < 0 || key_lens[r] < 0 || (key_lens[r] > 0 && keys[r] == nullptr)) return ALORA_EINVAL;
     first[r + 1] = first[r] + n_blocks[r];
   }
-  const int64_t total = first[n_req];
-  int64_t want = total / 192;  // a thread pays for its spawn above a few hundred blocks
-  if (want > n_threads) want = n_threads;
-  if (want > n_req) want = n_req;
-  std::atomic<int32_t> next{0};
-  std::atomic<int> status{ALORA_OK};
-  auto work = [&]() {
-    std::vector<uint32_t> blk(static_cast<size_t>(block_size));
-    for (int32_t r; (r = next.fetch_add(1)) < n_req;) {
-      const uint8_t* prev = nullptr;
-      uint8_t* out = out_digests + 16 * first[r];
-      for (int64_t i = 0; i < n_blocks[r]; ++i) {
-        const int64_t* t = tokens[r] + i * block_size;
-        for (int32_t j = 0; j < block_size; ++j) {
-          if (t[j] < 0 || t[j] > 0xffffffffLL) {
-            status.store(ALORA_EINVAL);
-            return;
-          }
-          blk[j] = static_cast<uint32_t>(t[j]);
-        }
-        // blocks [0, n_base) carry the base key "", the rest the request's key (compute_block_keys)
-        const bool base = i < n_base[r];
-        hash_one(prev, blk.data(), block_size, base ? "" : keys[r], base ? 0 : key_lens[r], out + 16 * i);
-        prev = out + 16 * i;
+  // Requests admitted together often share their base-key region (several adapters evaluated on one
+  // conversation): same n_base and the same tokens there give the same digests, so a follower copies
+  // its leader's and hashes only its own tail.
+  std::vector<int32_t> leader(static_cast<size_t>(n_req));
+  std::vector<int64_t> nbe(static_cast<size_t>(n_req));
+  std::vector<uint64_t> fp(static_cast<size_t>(n_req), 0);
+  for (int32_t r = 0; r < n_req; ++r) {
+    leader[r] = r;
+    nbe[r] = n_base[r] < 0 ? 0 : (n_base[r] < n_blocks[r] ? n_base[r] : n_blocks[r]);
+    if (nbe[r] == 0) continue;
+    const int64_t n = nbe[r] * block_size;
+    uint64_t h = 0x9e3779b97f4a7c15ULL ^ static_cast<uint64_t>(n);
+    for (int64_t i = 0; i < n; ++i) h = (h ^ static_cast<uint64_t>(tokens[r][i])) * 0x100000001b3ULL;
+    fp[r] = h;
+    for (int32_t q = 0; q < r; ++q)
+      if (leader[q] == q && nbe[q] == nbe[r] && fp[q] == h &&
+          std::memcmp(tokens[q], tokens[r], static_cast<size_t>(n) * sizeof(int64_t)) == 0) {
+        leader[r] = q;
+        break;
       }
+  }
+  std::atomic<int> status{ALORA_OK};
+  // hash request r's blocks [from, n_blocks) chained from `prev`
+  auto hash_tail = [&](int32_t r, int64_t from, const uint8_t* prev, std::vector<uint32_t>& blk) {
+    uint8_t* out = out_digests + 16 * first[r];
+    for (int64_t i = from; i < n_blocks[r]; ++i) {
+      const int64_t* t = tokens[r] + i * block_size;
+      for (int32_t j = 0; j < block_size; ++j) {
+        if (t[j] < 0 || t[j] > 0xffffffffLL) {
+          status.store(ALORA_EINVAL);
+          return;
+        }
+        blk[j] = static_cast<uint32_t>(t[j]);
+      }
+      // blocks [0, n_base) carry the base key "", the rest the request's key (compute_block_keys)
+      const bool base = i < n_base[r];
+      hash_one(prev, blk.data(), block_size, base ? "" : keys[r], base ? 0 : key_lens[r], out + 16 * i);
+      prev = out + 16 * i;
     }
   };
-  if (want <= 1) {
-    work();
-  } else {
-    std::vector<std::thread> pool;
-    for (int64_t t = 1; t < want; ++t) pool.emplace_back(work);
-    work();
-    for (auto& t : pool) t.join();
-  }
+  auto run = [&](bool followers) {
+    int64_t work_blocks = 0;
+    std::vector<int32_t> todo;
+    for (int32_t r = 0; r < n_req; ++r)
+      if ((leader[r] != r) == followers) {
+        todo.push_back(r);
+        work_blocks += followers ? n_blocks[r] - nbe[r] : n_blocks[r];
+      }
+    int64_t want = work_blocks / 96;  // a parked helper pays for its wake-up above ~100 blocks
+    if (want > n_threads) want = n_threads;
+    if (want > static_cast<int64_t>(todo.size())) want = static_cast<int64_t>(todo.size());
+    std::atomic<size_t> next{0};
+    auto work = [&]() {
+      std::vector<uint32_t> blk(static_cast<size_t>(block_size));
+      for (size_t k; (k = next.fetch_add(1)) < todo.size();) {
+        const int32_t r = todo[k];
+        if (!followers) {
+          hash_tail(r, 0, nullptr, blk);
+        } else {
+          uint8_t* out = out_digests + 16 * first[r];
+          std::memcpy(out, out_digests + 16 * first[leader[r]], static_cast<size_t>(16 * nbe[r]));
+          hash_tail(r, nbe[r], out + 16 * (nbe[r] - 1), blk);
+        }
+      }
+    };
+    helpers().run(static_cast<int>(want), work);
+  };
+  run(false);
+  if (status.load() == ALORA_OK) run(true);
   return status.load();
 }
 
@@ -243,8 +340,8 @@ int alora_hash_chains(int32_t n_chains, const uint8_t* const* parents, const uin
     total += n_blocks[c];
   }
   // chains are independent; each is sequential (block i hashes digest i-1). Threads take whole chains
-  // from a shared counter; a thread is worth its ~20 us spawn only above a few hundred blocks.
-  const int64_t kBlocksPerThread = 192;
+  // from a shared counter (parked helpers, see Helpers).
+  const int64_t kBlocksPerThread = 96;
   int64_t want = total / kBlocksPerThread;
   if (want > n_threads) want = n_threads;
   if (want > n_chains) want = n_chains;
@@ -257,15 +354,7 @@ int alora_hash_chains(int32_t n_chains, const uint8_t* const* parents, const uin
       if (rc != ALORA_OK) status.store(rc);
     }
   };
-  if (want <= 1) {
-    work();
-  } else {
-    std::vector<std::thread> pool;
-    pool.reserve(static_cast<size_t>(want - 1));
-    for (int64_t t = 1; t < want; ++t) pool.emplace_back(work);
-    work();
-    for (auto& t : pool) t.join();
-  }
+  helpers().run(static_cast<int>(want), work);
   return status.load();
 }
 

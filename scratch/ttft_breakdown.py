@@ -23,6 +23,11 @@ def wrap(obj, name, key=None):
     setattr(obj, name, w)
 wrap(eng.scheduler, "schedule_step"); wrap(eng, "_seq_inputs"); wrap(model, "pack"); wrap(model, "stage")
 wrap(model, "launch"); wrap(model, "run_packed"); wrap(eng.pool, "find_cached_prefix"); wrap(eng.scheduler, "_prehash")
+import paper_2512_17910_b200.scheduler as SCH
+_hr = SCH.hash_requests
+def _hr_w(*a, **k):
+    t = time.perf_counter(); r = _hr(*a, **k); tm["hash_requests"] = tm.get("hash_requests", 0) + time.perf_counter() - t; return r
+SCH.hash_requests = _hr_w
 rows = []
 for i in range(8):
     sp = P.PipelineSpec(**{**spec.__dict__, "seed": i})

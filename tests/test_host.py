@@ -79,7 +79,20 @@ def test_batched_chains_and_commit_digest_reuse_match_oracle():
         n_base = n if adapter is None else (0 if inv is None else min(-(-n_tok // B), inv // B))
         items.append((toks, n, n_base, adapter or ""))
         want.append(b"".join(P.hash_chain(toks, n, B, keys)))
+    # requests sharing their base-key region (one conversation, several adapters) share its digests
+    conv = rng.integers(0, 2**32, 200, dtype=np.uint64).astype(np.int64)
+    for k, (tail, adapter, inv) in enumerate(((7, "act", 200), (9, "act2", 200), (7, "act", 193), (5, None, None),
+                                              (12, "std", None), (7, "act", 200))):
+        toks = np.concatenate([conv, rng.integers(0, 2**32, tail, dtype=np.uint64).astype(np.int64)])
+        if k == 5:
+            toks[3] += 1  # same n_base, different base tokens
+        keys = P.compute_block_keys(toks, B, adapter_id=adapter if adapter != "std" else "std", inv_start=inv)
+        n = max(0, (len(toks) - 1) // B)
+        n_base = n if adapter is None else (0 if inv is None else min(-(-len(toks) // B), inv // B))
+        items.append((toks, n, n_base, adapter or ""))
+        want.append(b"".join(P.hash_chain(toks, n, B, keys)))
     assert K.hash_requests(items, B, n_threads=3) == want
+    assert K.hash_requests(items, B, n_threads=1) == want
     with pytest.raises(ValueError):
         K.hash_requests([(np.array([-1] * 32), 2, 2, "")], B)
     # commit_and_free reuses the admission chain for the unchanged prefix and hashes the rest
