@@ -457,14 +457,15 @@ __device__ __forceinline__ unsigned long long gtimer() {
     if (a.trace) a.trace[((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 6 + (slot)] = gtimer(); \
   } while (0)
 
-// K/V ring depth. The ring cycle of a stage is TMA latency + S MMA + softmax + PV (~2-3 us under load), so
-// the per-tile period is that over kNS; D=64 keeps the CTA at ~98 KB of smem (4 stages, one P buffer) so
-// two CTAs (two independent softmax chains) share an SM.
+// K/V ring depth. A stage is held from its TMA issue until PV of its tile completes (TMA latency + S MMA +
+// softmax + PV, ~2-3 us under load), so the per-tile period is that cycle over kNS. P lives in TMEM (written
+// over the S columns it came from), which leaves the smem to K/V: 5 stages at ~97 KB per CTA for D=64, so
+// two CTAs (two independent softmax chains) still share an SM.
 template <int D>
-constexpr int kNS = 3;
-// S runs two tiles ahead of the softmax (three S buffers in TMEM) and P is double-buffered in smem, so
-// neither the softmax nor the MMA warp waits on the other's previous step (the per-tile chain was the
-// bound: S MMA -> commit -> softmax -> P -> PV -> commit, ~1 us per 64-key tile with one buffer each).
+constexpr int kNS = 5;
+// S runs two tiles ahead of the softmax (three S buffers in TMEM). P_t overwrites the first 32 columns of
+// its S buffer, which the MMA warp reuses for S_{t+3} only after issuing PV_t (tcgen05.mma from one thread
+// execute in issue order), so neither warp waits on the other's previous step.
 constexpr int kSBuf = 3;
 constexpr int kThreads = 192;   // 4 softmax + 1 producer + 1 MMA warps
 constexpr float kRescaleLog2 = 8.f;
@@ -473,12 +474,10 @@ template <int D>
 struct Smem {
   static constexpr int kQBytes = kQT * D * 2;        // [D/64][128][64]
   static constexpr int kKVBytes = kKT * D * 2;       // one K (or V) tile [D/64][64][64]
-  static constexpr int kPBytes = kQT * kKT * 2;      // [128][64]
   static constexpr int kQ = 0;
   static constexpr int kK = kQ + kQBytes;
   static constexpr int kV = kK + kNS<D> * kKVBytes;
-  static constexpr int kP = kV + kNS<D> * kKVBytes;
-  static constexpr int kBar = kP + 2 * kPBytes;  // two P buffers
+  static constexpr int kBar = kV + kNS<D> * kKVBytes;
   static constexpr int kTotal = kBar + 256 + 1024;  // barriers + TMEM slot + alignment slack
 };
 
@@ -643,13 +642,12 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
         if (ready) {
           sm100::tc_fence_after();
           if (sm100::elect_one()) {
-            const uint8_t* pb = sm + L::kP + (tp & 1) * L::kPBytes;
+            const uint32_t tp_a = tS[tp % kSBuf];  // P_tp: bf16 pairs in the first 32 columns of its S buffer
             const uint8_t* vb = sm + L::kV + (tp % kNS<D>) * L::kKVBytes;
 #pragma unroll
-            for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys
-              const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
+            for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys, 16 per step = 8 TMEM columns
               const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
-              sm100::mma_bf16_ss(tO, da, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
+              sm100::mma_bf16_ts(tO, tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
             }
             sm100::mma_commit(&pv_done[tp & 1]);
             sm100::mma_commit(&kv_empty[tp % kNS<D>]);
@@ -732,22 +730,20 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       if (grow) m_run = m_new;
       const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
       float rs4[4] = {0.f, 0.f, 0.f, 0.f};
-      if (t >= 2) sm100::mbar_wait(&pv_done[t & 1], ((t - 2) >> 1) & 1);  // P buffer t&1 was read by PV_{t-2}
-      uint8_t* pb = sm + L::kP + (t & 1) * L::kPBytes;
 #pragma unroll
-      for (int c = 0; c < 8; ++c) {  // 8 keys -> one 16-byte swizzled chunk at a time (few live registers)
-        uint32_t pk[4];
+      for (int h = 0; h < 2; ++h) {  // P as bf16 pairs (key 2j in the low half of column j), 16 columns at a time
+        uint32_t pk[16];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float p0 = fast_exp2(fmaf(sv[c * 8 + 2 * e], sc, nb));
-          const float p1 = fast_exp2(fmaf(sv[c * 8 + 2 * e + 1], sc, nb));
-          rs4[e] += p0 + p1;
-          pk[e] = pack_bf16(p0, p1);
+        for (int j = 0; j < 16; ++j) {
+          const float p0 = fast_exp2(fmaf(sv[h * 32 + 2 * j], sc, nb));
+          const float p1 = fast_exp2(fmaf(sv[h * 32 + 2 * j + 1], sc, nb));
+          rs4[j & 3] += p0 + p1;
+          pk[j] = pack_bf16(p0, p1);
         }
-        *reinterpret_cast<int4*>(pb + sw_off(r, c, kQT)) = make_int4((int)pk[0], (int)pk[1], (int)pk[2], (int)pk[3]);
+        sm100::tmem_st_32x32b_x16(tS[t % kSBuf] + lane_base + h * 16, pk);
       }
+      sm100::tmem_st_wait();
       l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-      sm100::fence_proxy_async_smem();
       sm100::tc_fence_before();
       sm100::mbar_arrive(&p_full[t & 1]);
     }
