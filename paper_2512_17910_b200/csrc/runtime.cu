@@ -87,8 +87,18 @@ struct Launcher {
   Model& m;
   cudaStream_t st;
   int n = 0;
+  // Debug only (timing attribution): ALORA_SKIP="attention,gemm_o" drops those launches (results are wrong).
+  static bool skipped(const char* kind) {
+    static const char* env = getenv("ALORA_SKIP");
+    if (!env) return false;
+    const size_t n = strlen(kind);
+    for (const char* p = strstr(env, kind); p; p = strstr(p + 1, kind))
+      if ((p == env || p[-1] == ',') && (p[n] == ',' || p[n] == 0)) return true;
+    return false;
+  }
   template <typename F>
   int operator()(const char* kind, double bytes, double flops, F&& fn) {
+    if (skipped(kind)) return ALORA_OK;
     int e0 = m.prof.on ? m.prof.event(st) : -1;
     const int rc = fn();
     if (rc != ALORA_OK) return rc;
