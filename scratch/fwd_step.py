@@ -18,7 +18,8 @@ reps = int(sys.argv[4]) if len(sys.argv) > 4 else 5
 C2 = dict(arch="llama", n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64, d_model=2048, ffn_dim=8192,
           vocab_size=128256, max_seq_len=4096, seed=0)
 cfg = P.ModelConfig(**C2, dtype="bf16")
-model = P.Model(cfg, init="device", max_tokens=8192, max_seqs=64)
+import os
+model = P.Model(cfg, init="device", max_tokens=8192, max_seqs=64, graphs=os.environ.get("ALORA_GRAPHS", "1") != "0")
 B = 16
 nb = -(-(cached + suffix) // B)
 pool = P.BlockPool(n_req * nb + 8, B, cfg.n_layers, cfg.d_model, kv_width=cfg.kv_width, dtype="bf16")
