@@ -28,6 +28,11 @@ _hr = SCH.hash_requests
 def _hr_w(*a, **k):
     t = time.perf_counter(); r = _hr(*a, **k); tm["hash_requests"] = tm.get("hash_requests", 0) + time.perf_counter() - t; return r
 SCH.hash_requests = _hr_w
+import gc, os
+if os.environ.get("GC_MODE") == "off":
+    gc.disable()
+elif os.environ.get("GC_MODE") == "freeze":
+    gc.collect(); gc.freeze()
 rows = []
 for i in range(8):
     sp = P.PipelineSpec(**{**spec.__dict__, "seed": i})
