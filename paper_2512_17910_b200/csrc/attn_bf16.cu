@@ -797,6 +797,269 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
 
 }  // namespace tc
 
+// ============================================================================================================
+// Decode attention (every sequence of the step has ONE query row): G = H/Hkv query heads share a kv head, so
+// a work item is G rows -- far below a 128-row tcgen05 tile (4 live rows of 128 at G=4, one live softmax
+// warp whose per-tile chain bounded the tcgen05 kernel at ~20 us per layer for 12 x 2k contexts). Here:
+//   the keys are split into more partitions (~3 CTAs per SM); each of the 4 warps of a CTA owns every 4th
+//   32-key chunk of the partition and its own 2-stage smem ring filled by TMA page boxes [B keys x 64 dims]
+//   (SW128-swizzled, as in the tcgen05 kernel), so warps never synchronise until the end;
+//   S = Q K^T and O += P V run as warp-level mma.sync m16n8k16 (rows = the G heads, zero-padded to 16;
+//   K/V fragments by ldmatrix from the swizzled chunk), P stays in registers (S accumulator -> A fragment);
+//   online softmax per head in fp32 with exp2, scale applied to the fp32 scores.
+// Warp-level MMA is the right unit here: 16-row fragments waste 12 of 16 rows instead of 124 of 128, and the
+// kernel is bound by HBM and per-chunk latency, not by tensor throughput.
+// ============================================================================================================
+constexpr int kDecWarps = 4;
+constexpr int kDecMaxG = 8;
+constexpr int kDecNS = 2;     // ring stages per warp
+constexpr int kDecKeys = 32;  // keys per chunk (one per lane)
+
+template <int D>
+struct DecSmem {
+  static constexpr int kTile = kDecKeys * D * 2;           // one K (or V) chunk: [D/64][32][64] bf16
+  static constexpr int kStage = 2 * kTile;                 // K | V
+  static constexpr int kWarp = kDecNS * kStage;
+  static constexpr int kRing = kDecWarps * kWarp;
+  static constexpr int kTotal = kRing + 1024 + 256;        // + alignment slack + barriers
+};
+
+template <int D, int G>
+__global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnArgs a,
+                                                                   const __grid_constant__ CUtensorMap tm_kv) {
+  using L = DecSmem<D>;
+  constexpr int DL = D / 32;  // dims per lane in the PV accumulation (2 for D=64)
+  extern __shared__ uint8_t smem_dec_raw[];
+  uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dec_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring + L::kRing);  // [warps][NS]
+  __shared__ float sm_m[kDecWarps][G], sm_l[kDecWarps][G];
+  __shared__ float so[kDecWarps][G][D];
+  __shared__ int s_last;
+  const int s = blockIdx.z / a.Hkv, kvh = blockIdx.z % a.Hkv;
+  const int part = blockIdx.y;
+  const int row = a.cu_q[s];
+  const int start = a.start_pos[s];
+  const int key_begin = part * a.part_size;
+  const int key_end = min(start + 1, key_begin + a.part_size);
+  if (key_begin >= key_end) return;
+  const int parts_here = min(a.n_parts, (start + a.part_size) / a.part_size);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int32_t* bt = a.block_table + (int64_t)s * a.max_blocks;
+  const int last_blk = (key_end - 1) / a.B;
+  const int per_chunk = kDecKeys / a.B;  // pages per chunk (B divides 32)
+  const int n_chunks = (key_end - key_begin + kDecKeys - 1) / kDecKeys;
+  uint8_t* wring = ring + warp * L::kWarp;
+  uint64_t* wfull = full + warp * kDecNS;
+  if (lane == 0) {
+    sm100::prefetch_tmap(&tm_kv);
+    for (int i = 0; i < kDecNS; ++i) sm100::mbar_init(&wfull[i], 1);
+    sm100::fence_barrier_init();
+  }
+  __syncwarp();
+  const uint64_t pol = sm100::policy_evict_first();
+  auto issue = [&](int c, int st) {  // chunk c (partition-relative) of this warp into stage st
+    uint8_t* dk = wring + st * L::kStage;
+    uint8_t* dv = dk + L::kTile;
+    sm100::mbar_arrive_expect_tx(&wfull[st], L::kStage);
+    const int b0 = (key_begin + c * kDecKeys) / a.B;
+    for (int j = 0; j < per_chunk; ++j) {
+      const int64_t blk = bt[min(b0 + j, last_blk)];  // past the end: a valid duplicate, masked below
+      const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+#pragma unroll
+      for (int sub = 0; sub < D / 64; ++sub) {
+        sm100::tma_load_2d(dk + sub * kDecKeys * 128 + j * a.B * 128, &tm_kv, &wfull[st], kvh * D + sub * 64, rowk, pol);
+        sm100::tma_load_2d(dv + sub * kDecKeys * 128 + j * a.B * 128, &tm_kv, &wfull[st], kvh * D + sub * 64,
+                           rowk + a.B, pol);
+      }
+    }
+  };
+  // chunks of this warp: c = warp, warp + 4, ...; the cached prefix streams in before the dependency wait
+  // (only the step's last key -- the row being decoded -- is written by the kernel before this one)
+  const int cached_end = (start / a.B) * a.B;
+  int issued = 0;
+  if (lane == 0)
+    for (int c = warp; issued < kDecNS && c < n_chunks; c += kDecWarps, ++issued) {
+      if (key_begin + (c + 1) * kDecKeys > cached_end) break;
+      issue(c, issued);
+    }
+  issued = __shfl_sync(0xffffffffu, issued, 0);
+  pdl_wait();  // q and this step's K/V row come from the kernels before
+  pdl_trigger();
+  if (lane == 0)
+    for (int k = issued, c = warp + issued * kDecWarps; k < kDecNS && c < n_chunks; ++k, c += kDecWarps) issue(c, k);
+  // Q as mma.sync A fragments: row = lane/4 is query head g (rows >= G and the upper 8 rows are zero)
+  const int qg = lane >> 2, qt4 = lane & 3;
+  uint32_t qf[D / 16][4];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+    const uint32_t* qr = reinterpret_cast<const uint32_t*>(a.q + (int64_t)row * a.ld_q + (kvh * G + qg) * D + kk * 16);
+    qf[kk][0] = qg < G ? qr[qt4] : 0u;
+    qf[kk][1] = 0u;
+    qf[kk][2] = qg < G ? qr[4 + qt4] : 0u;
+    qf[kk][3] = 0u;
+  }
+  // swizzled element offset of (row, 16-byte unit u) in a [D/64][32][64] chunk tile (TMA SW128 boxes)
+  auto sw = [](int r, int u) { return (u >> 3) * kDecKeys * 64 + r * 64 + (((u & 7) ^ (r & 7)) << 3); };
+  int koff[2][D / 16], voff[D / 16];
+#pragma unroll
+  for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+    for (int jn = 0; jn < 2; ++jn)
+      koff[jn][kk] = sw(jn * 16 + (lane & 7) + (lane >> 4) * 8, kk * 2 + ((lane >> 3) & 1));
+    voff[kk] = sw(lane & 15, kk * 2 + (lane >> 4)) - (lane & 15) * 64;  // + row term added per key block
+  }
+  const float scl = a.scale_log2;
+  float m_run = -INFINITY, l_run = 0.f;  // row qg
+  float o[D / 8][4];
+#pragma unroll
+  for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
+  int it = 0;
+  for (int c = warp; c < n_chunks; c += kDecWarps, ++it) {
+    const int st = it % kDecNS;
+    sm100::mbar_wait(&wfull[st], (it / kDecNS) & 1);
+    const __nv_bfloat16* sk = reinterpret_cast<const __nv_bfloat16*>(wring + st * L::kStage);
+    const __nv_bfloat16* sv = sk + kDecKeys * D;
+    const int c0 = key_begin + c * kDecKeys;
+    float sc4[4][4];  // S = Q K^T: 16 rows x 32 keys (n-tiles of 8 keys)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) sc4[j][0] = sc4[j][1] = sc4[j][2] = sc4[j][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < D / 16; ++kk) {
+#pragma unroll
+      for (int jn = 0; jn < 2; ++jn) {
+        uint32_t bfr[4];
+        ldsm_x4(bfr, sk + koff[jn][kk]);
+        mma16816(sc4[2 * jn], qf[kk], bfr[0], bfr[1]);
+        mma16816(sc4[2 * jn + 1], qf[kk], bfr[2], bfr[3]);
+      }
+    }
+    float mx = -INFINITY;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        float v = sc4[j][e] * scl;
+        if (c0 + j * 8 + 2 * qt4 + e >= key_end) v = -INFINITY;
+        sc4[j][e] = v;
+        mx = fmaxf(mx, v);
+      }
+    }
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+    const float m_new = fmaxf(m_run, mx);  // finite: every chunk holds at least one valid key
+    const float corr = fast_exp2(m_run - m_new);
+    m_run = m_new;
+    float rs = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      sc4[j][0] = fast_exp2(sc4[j][0] - m_new);
+      sc4[j][1] = fast_exp2(sc4[j][1] - m_new);
+      rs += sc4[j][0] + sc4[j][1];
+    }
+    l_run = l_run * corr + rs;
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) { o[j][0] *= corr; o[j][1] *= corr; }
+    // O += P V (P from the S accumulators; the dead upper 8 rows stay zero)
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      uint32_t pa[4];
+      pa[0] = pack_bf16(sc4[2 * kk][0], sc4[2 * kk][1]);
+      pa[1] = 0u;
+      pa[2] = pack_bf16(sc4[2 * kk + 1][0], sc4[2 * kk + 1][1]);
+      pa[3] = 0u;
+#pragma unroll
+      for (int jd = 0; jd < D / 16; ++jd) {
+        uint32_t bfr[4];
+        ldsm_x4_t(bfr, sv + (kk * 16 + (lane & 15)) * 64 + voff[jd]);
+        mma16816(o[2 * jd], pa, bfr[0], bfr[1]);
+        mma16816(o[2 * jd + 1], pa, bfr[2], bfr[3]);
+      }
+    }
+    // this stage is consumed: refill it with chunk c + NS*4 (generic reads -> async-proxy writes)
+    __syncwarp();
+    if (lane == 0 && c + kDecNS * kDecWarps < n_chunks) {
+      sm100::fence_proxy_async_smem();
+      issue(c + kDecNS * kDecWarps, st);
+    }
+    __syncwarp();
+  }
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 1);
+  l_run += __shfl_xor_sync(0xffffffffu, l_run, 2);
+  if (qg < G) {
+    if (qt4 == 0) {
+      sm_m[warp][qg] = m_run;
+      sm_l[warp][qg] = l_run;
+    }
+#pragma unroll
+    for (int j = 0; j < D / 8; ++j) {
+      so[warp][qg][j * 8 + 2 * qt4] = o[j][0];
+      so[warp][qg][j * 8 + 2 * qt4 + 1] = o[j][1];
+    }
+  }
+  __syncthreads();
+  for (int i = tid; i < G * D; i += blockDim.x) {
+    const int g = i / D, d = i % D;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) mx = fmaxf(mx, sm_m[w][g]);
+    float l = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < kDecWarps; ++w) {
+      const float f = sm_m[w][g] == -INFINITY ? 0.f : fast_exp2(sm_m[w][g] - mx);
+      l += f * sm_l[w][g];
+      acc += f * so[w][g][d];
+    }
+    const int head = kvh * G + g;
+    if (parts_here == 1) {
+      a.out[(int64_t)row * a.ld_out + head * D + d] = __float2bfloat16_rn(l > 0.f ? acc / l : 0.f);
+    } else {
+      const int64_t slot = ((int64_t)part * a.M + row) * a.H + head;
+      __stcg(a.ws_o + slot * D + d, acc);
+      if (d == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(mx, l));
+    }
+  }
+  if (parts_here > 1) merge_partials<D>(a, s, kvh, 0, row, start, G, parts_here, G, &s_last);
+}
+
+template <int D, int G>
+int launch_decode_g(const AttnArgs& a, dim3 grid, const CUtensorMap& tm, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DecSmem<D>::kTotal) != cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  ALORA_CUDA_CHECK(launch_pdl(attn_decode_kernel<D, G>, grid, dim3(32 * kDecWarps), DecSmem<D>::kTotal, st, nullptr,
+                              0, a, tm));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+template <int D>
+int launch_decode(const AttnArgs& a, dim3 grid, int G, int64_t kv_rows, cudaStream_t st) {
+  CUtensorMap tm{};
+  if (!make_tmap_2d(&tm, a.kv, (uint64_t)kv_rows, (uint64_t)a.Hkv * D, (uint64_t)a.Hkv * D, a.B, 64))
+    return ALORA_ECUDA;
+  switch (G) {
+    case 1: return launch_decode_g<D, 1>(a, grid, tm, st);
+    case 2: return launch_decode_g<D, 2>(a, grid, tm, st);
+    case 4: return launch_decode_g<D, 4>(a, grid, tm, st);
+    case 8: return launch_decode_g<D, 8>(a, grid, tm, st);
+    default: return ALORA_EINVAL;
+  }
+}
+
+// Decode partition plan: ~4 resident CTAs per SM, >= 128 keys per partition, <= kMaxParts.
+void plan_decode(int n_seqs, int max_ctx, int Hkv, int& part_size, int& n_parts) {
+  const int units = std::max(1, n_seqs * Hkv);
+  int np = std::max(1, std::min({kMaxParts, (3 * kNumSMs) / units, (max_ctx + kMinPartKeys - 1) / kMinPartKeys}));
+  int ps = (max_ctx + np - 1) / np;
+  ps = (ps + 31) / 32 * 32;
+  n_parts = (max_ctx + ps - 1) / ps;
+  part_size = ps;
+}
+
 // Partition plan shared by the workspace query and the launch. When the step has fewer work items than
 // resident CTA slots (aLoRA suffix turns, decode) the keys are split so that all partitions run in ONE wave:
 // a second wave would double the per-CTA fixed cost (setup, Q load, merge) on the critical path.
@@ -897,6 +1160,11 @@ int64_t attn_bf16_workspace_bound(int H, int D) {
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D) {
   int ps, np, nq;
   plan(n_seqs, max_q, max_ctx, H, Hkv, D, ps, np, nq);
+  if (max_q == 1 && H / Hkv <= kDecMaxG) {
+    int dps, dnp;
+    plan_decode(n_seqs, max_ctx, Hkv, dps, dnp);
+    np = std::max(np, dnp);
+  }
   if (np <= 1) return 0;
   return (int64_t)np * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
 }
@@ -912,7 +1180,23 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
   a.max_blocks = max_blocks; a.kv = kv; a.n_layers = n_layers; a.layer = layer; a.B = B; a.H = H; a.Hkv = Hkv;
   a.D = D; a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
   a.out = out; a.ld_out = ld_out; a.M = M;
-  plan(n_seqs, max_q, max_ctx, H, Hkv, D, a.part_size, a.n_parts, a.n_qtiles);
+  static const bool no_dec = getenv("ALORA_ATTN_NO_DECODE") != nullptr;  // A/B switch
+  const int Gq = H / Hkv;
+  const int64_t kv_rows_all = (int64_t)total_blocks * n_layers * 2 * B;
+  const bool decode = !no_dec && max_q == 1 && (Gq == 1 || Gq == 2 || Gq == 4 || Gq == 8) && total_blocks > 0 &&
+                      B <= kDecKeys && kDecKeys % B == 0 && kv_rows_all < (1ll << 31);
+  if (decode) {
+    plan_decode(n_seqs, max_ctx, Hkv, a.part_size, a.n_parts);
+    a.n_qtiles = 1;
+    // fewer partitions when the caller's workspace cannot hold them (it is sized by attn_bf16_workspace_bound)
+    while (a.n_parts > 1 && (ws == nullptr || ws_bytes < (int64_t)a.n_parts * M * H * (D + 2) * 4 +
+                                                             (int64_t)kMaxCounters * 4)) {
+      a.part_size = ((max_ctx + a.n_parts - 2) / (a.n_parts - 1) + 31) / 32 * 32;
+      a.n_parts = (max_ctx + a.part_size - 1) / a.part_size;
+    }
+  } else {
+    plan(n_seqs, max_q, max_ctx, H, Hkv, D, a.part_size, a.n_parts, a.n_qtiles);
+  }
   if (a.n_parts > 1) {
     const int64_t need = (int64_t)a.n_parts * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;
     if (ws == nullptr || ws_bytes < need) return ALORA_EINVAL;
@@ -920,6 +1204,10 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
     a.counters = reinterpret_cast<int*>(static_cast<char*>(ws) + ws_bytes - (int64_t)kMaxCounters * 4);
     a.ws_o = static_cast<float*>(ws);
     a.ws_ml = a.ws_o + (int64_t)a.n_parts * M * H * D;
+  }
+  if (decode) {
+    const dim3 grid(1, a.n_parts, n_seqs * Hkv);
+    return D == 64 ? launch_decode<64>(a, grid, Gq, kv_rows_all, st) : launch_decode<128>(a, grid, Gq, kv_rows_all, st);
   }
   const int64_t kv_rows = (int64_t)total_blocks * n_layers * 2 * B;
   return D == 64 ? launch_attn<64>(a, n_seqs, kv_rows, st) : launch_attn<128>(a, n_seqs, kv_rows, st);

@@ -56,6 +56,14 @@ def _attn_case(n_seqs, H, Hkv, D, B, starts, lens, seed):
     (8, 8, 128, 16, [100, 0, 517], [33, 1, 64]),    # MHA, D=128, mixed batch
     (8, 2, 64, 5, [13, 300], [40, 3]),              # odd block size
     (32, 8, 64, 16, [0, 0, 0, 0], [300, 257, 1, 64]),
+    # decode steps (one query row per sequence): the split-KV decode kernel, every GQA group size it serves
+    (32, 8, 64, 16, [2047, 5, 0, 130, 31, 32, 33], [1] * 7),
+    (8, 8, 128, 16, [1000, 77], [1, 1]),             # G=1, D=128
+    (16, 2, 64, 16, [511, 3], [1, 1]),               # G=8
+    (8, 4, 64, 8, [300, 64, 7], [1, 1, 1]),          # G=2, B=8
+    (32, 8, 64, 32, [4000, 100], [1, 1]),            # B=32: one page per 32-key chunk
+    (32, 8, 64, 16, list(range(0, 1200, 50)), [1] * 24),   # many sequences: few partitions each
+    (8, 2, 64, 5, [300, 12], [1, 1]),                # B=5: not a divisor of 32 -> tensor-core kernel
 ])
 def test_paged_attention_bf16_vs_dense(H, Hkv, D, B, starts, lens):
     n = len(starts)
