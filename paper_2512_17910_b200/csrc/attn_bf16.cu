@@ -1131,10 +1131,16 @@ int launch_attn(const AttnArgs& a, int n_seqs, int64_t kv_rows, cudaStream_t st)
         for (int p = 0; p < 5; ++p)
           if (h[6 * c + p + 1] && h[6 * c + p]) ph[p] += double(h[6 * c + p + 1] - h[6 * c + p]);
       }
-      fprintf(stderr, "[attn trace] ctas %d/%d span %.2f us; mean start->Q %.2f, Q->S0 %.2f, S0->last P %.2f, "
-              "->epilogue %.2f, merge %.2f us (parts %d, part keys %d)\n", live, n_ctas, (t1 - t0) / 1e3,
-              ph[0] / live / 1e3, ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3, ph[4] / live / 1e3,
-              a.n_parts, a.part_size);
+      unsigned long long last_start = 0, max_dur = 0;
+      for (int c = 0; c < n_ctas; ++c) {
+        if (!h[6 * c] || !h[6 * c + 5]) continue;
+        last_start = std::max(last_start, h[6 * c] - t0);
+        max_dur = std::max(max_dur, h[6 * c + 5] - h[6 * c]);
+      }
+      fprintf(stderr, "[attn trace] ctas %d/%d span %.2f us (last CTA start +%.2f, longest CTA %.2f); mean start->Q "
+              "%.2f, Q->S0 %.2f, S0->last P %.2f, ->epilogue %.2f, merge %.2f us (parts %d, part keys %d)\n", live,
+              n_ctas, (t1 - t0) / 1e3, last_start / 1e3, max_dur / 1e3, ph[0] / live / 1e3, ph[1] / live / 1e3,
+              ph[2] / live / 1e3, ph[3] / live / 1e3, ph[4] / live / 1e3, a.n_parts, a.part_size);
     }
   }
   ALORA_LAUNCH_CHECK();
