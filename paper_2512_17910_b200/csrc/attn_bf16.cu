@@ -553,31 +553,44 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     // KV streams through L2 with evict_first: keeping it (evict_last) pushed the next kernels' weights and
     // split-K partials out of L2 and cost ~3.5% of the forward (measured A/B)
     const uint64_t pol = sm100::policy_evict_first();
-    auto issue_kv = [&](int t) {  // K/V tile t: TMA boxes of [B keys x 64 dims], page by page via the block table
+    // Block-table window: lane i holds the page id of page w0 + i, refilled with one coalesced load when a
+    // tile needs a page past it (a dependent L2 load per page serialised the issue loop: ~4 us before Q).
+    int w0 = -(1 << 30);
+    int32_t win = 0;
+    auto issue_kv = [&](int t) {  // warp-wide. K/V tile t: TMA boxes of [B keys x 64 dims], page by page
       const int st = t % kNS<D>;
-      sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
+      if (sm100::elect_one()) sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
       uint8_t* dk = sm + L::kK + st * L::kKVBytes;
       uint8_t* dv = sm + L::kV + st * L::kKVBytes;
       const int b0 = (key_begin + t * kKT) / a.B;
       for (int j = 0; j < per_tile; ++j) {
-        const int64_t blk = bt[min(b0 + j, last_blk)];  // past the end: a valid duplicate, masked later
-        const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
-#pragma unroll
-        for (int sub = 0; sub < D / 64; ++sub) {
-          sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk, pol);
-          sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
-                             rowk + a.B, pol);
+        const int idx = min(b0 + j, last_blk);  // past the end: a valid duplicate, masked later
+        if (idx >= w0 + 32) {
+          w0 = idx;
+          win = bt[min(w0 + lane, last_blk)];
         }
+        const int64_t blk = __shfl_sync(0xffffffffu, win, idx - w0);
+        const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int sub = 0; sub < D / 64; ++sub) {
+            sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk,
+                               pol);
+            sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
+                               rowk + a.B, pol);
+          }
+        }
+        __syncwarp();
       }
     };
     // Tiles made only of pages wholly before this sequence's start position hold cached KV that no kernel of
     // this step writes: they stream in before the dependency wait, overlapping the kernels before.
     const int cached_end = (start / a.B) * a.B;
     int t = 0;
-    for (; t < min(n_tiles, kNS<D>); ++t) {
+    static constexpr int kPreTiles = 2;  // before Q: each tile is 2 * 64/B TMA issues, which delay the Q gather
+    for (; t < min(n_tiles, kPreTiles); ++t) {
       if (key_begin + (t + 1) * kKT > cached_end) break;
-      if (sm100::elect_one()) issue_kv(t);
-      __syncwarp();
+      issue_kv(t);
     }
     pdl_wait();  // q and this step's fresh K/V rows come from the kernels before
     pdl_trigger();
@@ -596,8 +609,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     for (; t < n_tiles; ++t) {
       const int st = t % kNS<D>;
       if (t >= kNS<D>) sm100::mbar_wait(&kv_empty[st], ((t / kNS<D>) - 1) & 1);
-      if (sm100::elect_one()) issue_kv(t);
-      __syncwarp();
+      issue_kv(t);
     }
   } else if (warp == 5) {
     // ------------------------------------------------------------------ MMA issuer
@@ -1082,6 +1094,7 @@ template <int D>
 int launch_attn(const AttnArgs& a, int n_seqs, int64_t kv_rows, cudaStream_t st) {
   dim3 grid(a.n_qtiles, a.n_parts, n_seqs * a.Hkv);
   static const bool force_mma = getenv("ALORA_ATTN_MMA") != nullptr;  // A/B switch to the mma.sync kernel
+  // the tcgen05 kernel loads pages with TMA boxes of [B x 64]: B must tile the 64-key KV tile
   // the tcgen05 kernel loads pages with TMA boxes of [B x 64]: B must tile the 64-key KV tile
   const bool use_tc = !force_mma && a.B <= kKT && kKT % a.B == 0 && kv_rows > 0 && kv_rows < (1ll << 31);
   CUtensorMap tm{};

@@ -56,6 +56,9 @@ def _attn_case(n_seqs, H, Hkv, D, B, starts, lens, seed):
     (8, 8, 128, 16, [100, 0, 517], [33, 1, 64]),    # MHA, D=128, mixed batch
     (8, 2, 64, 5, [13, 300], [40, 3]),              # odd block size
     (32, 8, 64, 16, [0, 0, 0, 0], [300, 257, 1, 64]),
+    (32, 8, 64, 32, [100, 0, 1500], [40, 70, 9]),    # B=32: two pages per 64-key tile
+    (8, 8, 128, 64, [300, 0], [20, 90]),             # B=64: one page per tile, D=128
+    (8, 2, 64, 8, [40, 0], [30, 17]),                # B=8: eight pages per 64-key tile
     # decode steps (one query row per sequence): the split-KV decode kernel, every GQA group size it serves
     (32, 8, 64, 16, [2047, 5, 0, 130, 31, 32, 33], [1] * 7),
     (8, 8, 128, 16, [1000, 77], [1, 1]),             # G=1, D=128
