@@ -29,6 +29,17 @@ def _hr_w(*a, **k):
     t = time.perf_counter(); r = _hr(*a, **k); tm["hash_requests"] = tm.get("hash_requests", 0) + time.perf_counter() - t; return r
 SCH.hash_requests = _hr_w
 import gc, os
+from paper_2512_17910_b200 import _native as _N
+_fn = _N.lib.alora_hash_requests
+class _W:
+    def __call__(self, *a):
+        t = time.perf_counter(); r = _fn(*a); tm["ctypes_hash"] = tm.get("ctypes_hash", 0) + time.perf_counter() - t; return r
+_N.lib.alora_hash_requests = _W()
+_fl = _N.lib.alora_pool_lookup
+class _W2:
+    def __call__(self, *a):
+        t = time.perf_counter(); r = _fl(*a); tm["ctypes_lookup"] = tm.get("ctypes_lookup", 0) + time.perf_counter() - t; return r
+_N.lib.alora_pool_lookup = _W2()
 if os.environ.get("GC_MODE") == "off":
     gc.disable()
 elif os.environ.get("GC_MODE") == "freeze":
