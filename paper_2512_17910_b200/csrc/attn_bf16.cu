@@ -499,7 +499,8 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   uint64_t* s_full = kv_empty + kNS<D>;   // kSBuf
   uint64_t* p_full = s_full + kSBuf;   // 2
   uint64_t* pv_done = p_full + 2;      // 2
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pv_done + 2);
+  uint64_t* s_free = pv_done + 2;      // kSBuf: PV of the P held in S buffer i has completed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + kSBuf);
   __shared__ int s_last;
 
   const int G = a.H / a.Hkv;
@@ -528,7 +529,10 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::mbar_init(&kv_full[i], 1);
       sm100::mbar_init(&kv_empty[i], 1);
     }
-    for (int i = 0; i < kSBuf; ++i) sm100::mbar_init(&s_full[i], 1);
+    for (int i = 0; i < kSBuf; ++i) {
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&s_free[i], 1);
+    }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&p_full[i], 32 * live_warps);
       sm100::mbar_init(&pv_done[i], 1);
@@ -627,7 +631,12 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       if (ts < n_tiles && ts <= tp + 2) {
         const int st = ts % kNS<D>;
         uint32_t ready = 0;
-        if (lane == 0) ready = sm100::mbar_test(&kv_full[st], (ts / kNS<D>) & 1) ? 1u : 0u;
+        // S_ts overwrites the TMEM columns PV_{ts-3} reads its P from: wait for that PV to COMPLETE (issue
+        // order alone does not order a later MMA's accumulator writes after an earlier MMA's operand reads)
+        if (lane == 0)
+          ready = sm100::mbar_test(&kv_full[st], (ts / kNS<D>) & 1) &&
+                          (ts < kSBuf || sm100::mbar_test(&s_free[ts % kSBuf], ((ts / kSBuf) - 1) & 1))
+                      ? 1u : 0u;
         ready = __shfl_sync(0xffffffffu, ready, 0);
         if (ready) {
           sm100::tc_fence_after();
@@ -663,6 +672,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
             }
             sm100::mma_commit(&pv_done[tp & 1]);
             sm100::mma_commit(&kv_empty[tp % kNS<D>]);
+            sm100::mma_commit(&s_free[tp % kSBuf]);
           }
           __syncwarp();
           ++tp;
@@ -822,30 +832,31 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
 // Warp-level MMA is the right unit here: 16-row fragments waste 12 of 16 rows instead of 124 of 128, and the
 // kernel is bound by HBM and per-chunk latency, not by tensor throughput.
 // ============================================================================================================
-constexpr int kDecWarps = 4;
+constexpr int kDecWarpsSplit = 4;  // warps per CTA when the keys are split into partitions
+constexpr int kDecWarpsWhole = 8;  // warps per CTA when one CTA covers a (sequence, kv head)
 constexpr int kDecMaxG = 8;
 constexpr int kDecNS = 2;     // ring stages per warp
 constexpr int kDecKeys = 32;  // keys per chunk (one per lane)
 
-template <int D>
+template <int D, int W>
 struct DecSmem {
   static constexpr int kTile = kDecKeys * D * 2;           // one K (or V) chunk: [D/64][32][64] bf16
   static constexpr int kStage = 2 * kTile;                 // K | V
   static constexpr int kWarp = kDecNS * kStage;
-  static constexpr int kRing = kDecWarps * kWarp;
+  static constexpr int kRing = W * kWarp;
   static constexpr int kTotal = kRing + 1024 + 256;        // + alignment slack + barriers
 };
 
-template <int D, int G>
-__global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnArgs a,
+template <int D, int G, int W>
+__global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
                                                                    const __grid_constant__ CUtensorMap tm_kv) {
-  using L = DecSmem<D>;
+  using L = DecSmem<D, W>;
   constexpr int DL = D / 32;  // dims per lane in the PV accumulation (2 for D=64)
   extern __shared__ uint8_t smem_dec_raw[];
   uint8_t* ring = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_dec_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(ring + L::kRing);  // [warps][NS]
-  __shared__ float sm_m[kDecWarps][G], sm_l[kDecWarps][G];
-  __shared__ float so[kDecWarps][G][D];
+  __shared__ float sm_m[W][G], sm_l[W][G];
+  __shared__ float so[W][G][D];
   __shared__ int s_last;
   const int s = blockIdx.z / a.Hkv, kvh = blockIdx.z % a.Hkv;
   const int part = blockIdx.y;
@@ -890,7 +901,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
   const int cached_end = (start / a.B) * a.B;
   int issued = 0;
   if (lane == 0)
-    for (int c = warp; issued < kDecNS && c < n_chunks; c += kDecWarps, ++issued) {
+    for (int c = warp; issued < kDecNS && c < n_chunks; c += W, ++issued) {
       if (key_begin + (c + 1) * kDecKeys > cached_end) break;
       issue(c, issued);
     }
@@ -898,7 +909,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
   pdl_wait();  // q and this step's K/V row come from the kernels before
   pdl_trigger();
   if (lane == 0)
-    for (int k = issued, c = warp + issued * kDecWarps; k < kDecNS && c < n_chunks; ++k, c += kDecWarps) issue(c, k);
+    for (int k = issued, c = warp + issued * W; k < kDecNS && c < n_chunks; ++k, c += W) issue(c, k);
   // Q as mma.sync A fragments: row = lane/4 is query head g (rows >= G and the upper 8 rows are zero)
   const int qg = lane >> 2, qt4 = lane & 3;
   uint32_t qf[D / 16][4];
@@ -926,7 +937,7 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
 #pragma unroll
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   int it = 0;
-  for (int c = warp; c < n_chunks; c += kDecWarps, ++it) {
+  for (int c = warp; c < n_chunks; c += W, ++it) {
     const int st = it % kDecNS;
     sm100::mbar_wait(&wfull[st], (it / kDecNS) & 1);
     const __nv_bfloat16* sk = reinterpret_cast<const __nv_bfloat16*>(wring + st * L::kStage);
@@ -989,9 +1000,9 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
     }
     // this stage is consumed: refill it with chunk c + NS*4 (generic reads -> async-proxy writes)
     __syncwarp();
-    if (lane == 0 && c + kDecNS * kDecWarps < n_chunks) {
+    if (lane == 0 && c + kDecNS * W < n_chunks) {
       sm100::fence_proxy_async_smem();
-      issue(c + kDecNS * kDecWarps, st);
+      issue(c + kDecNS * W, st);
     }
     __syncwarp();
   }
@@ -1013,10 +1024,10 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
     const int g = i / D, d = i % D;
     float mx = -INFINITY;
 #pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) mx = fmaxf(mx, sm_m[w][g]);
+    for (int w = 0; w < W; ++w) mx = fmaxf(mx, sm_m[w][g]);
     float l = 0.f, acc = 0.f;
 #pragma unroll
-    for (int w = 0; w < kDecWarps; ++w) {
+    for (int w = 0; w < W; ++w) {
       const float f = sm_m[w][g] == -INFINITY ? 0.f : fast_exp2(sm_m[w][g] - mx);
       l += f * sm_l[w][g];
       acc += f * so[w][g][d];
@@ -1033,16 +1044,16 @@ __global__ void __launch_bounds__(32 * kDecWarps) attn_decode_kernel(const AttnA
   if (parts_here > 1) merge_partials<D>(a, s, kvh, 0, row, start, G, parts_here, G, &s_last);
 }
 
-template <int D, int G>
+template <int D, int G, int W>
 int launch_decode_g(const AttnArgs& a, dim3 grid, const CUtensorMap& tm, cudaStream_t st) {
   static bool configured = false;
   if (!configured) {
-    if (cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             DecSmem<D>::kTotal) != cudaSuccess)
+    if (cudaFuncSetAttribute(attn_decode_kernel<D, G, W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             DecSmem<D, W>::kTotal) != cudaSuccess)
       return ALORA_ECUDA;
     configured = true;
   }
-  ALORA_CUDA_CHECK(launch_pdl(attn_decode_kernel<D, G>, grid, dim3(32 * kDecWarps), DecSmem<D>::kTotal, st, nullptr,
+  ALORA_CUDA_CHECK(launch_pdl(attn_decode_kernel<D, G, W>, grid, dim3(32 * W), DecSmem<D, W>::kTotal, st, nullptr,
                               0, a, tm));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
@@ -1053,18 +1064,32 @@ int launch_decode(const AttnArgs& a, dim3 grid, int G, int64_t kv_rows, cudaStre
   CUtensorMap tm{};
   if (!make_tmap_2d(&tm, a.kv, (uint64_t)kv_rows, (uint64_t)a.Hkv * D, (uint64_t)a.Hkv * D, a.B, 64))
     return ALORA_ECUDA;
+  // one CTA per (sequence, kv head) with 8 warps when that alone fills most SMs (no partition merge),
+  // otherwise 4-warp CTAs over key partitions
+  const bool whole = a.n_parts == 1;
   switch (G) {
-    case 1: return launch_decode_g<D, 1>(a, grid, tm, st);
-    case 2: return launch_decode_g<D, 2>(a, grid, tm, st);
-    case 4: return launch_decode_g<D, 4>(a, grid, tm, st);
-    case 8: return launch_decode_g<D, 8>(a, grid, tm, st);
+    case 1: return whole ? launch_decode_g<D, 1, kDecWarpsWhole>(a, grid, tm, st)
+                         : launch_decode_g<D, 1, kDecWarpsSplit>(a, grid, tm, st);
+    case 2: return whole ? launch_decode_g<D, 2, kDecWarpsWhole>(a, grid, tm, st)
+                         : launch_decode_g<D, 2, kDecWarpsSplit>(a, grid, tm, st);
+    case 4: return whole ? launch_decode_g<D, 4, kDecWarpsWhole>(a, grid, tm, st)
+                         : launch_decode_g<D, 4, kDecWarpsSplit>(a, grid, tm, st);
+    case 8: return whole ? launch_decode_g<D, 8, kDecWarpsWhole>(a, grid, tm, st)
+                         : launch_decode_g<D, 8, kDecWarpsSplit>(a, grid, tm, st);
     default: return ALORA_EINVAL;
   }
 }
 
-// Decode partition plan: ~4 resident CTAs per SM, >= 128 keys per partition, <= kMaxParts.
+// Decode plan: with at least ~half an SM-count of (sequence, kv head) units, one 8-warp CTA per unit
+// covers all its keys (no partition merge); below that, 4-warp CTAs over key partitions (~3 per SM).
 void plan_decode(int n_seqs, int max_ctx, int Hkv, int& part_size, int& n_parts) {
   const int units = std::max(1, n_seqs * Hkv);
+  static const int whole_min = getenv("ALORA_DEC_WHOLE_MIN") ? atoi(getenv("ALORA_DEC_WHOLE_MIN")) : kNumSMs / 2;
+  if (units >= whole_min) {
+    n_parts = 1;
+    part_size = (max_ctx + 31) / 32 * 32;
+    return;
+  }
   int np = std::max(1, std::min({kMaxParts, (3 * kNumSMs) / units, (max_ctx + kMinPartKeys - 1) / kMinPartKeys}));
   int ps = (max_ctx + np - 1) / np;
   ps = (ps + 31) / 32 * 32;
