@@ -61,6 +61,8 @@ def parse():
                     help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k); "
                          "c3: Llama-3-8B + 8 aLoRA adapters, 64 eval requests over 8k contexts (one replica)")
     ap.add_argument("--contexts", default="4096,8192,16384,32768")
+    ap.add_argument("--sync-decode", action="store_true",
+                    help="read every decode step's ids back before launching the next (default: pipelined decode)")
     return ap.parse_args()
 
 
@@ -121,6 +123,7 @@ def c2_config(args, world):
                         "prompt tokens (cached + computed) per second of the TTFT-defining forward",
             "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
             "l2": "working set (2.5 GB weights + KV) exceeds the 126 MB L2; no flush needed",
+            "decode": "synchronous" if getattr(args, "sync_decode", False) else "pipelined (Engine pipelined_decode)",
             **{k: v for k, v in C2.items() if k != "seed"}}
 
 
@@ -214,7 +217,7 @@ def run_sweep_c4(args):
                                  adapters=(P.AdapterSpec(adapter_id="adapter0", rank=32, seed=0,
                                                          invocation_tokens=P.invocation_for(mcfg.vocab_size, 0)),),
                                  comparison_mode=mode)
-            eng = P.Engine(cfg, clock=P.WallClock(), model=model)
+            eng = P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
             ttft, e2e, comp, base_tps = [], [], [], []
             for i in range(1 + max(1, args.lora_steps)):  # first pipeline is warm-up
                 sp = P.PipelineSpec(**{**spec.__dict__, "seed": i})
@@ -273,7 +276,7 @@ def run_c3(args):
                                                           invocation_tokens=P.invocation_for(mcfg.vocab_size, k))
                                             for k in range(n_ad)),
                              comparison_mode=mode)
-        eng = P.Engine(cfg, clock=P.WallClock(), model=model)
+        eng = P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
         ph = P.pipeline.pipeline_phases(spec, eng, rid_prefix=f"{mode}-")
         _, sub = next(ph)
         P.pipeline.run_phase(eng, sub)
@@ -339,7 +342,7 @@ def main():
                                             for k in range(n_eval)),
                              comparison_mode=mode)
         model = P.Model(mcfg, init="device", max_tokens=budget, max_seqs=cfg.scheduler.max_batch_requests)
-        return spec, P.Engine(cfg, clock=P.WallClock(), model=model)
+        return spec, P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
 
     # instrument the engine: capture the eval turn's first packed step and count native launches
     class Spy:

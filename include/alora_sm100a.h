@@ -221,7 +221,8 @@ typedef struct AloraModelDesc {
 /* One engine step: all spans packed back to back (varlen). Device arrays. */
 typedef struct AloraStepDesc {
   int32_t n_tokens, n_seqs, max_blocks, max_q, max_ctx;
-  const int32_t* tokens;        /* [M] */
+  const int32_t* tokens;        /* [M]; a negative entry t is next_ids[-t-1] of the PREVIOUS forward on this
+                                   buffer (a decode step launched before the host read that step's output) */
   const int32_t* positions;     /* [M] absolute */
   const int32_t* slot_mapping;  /* [M] */
   const int32_t* row_slot;      /* [M] adapter slot or -1 */
@@ -231,7 +232,7 @@ typedef struct AloraStepDesc {
   const int32_t* block_table;   /* [S, max_blocks] */
   const int32_t* last_row;      /* [S] row whose logits are produced */
   float* logits;                /* [S, V] fp32 out */
-  int32_t* next_ids;            /* [S] argmax out */
+  int32_t* next_ids;            /* [S] argmax out (read first for negative tokens, written last) */
   /* host-side shape summary, used only for the profiler's algorithmic bytes/flops */
   double attn_kv_tokens;        /* sum over spans of (start_pos + n) */
   double attn_qk_pairs;         /* sum over spans of n * (start_pos + (n + 1) / 2) */

@@ -11,13 +11,18 @@ namespace alora {
 
 // ----------------------------------------------------------------- embed ---
 // x (fp32 residual) = embed[tok] (+ sinusoidal pos for the ref arch, model.py:263)
+// tokens[m] < 0 names the previous forward's greedy id of span -tokens[m]-1 (prev_ids: the next_ids buffer
+// of the step, which still holds the previous launch's ids when this first kernel runs): decode steps can be
+// launched before the host has read the previous step's output.
 __global__ void embed_bf16_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
                                   const __nv_bfloat16* __restrict__ embed, const float* __restrict__ pos_table, int d,
-                                  float* __restrict__ x) {
+                                  float* __restrict__ x, const int32_t* __restrict__ prev_ids) {
   pdl_wait();
   pdl_trigger();
   const int m = blockIdx.x;
-  const __nv_bfloat16* e = embed + (int64_t)tokens[m] * d;
+  int tok = tokens[m];
+  if (tok < 0) tok = prev_ids[-tok - 1];
+  const __nv_bfloat16* e = embed + (int64_t)tok * d;
   const float* p = pos_table ? pos_table + (int64_t)positions[m] * d : nullptr;
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = __bfloat162float(e[i]);
@@ -26,9 +31,10 @@ __global__ void embed_bf16_kernel(const int32_t* __restrict__ tokens, const int3
 }
 
 int embed_bf16(const int32_t* tokens, const int32_t* positions, const __nv_bfloat16* embed, const float* pos_table,
-               int M, int d, float* x, cudaStream_t st) {
+               int M, int d, float* x, cudaStream_t st, const int32_t* prev_ids) {
   if (M == 0) return ALORA_OK;
-  ALORA_CUDA_CHECK(launch_pdl(embed_bf16_kernel, dim3(M), dim3(256), 0, st, nullptr, 0, tokens, positions, embed, pos_table, d, x));
+  ALORA_CUDA_CHECK(launch_pdl(embed_bf16_kernel, dim3(M), dim3(256), 0, st, nullptr, 0, tokens, positions, embed, pos_table, d, x,
+                              prev_ids));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }

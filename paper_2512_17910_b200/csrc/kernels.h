@@ -18,7 +18,8 @@ enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3, kEpiR
 
 // ---- fp32 storage / fp64 accumulation (parity tier), parity_f64.cu
 int embed_f32(const int32_t* tokens, const int32_t* positions, const float* embed, const float* pos_table, int M,
-              int d, float* x, cudaStream_t st);
+              int d, float* x, cudaStream_t st,
+              const int32_t* prev_ids = nullptr);
 int rmsnorm_f64(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps, float* out,
                 cudaStream_t st);
 int gemm_f64(int epi, const float* A, int lda, const float* Bt, int ldb, float* C, int ldc, int M, int N, int K,
@@ -40,7 +41,8 @@ int argmax_rows(const float* logits, int rows, int vocab, int32_t* out_ids, cuda
 
 // ---- bf16 storage / fp32 accumulation (tensor-core tier)
 int embed_bf16(const int32_t* tokens, const int32_t* positions, const __nv_bfloat16* embed, const float* pos_table,
-               int M, int d, float* x, cudaStream_t st);
+               int M, int d, float* x, cudaStream_t st,
+               const int32_t* prev_ids = nullptr);
 // out_bf16[r] = bf16( rmsnorm(x[rows[r]]) * w )
 int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps,
                  __nv_bfloat16* out, cudaStream_t st);

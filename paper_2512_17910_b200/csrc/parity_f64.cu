@@ -16,17 +16,19 @@ namespace alora {
 // ----------------------------------------------------------------- embed ---
 __global__ void embed_f32_kernel(const int32_t* __restrict__ tokens, const int32_t* __restrict__ positions,
                                  const float* __restrict__ embed, const float* __restrict__ pos_table, int d,
-                                 float* __restrict__ x) {
+                                 float* __restrict__ x, const int32_t* __restrict__ prev_ids) {
   const int m = blockIdx.x;
-  const float* e = embed + (int64_t)tokens[m] * d;
+  int tok = tokens[m];
+  if (tok < 0) tok = prev_ids[-tok - 1];  // the previous forward's greedy id of that span (see embed_bf16)
+  const float* e = embed + (int64_t)tok * d;
   const float* p = pos_table ? pos_table + (int64_t)positions[m] * d : nullptr;
   for (int i = threadIdx.x; i < d; i += blockDim.x) x[(int64_t)m * d + i] = p ? e[i] + p[i] : e[i];
 }
 
 int embed_f32(const int32_t* tokens, const int32_t* positions, const float* embed, const float* pos_table,
-              int M, int d, float* x, cudaStream_t st) {
+              int M, int d, float* x, cudaStream_t st, const int32_t* prev_ids) {
   if (M == 0) return ALORA_OK;
-  embed_f32_kernel<<<M, 256, 0, st>>>(tokens, positions, embed, pos_table, d, x);
+  embed_f32_kernel<<<M, 256, 0, st>>>(tokens, positions, embed, pos_table, d, x, prev_ids);
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }

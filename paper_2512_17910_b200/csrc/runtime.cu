@@ -218,7 +218,7 @@ int forward_f32(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     ++n;                               \
   } while (0)
   RUN(embed_f32(s.tokens, s.positions, static_cast<const float*>(d.embed), llama ? nullptr : d.pos_table, M, dm, x,
-                st));
+                st, s.next_ids));
   for (int l = 0; l < d.n_layers; ++l) {
     RUN(rmsnorm_f64(x, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     RUN(gemm_f64(kEpiStore, h, dm, static_cast<const float*>(mdl.w_qkv_t[l]), dm, qkv, Nqkv, M, Nqkv, dm, st));
@@ -312,7 +312,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     if (rc != ALORA_OK) return rc;                                              \
   } while (0)
   RUN("embed", m_ * dm_ * 6, 0, embed_bf16(s.tokens, s.positions, static_cast<const __nv_bfloat16*>(d.embed),
-                                           llama ? nullptr : d.pos_table, M, dm, x, st));
+                                           llama ? nullptr : d.pos_table, M, dm, x, st, s.next_ids));
   if (lora) RUN("lora_masks", m_ * 5, 0, lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
   for (int l = 0; l < d.n_layers; ++l) {
     RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,

@@ -148,6 +148,11 @@ class Model:
         self._logits = torch.empty((max_seqs, cfg.vocab_size), dtype=torch.float32, device="cuda")
         self._ids = torch.empty(max_seqs, dtype=torch.int32, device="cuda")
         self._ids_host = torch.empty(max_seqs, dtype=torch.int32, pin_memory=True)
+        # pipelined decode (launch_async / resolve): two pinned id buffers, the last launch's span count
+        self._ids_pin = [torch.empty(max_seqs, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+        self._pin_slot = 0
+        self._last_S = 0
+        self._h2d_event = None  # the last metadata upload; the pinned staging buffer is rewritten only after it
         self.last_launches = 0
 
     # ------------------------------------------------------------ weights ---
@@ -352,7 +357,7 @@ class Model:
                 or kv.shape[4] != cfg.kv_width or not kv.is_contiguous():
             raise ValueError(f"kv pool shape/dtype {tuple(kv.shape)} {kv.dtype} does not match the model")
 
-    def pack(self, seqs, block_size: int) -> dict:
+    def pack(self, seqs, block_size: int, token_refs: bool = False) -> dict:
         """Validate (model.py:250-259, 160-163) and pack all spans into one varlen int32 record."""
         cfg = self.config
         S = len(seqs)
@@ -391,8 +396,12 @@ class Model:
             toks.append(tk)
             tables.append(seq.block_ids[:need])
         tokens = np.concatenate(toks) if S > 1 else toks[0]
-        if tokens.min() < 0 or tokens.max() >= cfg.vocab_size:
+        if tokens.max() >= cfg.vocab_size:
             raise ValueError("token id outside the vocabulary")
+        if tokens.min() < 0:
+            # token_refs: -(j+1) = the previous launch's greedy id of its span j (resolved on the device)
+            if not token_refs or int(tokens.min()) < -self._last_S:
+                raise ValueError("token id outside the vocabulary")
         M = int(sum(lens))
         lens_a = np.asarray(lens, dtype=np.int64)
         starts_a = np.asarray(starts, dtype=np.int64)
@@ -437,7 +446,33 @@ class Model:
         logits = self._logits[:S].cpu().numpy() if want_logits else None
         t.cuda.current_stream().synchronize()
         self.last_d2h_bytes = 4 * S + (logits.nbytes if logits is not None else 0)
+        self._last_S = S
         return self._ids_host[:S].numpy().copy(), logits
+
+    def launch_async(self, p: dict, kv):
+        """Stage and launch a packed step without waiting for it; the greedy ids come back through `resolve`.
+        The step may reference the previous launch's ids (pack(token_refs=True)): pipelined decode."""
+        t = self._torch
+        st = self.stage(p, kv)
+        self._h2d_event = t.cuda.Event()  # the pinned staging buffer is rewritten only after this upload ran
+        self._h2d_event.record()
+        self.launch(st)
+        S = p["S"]
+        self._pin_slot ^= 1
+        buf = self._ids_pin[self._pin_slot]
+        buf[:S].copy_(self._ids[:S], non_blocking=True)
+        ev = t.cuda.Event()
+        ev.record()
+        self._last_S = S
+        self.last_d2h_bytes = 4 * S
+        return ev, buf, S
+
+    @staticmethod
+    def resolve(handle) -> np.ndarray:
+        """Wait for a launch_async step and return its greedy ids."""
+        ev, buf, S = handle
+        ev.synchronize()
+        return buf[:S].numpy().copy()
 
     def launch(self, st) -> None:
         """Enqueue one staged step on the current stream (decode steps: a CUDA-graph replay); no host sync."""
@@ -468,6 +503,9 @@ class Model:
         total = int(offs[-1])
         if total > self._steps.cap:
             self._steps = _StepBuffers(t, 2 * total)
+        if self._h2d_event is not None:  # a pipelined step's upload may still be queued behind the running one
+            self._h2d_event.synchronize()
+            self._h2d_event = None
         host = self._steps.host.numpy()
         host[:total] = np.concatenate(parts)
         dev = self._steps.dev
