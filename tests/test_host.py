@@ -333,3 +333,69 @@ def test_engine_config_json(tmp_path):
     p.write_text(json.dumps({"pool_block": 3}))
     with pytest.raises(ValueError, match="unknown engine config keys"):
         P.load_engine_config(p)
+
+
+class _DeferredOracle:
+    """Oracle model with the pipelined-decode interface (pack / launch_async / resolve): a decode step's input
+    token may name the previous launch's greedy id of a span (-(j+1)), as on the device."""
+
+    def __init__(self, oracle):
+        self.o = oracle
+        self.last_ids = np.zeros(0, dtype=np.int64)
+
+    def _ids(self, seqs, out):
+        return np.array([int(np.argmax(out[s.request_id])) for s in seqs], dtype=np.int64)
+
+    def forward_step(self, seqs, kv):
+        out = self.o.forward_step(seqs, kv)
+        self.last_ids = self._ids(seqs, out)
+        return out
+
+    def pack(self, seqs, block_size, token_refs=False):
+        res = []
+        for s in seqs:
+            t = np.asarray(s.tokens, dtype=np.int64)
+            if (t < 0).any():
+                assert token_refs and t.min() >= -len(self.last_ids)
+                t = np.where(t < 0, self.last_ids[np.maximum(-t - 1, 0)], t)
+            res.append(P.SeqInput(s.request_id, t, s.start_pos, list(s.block_ids), s.adapter, s.mask))
+        return res
+
+    def launch_async(self, seqs, kv):
+        return self.forward_step(seqs, kv) and self.last_ids
+
+    @staticmethod
+    def resolve(handle):
+        return handle
+
+
+@pytest.mark.parametrize("name", ["d64_multi_alora", "d64_bab_alora_b8", "c1_bab_alora"])
+def test_pipelined_decode_engine_matches_reference_pipeline(name):
+    """Engine(pipelined_decode=True) bookkeeping (placeholder tokens, deferred retire, device token refs) must
+    give the reference pipeline's ids, hits, first block tables, schedule and pool digests."""
+    g = golden_json("pipelines.json")[name]
+    spec = P.PipelineSpec(**g["spec"])
+    model = _DeferredOracle(O.OracleModel(O.OracleConfig(**g["model"])))
+    eng = P.build_engine(spec, model=P.ModelConfig(**g["model"]), engine_model=model, pool_storage="numpy",
+                         pipelined_decode=True, **g["engine"])
+    assert eng.pipelined_decode
+    tables = {}
+    orig = eng.scheduler._cache_lookup
+
+    def spy(req):
+        orig(req)
+        bt = eng.pool.block_table(req.request_id)
+        tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
+
+    eng.scheduler._cache_lookup = spy
+    P.run_sync_pipeline(spec, eng)
+    for rid, r in g["requests"].items():
+        mine = eng.finished[rid]
+        assert list(map(int, mine.generated)) == r["generated"], rid
+        assert (mine.hit_tokens, mine.computed_tokens) == (r["hit_tokens"], r["computed_tokens"]), rid
+    assert tables == g["first_tables"]
+    strip = lambda tr: [{k: v for k, v in row.items() if k != "pool_free"} for row in tr]
+    assert strip(eng.trace) == strip(g["trace"])
+    assert sorted(r["digest"] for r in eng.pool.dump_state() if r["digest"]) == \
+        sorted(r["digest"] for r in g["pool_dump"] if r["digest"])
+    eng.pool.check_conservation()
