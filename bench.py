@@ -359,6 +359,14 @@ def main():
                     self.launches += model.last_launches
                 return out
             model.run_packed = wrapped
+            orig_async = model.launch_async
+
+            def wrapped_async(p, kv):  # pipelined decode steps count too
+                out = orig_async(p, kv)
+                if self.armed:
+                    self.launches += model.last_launches
+                return out
+            model.launch_async = wrapped_async
 
     def run_turns(engine, spec, step_idx, spy, timed):
         """Base turn (untimed) then the eval turn; returns eval rows and the turn's wall/device times."""
