@@ -114,6 +114,33 @@ int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const f
   return ALORA_OK;
 }
 
+// Sum of exactly NP split-K partials (all loads issued before the adds; split order kept). A compile-time
+// count keeps only NP float4 in flight per call: the runtime-count version held 8 (32 registers), which
+// capped qkv_finalize at one 512-thread CTA per SM (two waves at M = 240).
+template <int NP>
+__device__ __forceinline__ float4 sum_parts_n(const float* __restrict__ base, int64_t pstride) {
+  float4 t[NP];
+#pragma unroll
+  for (int p = 0; p < NP; ++p) t[p] = __ldcg(reinterpret_cast<const float4*>(base + p * pstride));
+  float4 acc = t[0];
+#pragma unroll
+  for (int p = 1; p < NP; ++p) { acc.x += t[p].x; acc.y += t[p].y; acc.z += t[p].z; acc.w += t[p].w; }
+  return acc;
+}
+
+// Dispatch a kernel template on the split count (1..8).
+#define ALORA_NP_SWITCH(np, ...)                                          \
+  switch (np) {                                                           \
+    case 1: { constexpr int NP = 1; __VA_ARGS__; } break;                 \
+    case 2: { constexpr int NP = 2; __VA_ARGS__; } break;                 \
+    case 3: { constexpr int NP = 3; __VA_ARGS__; } break;                 \
+    case 4: { constexpr int NP = 4; __VA_ARGS__; } break;                 \
+    case 5: { constexpr int NP = 5; __VA_ARGS__; } break;                 \
+    case 6: { constexpr int NP = 6; __VA_ARGS__; } break;                 \
+    case 7: { constexpr int NP = 7; __VA_ARGS__; } break;                 \
+    default: { constexpr int NP = 8; __VA_ARGS__; } break;                \
+  }
+
 // Sum of up to 8 split-K partials at float4 index i (all loads issued before the adds; split order kept).
 __device__ __forceinline__ float4 sum_parts4(const float* __restrict__ base, int64_t pstride, int nparts) {
   float4 t[8];
@@ -130,9 +157,9 @@ __device__ __forceinline__ float4 sum_parts4(const float* __restrict__ base, int
 // ------------------------------------------------- deferred split-K consumers ---
 // x[src] (+)= sum_p partials[p][src] in split order (the o-proj / MLP-down epilogue the split-K GEMM
 // deferred), then out[r] = bf16(rmsnorm(x[src]) * w).
-template <int V>
+template <int V, int NP>
 __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict__ x, const float* __restrict__ part,
-                                                               int nparts, int64_t pstride,
+                                                               int64_t pstride,
                                                                const int32_t* __restrict__ rows, int d,
                                                                const float* __restrict__ w, float eps,
                                                                __nv_bfloat16* __restrict__ out,
@@ -146,20 +173,26 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)src * d);
   const int n4 = d >> 2;
   float4 v[V];
+  // every load of the row (x and the NP partials of all V chunks) is in flight before the first add
+  float4 pp[V][NP > 0 ? NP : 1];
+#pragma unroll
+  for (int j = 0; j < V; ++j) {
+    const int i = threadIdx.x + j * 256;
+    v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int p = 0; p < NP; ++p)
+      if (i < n4) pp[j][p] = __ldcg(reinterpret_cast<const float4*>(part + (int64_t)src * d + 4 * i + p * pstride));
+  }
   float ss = 0.f;
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     const int i = threadIdx.x + j * 256;
-    if (i < n4) {
-      float4 xv = xr[i];
-      if (nparts > 0) {
-        const float4 acc = sum_parts4(part + (int64_t)src * d + 4 * i, pstride, nparts);
-        xv.x += acc.x; xv.y += acc.y; xv.z += acc.z; xv.w += acc.w;
-        xr[i] = xv;
-      }
-      v[j] = xv;
-    } else {
-      v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (NP > 0 && i < n4) {
+      float4 acc = pp[j][0];
+#pragma unroll
+      for (int p = 1; p < NP; ++p) { acc.x += pp[j][p].x; acc.y += pp[j][p].y; acc.z += pp[j][p].z; acc.w += pp[j][p].w; }
+      v[j].x += acc.x; v[j].y += acc.y; v[j].z += acc.z; v[j].w += acc.w;
+      xr[i] = v[j];
     }
     ss = fmaf(v[j].x, v[j].x, ss); ss = fmaf(v[j].y, v[j].y, ss);
     ss = fmaf(v[j].z, v[j].z, ss); ss = fmaf(v[j].w, v[j].w, ss);
@@ -193,10 +226,23 @@ int residual_rmsnorm_bf16(float* x, const float* partials, int nparts, int M, co
   if (nparts > 8) return ALORA_EINVAL;
   const int v = (d / 4 + 255) / 256;
   const int64_t ps = (int64_t)M * d;
-  if (v <= 1) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<1>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
-  else if (v <= 2) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<2>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
-  else if (v <= 4) ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<4>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
-  else ALORA_CUDA_CHECK(launch_pdl(residual_rmsnorm_kernel<8>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, nparts, ps, rows, d, w, eps, out, zero_rows));
+  cudaError_t err = cudaSuccess;
+#define ALORA_RMS_LAUNCH(VV, NPP)                                                                                  \
+  err = launch_pdl(residual_rmsnorm_kernel<VV, NPP>, dim3(n_rows), dim3(256), 0, st, nullptr, 0, x, partials, ps, rows, \
+                   d, w, eps, out, zero_rows)
+#define ALORA_RMS_V(VV)                                          \
+  if (nparts == 0) {                                             \
+    ALORA_RMS_LAUNCH(VV, 0);                                     \
+  } else {                                                       \
+    ALORA_NP_SWITCH(nparts, ALORA_RMS_LAUNCH(VV, NP));           \
+  }
+  if (v <= 1) { ALORA_RMS_V(1) }
+  else if (v <= 2) { ALORA_RMS_V(2) }
+  else if (v <= 4) { ALORA_RMS_V(4) }
+  else { ALORA_RMS_V(8) }
+#undef ALORA_RMS_V
+#undef ALORA_RMS_LAUNCH
+  ALORA_CUDA_CHECK(err);
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -222,7 +268,8 @@ int sum_partials_f32(const float* partials, int nparts, int64_t n, float* out, c
 // Deferred epilogue of a split-K QKV projection: per row, sum the splits (in order), rotate-half RoPE in
 // fp32 on the q and k heads (the kEpiRope math of the GEMM epilogue, one rounding), store q|k|v bf16 and
 // scatter the k and v rows into the paged pool (model.py:217-222) -- the step's kv_write, fused.
-__global__ void __launch_bounds__(512) qkv_finalize_kernel(const float* __restrict__ part, int nparts, int64_t pstride,
+template <int NP>
+__global__ void __launch_bounds__(512, 2) qkv_finalize_kernel(const float* __restrict__ part, int64_t pstride,
                                                            int Nq, int Nkv, int D,
                                                            const int32_t* __restrict__ positions,
                                                            const float* __restrict__ cos_t,
@@ -246,7 +293,7 @@ __global__ void __launch_bounds__(512) qkv_finalize_kernel(const float* __restri
     vrow = pool + (((blk * n_layers + layer) * 2 + 1) * B + r) * Nkv;
   }
   const float* row = part + (int64_t)m * N;
-  auto sum4 = [&](int col) { return sum_parts4(row + col, pstride, nparts); };
+  auto sum4 = [&](int col) { return sum_parts_n<NP>(row + col, pstride); };
   auto pack4 = [](float a, float b, float c, float d) {
     __nv_bfloat162 lo = __floats2bfloat162_rn(a, b), hi = __floats2bfloat162_rn(c, d);
     return make_uint2(*reinterpret_cast<uint32_t*>(&lo), *reinterpret_cast<uint32_t*>(&hi));
@@ -288,8 +335,11 @@ int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv,
   if (nparts < 1 || nparts > 8 || !partials || !positions || !cos_t || !sin_t || D % 8 || Nq % D || Nkv % D || ldq % 4)
     return ALORA_EINVAL;
   const int64_t ps = (int64_t)M * (Nq + 2 * Nkv);
-  ALORA_CUDA_CHECK(launch_pdl(qkv_finalize_kernel, dim3(M), dim3(512), 0, st, nullptr, 0, partials, nparts, ps, Nq, Nkv,
-                              D, positions, cos_t, sin_t, qkv, ldq, slot_mapping, kv_pool, n_layers, layer, B));
+  cudaError_t err = cudaSuccess;
+  ALORA_NP_SWITCH(nparts, err = launch_pdl(qkv_finalize_kernel<NP>, dim3(M), dim3(512), 0, st, nullptr, 0, partials, ps,
+                                           Nq, Nkv, D, positions, cos_t, sin_t, qkv, ldq, slot_mapping, kv_pool,
+                                           n_layers, layer, B));
+  ALORA_CUDA_CHECK(err);
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -450,11 +500,18 @@ void configure_bf16_ops() {
   prefer_max_smem(rmsnorm_bf16_vec_kernel<2>);
   prefer_max_smem(rmsnorm_bf16_vec_kernel<4>);
   prefer_max_smem(rmsnorm_bf16_vec_kernel<8>);
-  prefer_max_smem(residual_rmsnorm_kernel<1>);
-  prefer_max_smem(residual_rmsnorm_kernel<2>);
-  prefer_max_smem(residual_rmsnorm_kernel<4>);
-  prefer_max_smem(residual_rmsnorm_kernel<8>);
-  prefer_max_smem(qkv_finalize_kernel);
+#define ALORA_PREFER_RMS(VV)                                                                                 \
+  prefer_max_smem(residual_rmsnorm_kernel<VV, 0>); prefer_max_smem(residual_rmsnorm_kernel<VV, 1>);             \
+  prefer_max_smem(residual_rmsnorm_kernel<VV, 2>); prefer_max_smem(residual_rmsnorm_kernel<VV, 3>);             \
+  prefer_max_smem(residual_rmsnorm_kernel<VV, 4>); prefer_max_smem(residual_rmsnorm_kernel<VV, 5>);             \
+  prefer_max_smem(residual_rmsnorm_kernel<VV, 6>); prefer_max_smem(residual_rmsnorm_kernel<VV, 7>);             \
+  prefer_max_smem(residual_rmsnorm_kernel<VV, 8>);
+  ALORA_PREFER_RMS(1) ALORA_PREFER_RMS(2) ALORA_PREFER_RMS(4) ALORA_PREFER_RMS(8)
+#undef ALORA_PREFER_RMS
+  prefer_max_smem(qkv_finalize_kernel<1>); prefer_max_smem(qkv_finalize_kernel<2>);
+  prefer_max_smem(qkv_finalize_kernel<3>); prefer_max_smem(qkv_finalize_kernel<4>);
+  prefer_max_smem(qkv_finalize_kernel<5>); prefer_max_smem(qkv_finalize_kernel<6>);
+  prefer_max_smem(qkv_finalize_kernel<7>); prefer_max_smem(qkv_finalize_kernel<8>);
   prefer_max_smem(lora_select_finalize_kernel);
   prefer_max_smem(sum_partials_kernel);
 }
