@@ -497,9 +497,13 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   uint64_t* kv_full = bars + 1;        // kNS<D>
   uint64_t* kv_empty = kv_full + kNS<D>;  // kNS<D>
   uint64_t* s_full = kv_empty + kNS<D>;   // kSBuf
-  uint64_t* p_full = s_full + kSBuf;   // 2
-  uint64_t* pv_done = p_full + 2;      // 2
-  uint64_t* s_free = pv_done + 2;      // kSBuf: PV of the P held in S buffer i has completed
+  // p_full[t % 3]: P_t is in TMEM. Three deep like S: softmax_{t+3} needs S_{t+3}, which needs PV_t complete,
+  // so a P barrier can never run a phase ahead of the MMA warp's parity test.
+  uint64_t* p_full = s_full + kSBuf;   // kSBuf
+  // s_free[i]: PV of the P held in S buffer i has completed (one phase per use of the buffer). It is also
+  // the softmax's "O holds PV_t" signal: the previous phase on s_free[t % 3] (PV_{t-3}) always completed
+  // before S_t was issued, so a parity wait on it can never match a stale phase (a 2-deep PV barrier could).
+  uint64_t* s_free = p_full + kSBuf;   // kSBuf
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + kSBuf);
   __shared__ int s_last;
 
@@ -533,10 +537,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&s_free[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
-      sm100::mbar_init(&p_full[i], 32 * live_warps);
-      sm100::mbar_init(&pv_done[i], 1);
-    }
+    for (int i = 0; i < kSBuf; ++i) sm100::mbar_init(&p_full[i], 32 * live_warps);
     sm100::fence_barrier_init();
   }
   if (warp == 5) sm100::tmem_alloc<(D == 64 ? 256 : 512)>(tmem_slot);
@@ -658,7 +659,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       }
       if (tp < ts) {
         uint32_t ready = 0;
-        if (lane == 0) ready = sm100::mbar_test(&p_full[tp & 1], (tp >> 1) & 1) ? 1u : 0u;
+        if (lane == 0) ready = sm100::mbar_test(&p_full[tp % kSBuf], (tp / kSBuf) & 1) ? 1u : 0u;
         ready = __shfl_sync(0xffffffffu, ready, 0);
         if (ready) {
           sm100::tc_fence_after();
@@ -670,7 +671,6 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
               const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
               sm100::mma_bf16_ts(tO, tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
             }
-            sm100::mma_commit(&pv_done[tp & 1]);
             sm100::mma_commit(&kv_empty[tp % kNS<D>]);
             sm100::mma_commit(&s_free[tp % kSBuf]);
           }
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::tc_fence_after();
       if (a.exp == 3) {  // timing experiment: no softmax work at all
         sm100::tc_fence_before();
-        sm100::mbar_arrive(&p_full[t & 1]);
+        sm100::mbar_arrive(&p_full[t % kSBuf]);
         continue;
       }
       if (t == 0 && tid == 0) ATTN_TRACE(2);
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
       if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
         const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
-        sm100::mbar_wait(&pv_done[(t - 1) & 1], ((t - 1) >> 1) & 1);  // O holds PV_{t-1}
+        sm100::mbar_wait(&s_free[(t - 1) % kSBuf], ((t - 1) / kSBuf) & 1);  // O holds PV_{t-1}
         sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
@@ -767,11 +767,11 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       sm100::tmem_st_wait();
       l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&p_full[t & 1]);
+      sm100::mbar_arrive(&p_full[t % kSBuf]);
     }
     if (tid == 0) ATTN_TRACE(3);
     // final O
-    sm100::mbar_wait(&pv_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+    sm100::mbar_wait(&s_free[(n_tiles - 1) % kSBuf], ((n_tiles - 1) / kSBuf) & 1);
     sm100::tc_fence_after();
     {
       const int pr = qt * kQT + r;

@@ -24,9 +24,30 @@ __global__ void embed_bf16_kernel(const int32_t* __restrict__ tokens, const int3
   if (tok < 0) tok = prev_ids[-tok - 1];
   const __nv_bfloat16* e = embed + (int64_t)tok * d;
   const float* p = pos_table ? pos_table + (int64_t)positions[m] * d : nullptr;
+  float* xr = x + (int64_t)m * d;
+  if (d % 8 == 0) {  // 16-byte embedding loads, two float4 stores
+    for (int i = threadIdx.x * 8; i < d; i += blockDim.x * 8) {
+      const uint4 u = *reinterpret_cast<const uint4*>(e + i);
+      const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+      float f[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[k]));
+        f[2 * k] = t.x;
+        f[2 * k + 1] = t.y;
+      }
+      if (p) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) f[k] += p[i + k];
+      }
+      *reinterpret_cast<float4*>(xr + i) = make_float4(f[0], f[1], f[2], f[3]);
+      *reinterpret_cast<float4*>(xr + i + 4) = make_float4(f[4], f[5], f[6], f[7]);
+    }
+    return;
+  }
   for (int i = threadIdx.x; i < d; i += blockDim.x) {
     const float v = __bfloat162float(e[i]);
-    x[(int64_t)m * d + i] = p ? v + p[i] : v;
+    xr[i] = p ? v + p[i] : v;
   }
 }
 
