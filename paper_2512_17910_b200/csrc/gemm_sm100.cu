@@ -391,6 +391,197 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (threadIdx.x == 64) TRACE(5);
 }
 
+// ============================================================================================================
+// Persistent large-M GEMM (prefill / LoRA recompute, no split-K): one CTA per SM walks the output tiles
+// (N-fastest, so the tiles in flight share A row blocks and B column blocks through L2) and keeps TWO TMEM
+// accumulators: the epilogue of tile i (TMEM -> registers -> fused epilogue -> global) runs while the MMA warp
+// accumulates tile i+1, instead of every CTA paying its epilogue, setup and TMEM allocation serially.
+//   warp 0   TMA producer over (tile, K block) through one smem ring
+//   warp 1   TMEM allocator (2 x BN columns) + tcgen05.mma issuer; waits tmem_empty[b] before reusing b
+//   warps 2-5 epilogue: wait tmem_full[b], emit, arrive tmem_empty[b]
+// ============================================================================================================
+template <int BN>
+struct PCfg {
+  static constexpr int kABytes = kBM * kBK * 2;
+  static constexpr int kBBytes = BN * kBK * 2;
+  static constexpr int kStage = kABytes + kBBytes;
+  static constexpr int kStages = (kSmemBudget / kStage) > 10 ? 10 : (kSmemBudget / kStage);
+  static constexpr int kTmemCols = 2 * BN;  // two accumulators
+  static constexpr int kSmem = 1024 + kStages * kStage + 256;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_bf16_persist_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                             const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_u,
+                             const GemmArgs args) {
+  using C = PCfg<BN>;
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tmem_full = empty + C::kStages;  // [2]
+  uint64_t* tmem_empty = tmem_full + 2;      // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n_n = (args.N + BN - 1) / BN, n_m = (args.M + kBM - 1) / kBM;
+  const int n_tiles = n_n * n_m;
+  const int nkb = (args.K + kBK - 1) / kBK;
+  const int nkl = args.ks > 0 ? (args.ks + kBK - 1) / kBK : 0;
+  if (threadIdx.x == 0) TRACE(0);
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tm_a);
+    sm100::prefetch_tmap(&tm_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&tmem_full[b], 1);
+      sm100::mbar_init(&tmem_empty[b], 4);  // one arrival per epilogue warp
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // LoRA extra K of a tile: the m tile's slot mask decides which K blocks are present
+  auto tile_of = [&](int t, int& m_tile, int& n0) { m_tile = t / n_n; n0 = (t % n_n) * BN; };
+
+  // Producer and MMA loops run warp-converged with one elected lane per operation (see gemm_ws_kernel: a lone
+  // lane looping while its siblings wait let ptxas clobber the MMA's uniform TMEM operand).
+  if (warp == 0) {
+    const uint64_t pol_act = sm100::policy_evict_last();
+    const uint64_t pol_w = sm100::policy_evict_normal();  // re-read by the m tiles in flight
+    int s = 0;
+    uint32_t phase = 0;
+    auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+      int m_tile, n0;
+      tile_of(t, m_tile, n0);
+      const int m0 = m_tile * kBM;
+      for (int kb = 0; kb < nkb; ++kb) {
+        sm100::mbar_wait(&empty[s], phase ^ 1);
+        if (sm100::elect_one()) {
+          uint8_t* sa = smem + s * C::kStage;
+          sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
+          sm100::tma_load_2d(sa, &tm_a, &full[s], kb * kBK, m0, pol_act);
+          sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
+        }
+        __syncwarp();
+        next();
+      }
+      if (nkl > 0) {
+        const int target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+        const uint32_t mask = args.tile_slot_mask[m_tile];
+        for (int j = 0; j < nkl; ++j) {
+          if (!lora_block_present(j, args.rank, mask)) continue;
+          sm100::mbar_wait(&empty[s], phase ^ 1);
+          if (sm100::elect_one()) {
+            uint8_t* sa = smem + s * C::kStage;
+            sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
+            sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, target, pol_act);
+            sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
+          }
+          __syncwarp();
+          next();
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
+    int s = 0;
+    uint32_t phase = 0;
+    int i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      int m_tile, n0;
+      tile_of(t, m_tile, n0);
+      const int b = i & 1;
+      if (i >= 2) sm100::mbar_wait(&tmem_empty[b], ((i >> 1) - 1) & 1);  // epilogue drained accumulator b
+      sm100::tc_fence_after();
+      const uint32_t acc_t = tmem + (uint32_t)(b * BN);
+      int n_iters = nkb;
+      if (nkl > 0) {
+        const uint32_t mask = args.tile_slot_mask[m_tile];
+        for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+      }
+      for (int it = 0; it < n_iters; ++it) {
+        sm100::mbar_wait(&full[s], phase);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint8_t* sa = smem + s * C::kStage;
+          const uint64_t da = sm100::umma_desc_sw128(sa);
+          const uint64_t db = sm100::umma_desc_sw128(sa + C::kABytes);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            sm100::mma_bf16_ss(acc_t, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, (it > 0 || k > 0) ? 1u : 0u);
+          sm100::mma_commit(&empty[s]);
+        }
+        __syncwarp();
+        if (++s == C::kStages) { s = 0; phase ^= 1; }
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&tmem_full[b]);
+      __syncwarp();
+    }
+  } else {
+    const int quarter = warp & 3;
+    const int trow_idx = quarter * 32 + lane;
+    int i = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+      int m_tile, n0;
+      tile_of(t, m_tile, n0);
+      const int m0 = m_tile * kBM;
+      const int b = i & 1;
+      sm100::mbar_wait(&tmem_full[b], (i >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t trow = tmem + (uint32_t)(b * BN) + ((uint32_t)(quarter * 32) << 16);
+      auto tmem_fetch = [&](int c0, float (&v)[32]) {  // warp-collective
+        uint32_t r[32];
+        sm100::tmem_ld_32x32b_x32(trow + c0, r);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 32; ++q) v[q] = __uint_as_float(r[q]);
+      };
+      if (m0 + quarter * 32 < args.M) {  // warp-uniform: skip all-padding lane quarters
+        const int units = units_per_row<BN>(args, n0);
+        for (int u = 0; u < units; ++u) emit_unit<BN>(args, n0, m0 + trow_idx, u, tmem_fetch);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tmem_empty[b]);
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) sm100::tmem_dealloc<C::kTmemCols>(tmem);
+  if (threadIdx.x == 64) TRACE(5);
+}
+
+template <int BN>
+int launch_persist(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, const CUtensorMap& u,
+                   const GemmArgs& args, cudaStream_t st) {
+  using C = PCfg<BN>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(gemm_bf16_persist_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
+        cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  const int tiles = ((args.N + BN - 1) / BN) * ((args.M + kBM - 1) / kBM);
+  const dim3 grid(std::min(tiles, kNumSMs));
+  ALORA_CUDA_CHECK(launch_pdl(gemm_bf16_persist_kernel<BN>, grid, dim3(kThreads), C::kSmem, st, nullptr, 0, a, b, s, u,
+                              args));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
 template <int BN>
 int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, const CUtensorMap& u,
            const GemmArgs& args, cudaStream_t st) {
@@ -1272,6 +1463,15 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (splits > 1) {
     args.partial = static_cast<float*>(ws->partial);
     args.counters = ws->counters;
+  }
+  static const bool no_persist = getenv("ALORA_GEMM_NO_PERSIST") != nullptr;  // A/B switch
+  if (splits == 1 && !no_persist && tiles > kNumSMs) {  // several tiles per SM: overlap epilogues with MMAs
+    switch (BN) {
+      case 256: return launch_persist<256>(ta, tb, ts, tu, args, st);
+      case 128: return launch_persist<128>(ta, tb, ts, tu, args, st);
+      case 64: return launch_persist<64>(ta, tb, ts, tu, args, st);
+      default: return launch_persist<32>(ta, tb, ts, tu, args, st);
+    }
   }
   switch (BN) {
     case 256: return launch<256>(ta, tb, ts, tu, args, st);

@@ -70,7 +70,8 @@ def test_gemm_split_k_deterministic_and_correct(M, N, K):
 
 
 @pytest.mark.parametrize("M,N,K", [(1, 64, 64), (5, 128, 256), (128, 256, 512), (200, 384, 1000), (1000, 512, 2048),
-                                   (77, 3072, 2048)])
+                                   (77, 3072, 2048),
+                                   (2100, 2048, 1024), (4100, 640, 512)])  # > 148 tiles: persistent kernel
 def test_gemm_store_and_fp32(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N)
     A, Bt = _bf((M, K), g), _bf((N, K), g)
@@ -85,8 +86,8 @@ def test_gemm_store_and_fp32(M, N, K):
     np.testing.assert_array_equal(C16.float().cpu().numpy(), C32.to(torch.bfloat16).float().cpu().numpy())
 
 
-def test_gemm_add_relu_swiglu():
-    M, N, K = 300, 512, 640
+@pytest.mark.parametrize("M,N,K", [(300, 512, 640), (3000, 2048, 640)])  # the second: persistent, SwiGLU BN=256
+def test_gemm_add_relu_swiglu(M, N, K):
     g = torch.Generator(device="cuda").manual_seed(1)
     A, Bt = _bf((M, K), g), _bf((N, K), g, 0.05)
     ref = A.double() @ Bt.double().T
@@ -106,13 +107,14 @@ def test_gemm_add_relu_swiglu():
     np.testing.assert_allclose(Sg.float().cpu().numpy(), want.float().cpu().numpy(), rtol=2e-2, atol=2e-2)
 
 
-def test_gemm_rows_independent_of_batch_bitwise():
+@pytest.mark.parametrize("M", [333, 2500])  # 2500 rows: the persistent kernel (160 tiles)
+def test_gemm_rows_independent_of_batch_bitwise(M):
     K, N = 2048, 1024
     g = torch.Generator(device="cuda").manual_seed(2)
-    A, Bt = _bf((333, K), g), _bf((N, K), g)
-    big = torch.empty((333, N), device="cuda")
-    gemm(16, A, Bt, big, 333, N, K)
-    for r in (0, 127, 128, 332):
+    A, Bt = _bf((M, K), g), _bf((N, K), g)
+    big = torch.empty((M, N), device="cuda")
+    gemm(16, A, Bt, big, M, N, K)
+    for r in (0, 127, 128, M - 1):
         one = torch.empty((1, N), device="cuda")
         gemm(16, A[r:r + 1].contiguous(), Bt, one, 1, N, K)
         assert torch.equal(one[0], big[r]), r
@@ -130,7 +132,7 @@ def _qkv(x, w_t, nq, nkv, row_slot, row_apply, down, up_t, n_slots, rank, target
     return out
 
 
-@pytest.mark.parametrize("M", [3, 130, 700])
+@pytest.mark.parametrize("M", [3, 130, 700, 4000])  # 4000: persistent kernel with the LoRA extra K
 def test_qkv_proj_fused_lora_bf16(M):
     K, nq, nkv, n_slots, rank = 512, 512, 128, 3, 32
     g = torch.Generator(device="cuda").manual_seed(M)
