@@ -250,54 +250,58 @@ __global__ void __launch_bounds__(kThreads, 1)
   int n_iters = kb1 - kb0;
   for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
 
+  // warp-converged loops, one elected lane per operation (see gemm_ws_kernel / gemm_bf16_persist_kernel)
   if (warp == 0) {
-    if (sm100::elect_one()) {
-      const uint64_t pol_act = sm100::policy_evict_last();  // activations: re-read by every N tile
-      const uint64_t pol_w = sm100::policy_evict_first();   // weights: streamed once per forward
-      int s = 0;
-      uint32_t phase = 0;
-      auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
-      for (int kb = kb0; kb < kb1; ++kb) {
-        sm100::mbar_wait(&empty[s], phase ^ 1);
+    const uint64_t pol_act = sm100::policy_evict_last();  // activations: re-read by every N tile
+    const uint64_t pol_w = sm100::policy_evict_first();   // weights: streamed once per forward
+    int s = 0;
+    uint32_t phase = 0;
+    auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
+    for (int kb = kb0; kb < kb1; ++kb) {
+      sm100::mbar_wait(&empty[s], phase ^ 1);
+      if (sm100::elect_one()) {
         uint8_t* sa = smem + s * C::kStage;
         sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
         sm100::tma_load_2d(sa, &tm_a, &full[s], kb * kBK, m0, pol_act);
         sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
-        next();
       }
-      for (int j = 0; j < nkl; ++j) {
-        if (!lora_block_present(j, args.rank, mask)) continue;
-        sm100::mbar_wait(&empty[s], phase ^ 1);
+      __syncwarp();
+      next();
+    }
+    for (int j = 0; j < nkl; ++j) {
+      if (!lora_block_present(j, args.rank, mask)) continue;
+      sm100::mbar_wait(&empty[s], phase ^ 1);
+      if (sm100::elect_one()) {
         uint8_t* sa = smem + s * C::kStage;
         sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
         sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, target, pol_act);
         sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
-        next();
       }
+      __syncwarp();
+      next();
     }
   } else if (warp == 1) {
-    if (sm100::elect_one()) {
-      constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
-      int s = 0;
-      uint32_t phase = 0;
-      uint32_t acc = 0;
-      for (int it = 0; it < n_iters; ++it) {
-        sm100::mbar_wait(&full[s], phase);
-        sm100::tc_fence_after();
-        if (it == 0) TRACE(1);
+    constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
+    int s = 0;
+    uint32_t phase = 0;
+    for (int it = 0; it < n_iters; ++it) {
+      sm100::mbar_wait(&full[s], phase);
+      sm100::tc_fence_after();
+      if (it == 0 && lane == 0) TRACE(1);
+      if (sm100::elect_one()) {
         const uint8_t* sa = smem + s * C::kStage;
         const uint64_t da = sm100::umma_desc_sw128(sa);
         const uint64_t db = sm100::umma_desc_sw128(sa + C::kABytes);
 #pragma unroll
-        for (int k = 0; k < kBK / 16; ++k) {  // +32 bytes per K=16 step inside the 128B swizzle atom
-          sm100::mma_bf16_ss(tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc, acc);
-          acc = 1;
-        }
+        for (int k = 0; k < kBK / 16; ++k)  // +32 bytes per K=16 step inside the 128B swizzle atom
+          sm100::mma_bf16_ss(tmem, da + (uint64_t)(k * 2), db + (uint64_t)(k * 2), idesc,
+                             (it > 0 || k > 0) ? 1u : 0u);
         sm100::mma_commit(&empty[s]);
-        if (++s == C::kStages) { s = 0; phase ^= 1; }
       }
-      sm100::mma_commit(tmem_full);
+      __syncwarp();
+      if (++s == C::kStages) { s = 0; phase ^= 1; }
     }
+    if (sm100::elect_one()) sm100::mma_commit(tmem_full);
     __syncwarp();
   } else {
     // epilogue warps: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
