@@ -833,7 +833,13 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
 // kernel is bound by HBM and per-chunk latency, not by tensor throughput.
 // ============================================================================================================
 constexpr int kDecWarpsSplit = 4;  // warps per CTA when the keys are split into partitions
-constexpr int kDecWarpsWhole = 8;  // warps per CTA when one CTA covers a (sequence, kv head)
+// warps per CTA when one CTA covers a (sequence, kv head): each warp's 2-stage ring is 8 KB x D/64, so D=128
+// stays at 4 warps (128 KB) -- 8 would need 256 KB of shared memory
+template <int D>
+constexpr int kDecWarpsWhole = D == 64 ? 8 : 4;
+// resident split-mode CTAs per SM (shared memory bound): 3 at D=64 (66 KB), 1 at D=128 (130 KB)
+template <int D>
+constexpr int kDecSplitCtasPerSm = D == 64 ? 3 : 1;
 constexpr int kDecMaxG = 8;
 constexpr int kDecNS = 2;     // ring stages per warp
 constexpr int kDecKeys = 32;  // keys per chunk (one per lane)
@@ -1068,13 +1074,13 @@ int launch_decode(const AttnArgs& a, dim3 grid, int G, int64_t kv_rows, cudaStre
   // otherwise 4-warp CTAs over key partitions
   const bool whole = a.n_parts == 1;
   switch (G) {
-    case 1: return whole ? launch_decode_g<D, 1, kDecWarpsWhole>(a, grid, tm, st)
+    case 1: return whole ? launch_decode_g<D, 1, kDecWarpsWhole<D>>(a, grid, tm, st)
                          : launch_decode_g<D, 1, kDecWarpsSplit>(a, grid, tm, st);
-    case 2: return whole ? launch_decode_g<D, 2, kDecWarpsWhole>(a, grid, tm, st)
+    case 2: return whole ? launch_decode_g<D, 2, kDecWarpsWhole<D>>(a, grid, tm, st)
                          : launch_decode_g<D, 2, kDecWarpsSplit>(a, grid, tm, st);
-    case 4: return whole ? launch_decode_g<D, 4, kDecWarpsWhole>(a, grid, tm, st)
+    case 4: return whole ? launch_decode_g<D, 4, kDecWarpsWhole<D>>(a, grid, tm, st)
                          : launch_decode_g<D, 4, kDecWarpsSplit>(a, grid, tm, st);
-    case 8: return whole ? launch_decode_g<D, 8, kDecWarpsWhole>(a, grid, tm, st)
+    case 8: return whole ? launch_decode_g<D, 8, kDecWarpsWhole<D>>(a, grid, tm, st)
                          : launch_decode_g<D, 8, kDecWarpsSplit>(a, grid, tm, st);
     default: return ALORA_EINVAL;
   }
@@ -1082,7 +1088,7 @@ int launch_decode(const AttnArgs& a, dim3 grid, int G, int64_t kv_rows, cudaStre
 
 // Decode plan: with at least ~half an SM-count of (sequence, kv head) units, one 8-warp CTA per unit
 // covers all its keys (no partition merge); below that, 4-warp CTAs over key partitions (~3 per SM).
-void plan_decode(int n_seqs, int max_ctx, int Hkv, int& part_size, int& n_parts) {
+void plan_decode(int n_seqs, int max_ctx, int Hkv, int D, int& part_size, int& n_parts) {
   const int units = std::max(1, n_seqs * Hkv);
   static const int whole_min = getenv("ALORA_DEC_WHOLE_MIN") ? atoi(getenv("ALORA_DEC_WHOLE_MIN")) : kNumSMs / 2;
   if (units >= whole_min) {
@@ -1090,7 +1096,8 @@ void plan_decode(int n_seqs, int max_ctx, int Hkv, int& part_size, int& n_parts)
     part_size = (max_ctx + 31) / 32 * 32;
     return;
   }
-  int np = std::max(1, std::min({kMaxParts, (3 * kNumSMs) / units, (max_ctx + kMinPartKeys - 1) / kMinPartKeys}));
+  const int slots = (D == 64 ? kDecSplitCtasPerSm<64> : kDecSplitCtasPerSm<128>) * kNumSMs;
+  int np = std::max(1, std::min({kMaxParts, slots / units, (max_ctx + kMinPartKeys - 1) / kMinPartKeys}));
   int ps = (max_ctx + np - 1) / np;
   ps = (ps + 31) / 32 * 32;
   n_parts = (max_ctx + ps - 1) / ps;
@@ -1206,7 +1213,7 @@ int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, in
   plan(n_seqs, max_q, max_ctx, H, Hkv, D, ps, np, nq);
   if (max_q == 1 && H / Hkv <= kDecMaxG) {
     int dps, dnp;
-    plan_decode(n_seqs, max_ctx, Hkv, dps, dnp);
+    plan_decode(n_seqs, max_ctx, Hkv, D, dps, dnp);
     np = std::max(np, dnp);
   }
   if (np <= 1) return 0;
@@ -1230,7 +1237,7 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
   const bool decode = !no_dec && max_q == 1 && (Gq == 1 || Gq == 2 || Gq == 4 || Gq == 8) && total_blocks > 0 &&
                       B <= kDecKeys && kDecKeys % B == 0 && kv_rows_all < (1ll << 31);
   if (decode) {
-    plan_decode(n_seqs, max_ctx, Hkv, a.part_size, a.n_parts);
+    plan_decode(n_seqs, max_ctx, Hkv, D, a.part_size, a.n_parts);
     a.n_qtiles = 1;
     // fewer partitions when the caller's workspace cannot hold them (it is sized by attn_bf16_workspace_bound)
     while (a.n_parts > 1 && (ws == nullptr || ws_bytes < (int64_t)a.n_parts * M * H * (D + 2) * 4 +

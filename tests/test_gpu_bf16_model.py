@@ -62,6 +62,7 @@ def _attn_case(n_seqs, H, Hkv, D, B, starts, lens, seed):
     # decode steps (one query row per sequence): the split-KV decode kernel, every GQA group size it serves
     (32, 8, 64, 16, [2047, 5, 0, 130, 31, 32, 33], [1] * 7),
     (8, 8, 128, 16, [1000, 77], [1, 1]),             # G=1, D=128
+    (32, 8, 128, 16, list(range(0, 1100, 100)), [1] * 11),  # D=128 with units >= 74: whole-context CTAs
     (16, 2, 64, 16, [511, 3], [1, 1]),               # G=8
     (8, 4, 64, 8, [300, 64, 7], [1, 1, 1]),          # G=2, B=8
     (32, 8, 64, 32, [4000, 100], [1, 1]),            # B=32: one page per 32-key chunk
