@@ -34,6 +34,7 @@ for r in range(n_req):
     mask = np.arange(cached, cached + suffix) < cached + suffix - 19  # adapter on the last 19 rows
     seqs.append(P.SeqInput(f"r{r}", toks, cached, ids, ads[r % 3], mask))
 p = model.pack(seqs, B)
+if os.environ.get("FORCE_GRAPH"): p["graphable"] = True
 st = model.stage(p, pool.kv)
 for _ in range(3):
     model.launch(st)
