@@ -701,8 +701,14 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
   const int split = blockIdx.z;
   if (threadIdx.x == 0) TRACE(0);
   const int nkb_all = (args.K + kBK - 1) / kBK;
-  const int per = (nkb_all + S - 1) / S;
-  const int kb0 = min(nkb_all, split * per), kb1 = min(nkb_all, kb0 + per);
+  // The LoRA K blocks ride with the last split: size the splits over base + LoRA blocks so that split does not
+  // run ~nkl blocks longer than the others, keeping at least one base block in it
+  int per = (nkb_all + S - 1) / S;
+  if (args.ks > 0 && S > 1) {
+    const int nkl_all = (args.ks + kBK - 1) / kBK;
+    per = max(per, min((nkb_all + nkl_all + S - 1) / S, (nkb_all - 1) / (S - 1)));
+  }
+  const int kb0 = min(nkb_all, split * per), kb1 = split == S - 1 ? nkb_all : min(nkb_all, kb0 + per);
   const int n_base = kb1 - kb0;
 
   if (warp == 0 && lane == 0) {
