@@ -506,11 +506,9 @@ class Model:
         self._check_pool(kv)
         self._grow_workspace(p["M"])
         handle = self._native_handle(kv)
-        parts = [np.ascontiguousarray(p[f], dtype=np.int32).reshape(-1) for f in self._FIELDS]
-        ap = p["row_apply"].astype(np.uint8)
-        ap = np.concatenate([ap, np.zeros((-len(ap)) % 4, np.uint8)]).view(np.int32)
-        parts.append(ap)
-        offs = np.cumsum([0] + [len(x) for x in parts])
+        parts = [p[f] for f in self._FIELDS]
+        sizes = [x.size for x in parts] + [(len(p["row_apply"]) + 3) // 4]  # row_apply: bytes packed in int32
+        offs = np.cumsum([0] + sizes)
         total = int(offs[-1])
         if total > self._steps.cap:
             self._steps = _StepBuffers(t, 2 * total)
@@ -518,7 +516,11 @@ class Model:
             self._h2d_event.synchronize()
             self._h2d_event = None
         host = self._steps.host.numpy()
-        host[:total] = np.concatenate(parts)
+        for i, x in enumerate(parts):  # straight into the pinned staging buffer (no intermediate concatenation)
+            host[offs[i]:offs[i + 1]] = np.asarray(x).reshape(-1)
+        ap = host[offs[-2]:offs[-1]].view(np.uint8)
+        ap[:len(p["row_apply"])] = p["row_apply"]
+        ap[len(p["row_apply"]):] = 0
         dev = self._steps.dev
         dev[:total].copy_(self._steps.host[:total], non_blocking=True)
         base = dev.data_ptr()
