@@ -399,3 +399,50 @@ def test_pipelined_decode_engine_matches_reference_pipeline(name):
     assert sorted(r["digest"] for r in eng.pool.dump_state() if r["digest"]) == \
         sorted(r["digest"] for r in g["pool_dump"] if r["digest"])
     eng.pool.check_conservation()
+
+
+def _fake_packer(vocab=384, graphs=False, last_S=0):
+    import types
+    cfg = P.ModelConfig(arch="llama", n_layers=2, n_heads=8, n_kv_heads=2, head_dim=64, d_model=256, ffn_dim=512,
+                        vocab_size=vocab, max_seq_len=4096, seed=4, dtype="bf16")
+    slots = {None: -1, "a0": 0, "a1": 1}
+    return types.SimpleNamespace(config=cfg, _max_seqs=64, _graphs=graphs, GRAPH_BLOCK_BUCKET=32, _last_S=last_S,
+                                 _prefill_shapes={},
+                                 _slot_for=lambda a: slots[None if a is None else a.adapter_id])
+
+
+def test_step_packer_layout_and_token_refs():
+    """Model.pack (the varlen step record the native forward reads), on CPU: positions, slot mapping, row
+    adapter slots / apply flags, block tables, and the pipelined-decode token references."""
+    from paper_2512_17910_b200.model import Model
+    act = P.generate_adapter("a0", 256, 4, seed=1, invocation_tokens=(1, 2, 3))
+    std = P.generate_adapter("a1", 256, 4, seed=2, mode="standard")
+    B = 16
+    seqs = [P.SeqInput("r0", np.array([5, 6, 7]), 30, [4, 9, 11], None, None),
+            P.SeqInput("r1", np.array([8, 9]), 0, [3], act, np.array([True, False])),
+            P.SeqInput("r2", np.array([10]), 17, [1, 2], std, None)]
+    p = Model.pack(_fake_packer(), seqs, B)
+    assert p["M"] == 6 and p["S"] == 3 and p["max_q"] == 3 and p["max_ctx"] == 33
+    np.testing.assert_array_equal(p["positions"], [30, 31, 32, 0, 1, 17])
+    np.testing.assert_array_equal(p["cu_q"], [0, 3, 5, 6])
+    np.testing.assert_array_equal(p["last_row"], [2, 4, 5])
+    np.testing.assert_array_equal(p["slot_mapping"], [9 * B + 14, 9 * B + 15, 11 * B, 3 * B, 3 * B + 1, 2 * B + 1])
+    np.testing.assert_array_equal(p["row_slot"], [-1, -1, -1, 0, 0, 1])
+    np.testing.assert_array_equal(p["row_apply"], [0, 0, 0, 0, 1, 1])  # masked activated row keeps the base
+    np.testing.assert_array_equal(p["block_table"], [[4, 9, 11], [3, 0, 0], [1, 2, 0]])
+    # token references: -(j+1) names span j of the previous launch; only with token_refs and j < last S
+    ref = [P.SeqInput("r0", np.array([-2]), 33, [4, 9, 11], None, None)]
+    with pytest.raises(ValueError):
+        Model.pack(_fake_packer(last_S=3), ref, B)
+    with pytest.raises(ValueError):
+        Model.pack(_fake_packer(last_S=1), ref, B, token_refs=True)
+    q = Model.pack(_fake_packer(last_S=3), ref, B, token_refs=True)
+    assert q["tokens"].tolist() == [-2]
+    with pytest.raises(ValueError):  # above the vocabulary is never a reference
+        Model.pack(_fake_packer(last_S=3), [P.SeqInput("r0", np.array([384]), 0, [1], None, None)], B,
+                   token_refs=True)
+    # a recurring prefill shape is marked for graph capture on its second sighting; decode steps always are
+    fk = _fake_packer(graphs=True)
+    assert not Model.pack(fk, seqs, B)["graphable"] and Model.pack(fk, seqs, B)["graphable"]
+    dec = Model.pack(fk, [P.SeqInput("r0", np.array([5]), 40, [4, 9, 11], None, None)], B)
+    assert dec["graphable"] and dec["maxb"] == 32 and dec["max_ctx"] == 32 * B
