@@ -443,6 +443,8 @@ __global__ void __launch_bounds__(kShrinkThreads) lora_shrink_bf16_kernel(
     const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem_raw);
+  pdl_wait();  // h comes from the RMSNorm before
+  pdl_trigger();
   const int m = blockIdx.x;
   const int KS = n_slots * R;
   const int slot = row_slot[m];
@@ -485,8 +487,17 @@ int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_sl
                      cudaStream_t st) {
   if (M == 0 || n_slots == 0) return ALORA_OK;
   if (K % 8 != 0) return ALORA_EINVAL;
-  lora_shrink_bf16_kernel<<<M, kShrinkThreads, K * 2, st>>>(h, M, K, row_slot, row_apply, down, n_slots, R,
-                                                            slot_targets, s);
+  if (K * 2 > 48 * 1024) {
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(lora_shrink_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, K * 2) !=
+          cudaSuccess)
+        return ALORA_ECUDA;
+      configured = true;
+    }
+  }
+  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_bf16_kernel, dim3(M), dim3(kShrinkThreads), (size_t)K * 2, st, nullptr, 0, h,
+                              M, K, row_slot, row_apply, down, n_slots, R, slot_targets, s));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
