@@ -194,29 +194,34 @@ __global__ void __launch_bounds__(256) residual_rmsnorm_kernel(float* __restrict
   float4* xr = reinterpret_cast<float4*>(x + (int64_t)src * d);
   const int n4 = d >> 2;
   float4 v[V];
-  // every load of the row (x and the NP partials of all V chunks) is in flight before the first add
-  float4 pp[V][NP > 0 ? NP : 1];
-#pragma unroll
-  for (int j = 0; j < V; ++j) {
-    const int i = threadIdx.x + j * 256;
-    v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int p = 0; p < NP; ++p)
-      if (i < n4) pp[j][p] = __ldcg(reinterpret_cast<const float4*>(part + (int64_t)src * d + 4 * i + p * pstride));
-  }
+  // Loads in flight before the first add: every chunk's at d <= 2048 (V * NP <= 16 float4); one chunk's
+  // at a time above that (d = 4096 / 8192), where holding all of them spilled and capped occupancy.
+  constexpr int kGroup = V * NP <= 16 ? V : 1;
   float ss = 0.f;
 #pragma unroll
-  for (int j = 0; j < V; ++j) {
-    const int i = threadIdx.x + j * 256;
-    if (NP > 0 && i < n4) {
-      float4 acc = pp[j][0];
+  for (int j0 = 0; j0 < V; j0 += kGroup) {
+    float4 pp[kGroup][NP > 0 ? NP : 1];
 #pragma unroll
-      for (int p = 1; p < NP; ++p) { acc.x += pp[j][p].x; acc.y += pp[j][p].y; acc.z += pp[j][p].z; acc.w += pp[j][p].w; }
-      v[j].x += acc.x; v[j].y += acc.y; v[j].z += acc.z; v[j].w += acc.w;
-      xr[i] = v[j];
+    for (int g = 0; g < kGroup; ++g) {
+      const int j = j0 + g, i = threadIdx.x + j * 256;
+      v[j] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int p = 0; p < NP; ++p)
+        if (i < n4) pp[g][p] = __ldcg(reinterpret_cast<const float4*>(part + (int64_t)src * d + 4 * i + p * pstride));
     }
-    ss = fmaf(v[j].x, v[j].x, ss); ss = fmaf(v[j].y, v[j].y, ss);
-    ss = fmaf(v[j].z, v[j].z, ss); ss = fmaf(v[j].w, v[j].w, ss);
+#pragma unroll
+    for (int g = 0; g < kGroup; ++g) {
+      const int j = j0 + g, i = threadIdx.x + j * 256;
+      if (NP > 0 && i < n4) {
+        float4 acc = pp[g][0];
+#pragma unroll
+        for (int p = 1; p < NP; ++p) { acc.x += pp[g][p].x; acc.y += pp[g][p].y; acc.z += pp[g][p].z; acc.w += pp[g][p].w; }
+        v[j].x += acc.x; v[j].y += acc.y; v[j].z += acc.z; v[j].w += acc.w;
+        xr[i] = v[j];
+      }
+      ss = fmaf(v[j].x, v[j].x, ss); ss = fmaf(v[j].y, v[j].y, ss);
+      ss = fmaf(v[j].z, v[j].z, ss); ss = fmaf(v[j].w, v[j].w, ss);
+    }
   }
   ss = block_sum(ss, red);
   const float inv = rsqrtf(ss / (float)d + eps);
