@@ -841,14 +841,15 @@ constexpr int kDecWarpsWhole = D == 64 ? 8 : 4;
 template <int D>
 constexpr int kDecSplitCtasPerSm = D == 64 ? 3 : 1;
 constexpr int kDecMaxG = 8;
-constexpr int kDecNS = 2;     // ring stages per warp
 constexpr int kDecKeys = 32;  // keys per chunk (one per lane)
 
 template <int D, int W>
 struct DecSmem {
   static constexpr int kTile = kDecKeys * D * 2;           // one K (or V) chunk: [D/64][32][64] bf16
   static constexpr int kStage = 2 * kTile;                 // K | V
-  static constexpr int kWarp = kDecNS * kStage;
+  // ring stages per warp: 3 for the 8-warp whole-sequence CTA at D=64 (one CTA per SM, 192 KB in flight)
+  static constexpr int kNS = (D == 64 && W == 8) ? 3 : 2;
+  static constexpr int kWarp = kNS * kStage;
   static constexpr int kRing = W * kWarp;
   static constexpr int kTotal = kRing + 1024 + 256;        // + alignment slack + barriers
 };
@@ -878,10 +879,10 @@ __global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
   const int per_chunk = kDecKeys / a.B;  // pages per chunk (B divides 32)
   const int n_chunks = (key_end - key_begin + kDecKeys - 1) / kDecKeys;
   uint8_t* wring = ring + warp * L::kWarp;
-  uint64_t* wfull = full + warp * kDecNS;
+  uint64_t* wfull = full + warp * L::kNS;
   if (lane == 0) {
     sm100::prefetch_tmap(&tm_kv);
-    for (int i = 0; i < kDecNS; ++i) sm100::mbar_init(&wfull[i], 1);
+    for (int i = 0; i < L::kNS; ++i) sm100::mbar_init(&wfull[i], 1);
     sm100::fence_barrier_init();
   }
   __syncwarp();
@@ -907,7 +908,7 @@ __global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
   const int cached_end = (start / a.B) * a.B;
   int issued = 0;
   if (lane == 0)
-    for (int c = warp; issued < kDecNS && c < n_chunks; c += W, ++issued) {
+    for (int c = warp; issued < L::kNS && c < n_chunks; c += W, ++issued) {
       if (key_begin + (c + 1) * kDecKeys > cached_end) break;
       issue(c, issued);
     }
@@ -915,7 +916,7 @@ __global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
   pdl_wait();  // q and this step's K/V row come from the kernels before
   pdl_trigger();
   if (lane == 0)
-    for (int k = issued, c = warp + issued * W; k < kDecNS && c < n_chunks; ++k, c += W) issue(c, k);
+    for (int k = issued, c = warp + issued * W; k < L::kNS && c < n_chunks; ++k, c += W) issue(c, k);
   // Q as mma.sync A fragments: row = lane/4 is query head g (rows >= G and the upper 8 rows are zero)
   const int qg = lane >> 2, qt4 = lane & 3;
   uint32_t qf[D / 16][4];
@@ -944,8 +945,8 @@ __global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
   for (int j = 0; j < D / 8; ++j) o[j][0] = o[j][1] = o[j][2] = o[j][3] = 0.f;
   int it = 0;
   for (int c = warp; c < n_chunks; c += W, ++it) {
-    const int st = it % kDecNS;
-    sm100::mbar_wait(&wfull[st], (it / kDecNS) & 1);
+    const int st = it % L::kNS;
+    sm100::mbar_wait(&wfull[st], (it / L::kNS) & 1);
     const __nv_bfloat16* sk = reinterpret_cast<const __nv_bfloat16*>(wring + st * L::kStage);
     const __nv_bfloat16* sv = sk + kDecKeys * D;
     const int c0 = key_begin + c * kDecKeys;
@@ -1006,9 +1007,9 @@ __global__ void __launch_bounds__(32 * W) attn_decode_kernel(const AttnArgs a,
     }
     // this stage is consumed: refill it with chunk c + NS*4 (generic reads -> async-proxy writes)
     __syncwarp();
-    if (lane == 0 && c + kDecNS * W < n_chunks) {
+    if (lane == 0 && c + L::kNS * W < n_chunks) {
       sm100::fence_proxy_async_smem();
-      issue(c + kDecNS * W, st);
+      issue(c + L::kNS * W, st);
     }
     __syncwarp();
   }
