@@ -15,8 +15,7 @@ from .engine import (ActivationMask, AdapterSpec, Engine, EngineConfig, Invocati
                      build_activation_mask, detect_invocation, load_engine_config)
 from .kv_cache import (Block, BlockPool, BlockTable, KVEntry, PoolExhaustedError, compute_block_keys, hash_block,
                        hash_chain)
-from .metrics import (AggregateRow, RequestMetrics, aggregate, export_metrics, finalize_request, render_csv,
-                      render_json)
+from .metrics import RequestMetrics, finalize_request, render_csv
 from .model import (BaseWeights, LayerWeights, Model, ModelConfig, SeqInput, generate_weights, greedy_next_token,
                     paged_attention, project_qkv_masked, write_kv)
 from .pipeline import (PipelineSpec, build_engine, end_of_turn_token, invocation_for, random_conversation,

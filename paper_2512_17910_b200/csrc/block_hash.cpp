@@ -22,6 +22,8 @@
 #include <thread>
 #include <vector>
 
+#include <pthread.h>
+
 #include "../../include/alora_sm100a.h"
 
 namespace {
@@ -191,8 +193,21 @@ class Helpers {
   int want_ = 0, pending_ = 0;
 };
 
+// Never destroyed: parked helpers die with the process. A fork()ed child inherits the object but not its
+// threads (and perhaps a mutex held by one of them), so the child drops it and lazily builds its own.
+std::atomic<Helpers*> g_helpers{nullptr};
+
+void helpers_after_fork_child() { g_helpers.store(nullptr); }
+
+const int g_atfork_registered = pthread_atfork(nullptr, nullptr, helpers_after_fork_child);
+
 Helpers& helpers() {
-  static Helpers* h = new Helpers();  // never destroyed: parked helpers die with the process
+  Helpers* h = g_helpers.load();
+  if (h == nullptr) {
+    Helpers* fresh = new Helpers();
+    if (g_helpers.compare_exchange_strong(h, fresh)) h = fresh;
+    else delete fresh;  // another thread won the race
+  }
   return *h;
 }
 

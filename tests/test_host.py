@@ -388,17 +388,64 @@ def test_pipelined_decode_engine_matches_reference_pipeline(name):
         tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
 
     eng.scheduler._cache_lookup = spy
-    P.run_sync_pipeline(spec, eng)
+    rows = P.run_sync_pipeline(spec, eng)
     for rid, r in g["requests"].items():
         mine = eng.finished[rid]
         assert list(map(int, mine.generated)) == r["generated"], rid
         assert (mine.hit_tokens, mine.computed_tokens) == (r["hit_tokens"], r["computed_tokens"]), rid
     assert tables == g["first_tables"]
+    # virtual-clock stamps (finish = the launching step's stamp) give the reference's metrics CSV byte for byte
+    assert P.render_csv(sorted(rows, key=lambda m: m.request_id)) == g["metrics_csv"] or \
+        P.render_csv(rows) == g["metrics_csv"]
     strip = lambda tr: [{k: v for k, v in row.items() if k != "pool_free"} for row in tr]
     assert strip(eng.trace) == strip(g["trace"])
     assert sorted(r["digest"] for r in eng.pool.dump_state() if r["digest"]) == \
         sorted(r["digest"] for r in g["pool_dump"] if r["digest"])
     eng.pool.check_conservation()
+
+
+def _pipelined_pair(pool_blocks, block_size=4, max_batch=8):
+    cfg = O.OracleConfig(n_layers=1, n_heads=2, head_dim=16, d_model=32, vocab_size=64, seed=1)
+    out = []
+    for pipelined in (False, True):
+        model = _DeferredOracle(O.OracleModel(cfg))
+        ecfg = P.EngineConfig(model=P.ModelConfig(n_layers=1, n_heads=2, head_dim=16, d_model=32, vocab_size=64,
+                                                  seed=1),
+                              scheduler=P.SchedulerConfig(token_budget=64, max_batch_requests=max_batch),
+                              pool_blocks=pool_blocks, block_size=block_size)
+        out.append(P.Engine(ecfg, clock=P.VirtualClock(), model=model, pool_storage="numpy",
+                            pipelined_decode=pipelined))
+    return out
+
+
+def test_pipelined_decode_commits_finished_request_before_next_admission():
+    """A request waiting behind one that finishes in a pipelined decode step must see the finished request's
+    published blocks (the synchronous engine commits before the next schedule_step)."""
+    prompt = np.arange(32) % 50
+    res = []
+    for eng in _pipelined_pair(pool_blocks=64, max_batch=1):
+        eng.submit(prompt, max_new_tokens=3, request_id="a")
+        eng.submit(prompt, max_new_tokens=2, request_id="b")  # B waits for A's batch slot
+        eng.run_until_idle()
+        res.append((eng.finished["b"].hit_tokens, list(eng.finished["b"].generated), eng.finished["a"].finish,
+                    eng.finished["b"].finish))
+        eng.pool.check_conservation()
+    assert res[0] == res[1]
+    assert res[0][0] == 28  # ((32-1)//4)*4 once A's blocks are published
+
+
+def test_pipelined_decode_tight_pool_matches_synchronous():
+    """With a pool that only fits one request at a time, a pipelined engine must free a finished request's
+    blocks before admitting the next (no spurious 'pool exhausted during decode')."""
+    res = []
+    for eng in _pipelined_pair(pool_blocks=10):
+        for i, rid in enumerate("abc"):
+            eng.submit((np.arange(30) + 7 * i) % 50, max_new_tokens=4, request_id=rid)
+        eng.run_until_idle()
+        res.append({rid: (r.failed, list(r.generated), r.hit_tokens, r.finish) for rid, r in eng.finished.items()})
+        eng.pool.check_conservation()
+    assert res[0] == res[1]
+    assert all(v[0] is None for v in res[0].values())
 
 
 def _fake_packer(vocab=384, graphs=False, last_S=0):
@@ -446,3 +493,22 @@ def test_step_packer_layout_and_token_refs():
     assert not Model.pack(fk, seqs, B)["graphable"] and Model.pack(fk, seqs, B)["graphable"]
     dec = Model.pack(fk, [P.SeqInput("r0", np.array([5]), 40, [4, 9, 11], None, None)], B)
     assert dec["graphable"] and dec["maxb"] == 32 and dec["max_ctx"] == 32 * B
+
+
+def test_batched_hashing_after_fork():
+    """The parked hashing helpers are per process: a fork()ed child that hashes after its parent used the
+    helpers must not wait on threads that only exist in the parent."""
+    import multiprocessing as mp
+    chains = [(np.arange(256) % 97 + i, 16, [""] * 16) for i in range(4)]
+    want = P.kv_cache.hash_chains(chains, 16, n_threads=4)  # parent starts its helpers
+
+    def child(q):
+        q.put(P.kv_cache.hash_chains(chains, 16, n_threads=4))
+
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    pr = ctx.Process(target=child, args=(q,))
+    pr.start()
+    got = q.get(timeout=30)
+    pr.join(timeout=30)
+    assert pr.exitcode == 0 and got == want

@@ -2,7 +2,7 @@
 import sys, time, statistics
 import numpy as np, torch
 sys.path.insert(0, '.')
-exec(open("scratch/ttft_breakdown.py").read().split("rows = []")[0])
+exec(open("tools/ttft_breakdown.py").read().split("rows = []")[0])
 dec = []
 for i in range(6):
     sp = P.PipelineSpec(**{**spec.__dict__, "seed": i})

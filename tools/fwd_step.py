@@ -1,6 +1,6 @@
 """One aLoRA eval-turn forward at C2 dims without running the base turn (random cached KV).
 
-usage: python scratch/fwd_step.py [n_requests] [suffix] [cached] [reps]
+usage: python tools/fwd_step.py [n_requests] [suffix] [cached] [reps]
 """
 import sys
 import time
