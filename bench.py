@@ -1,31 +1,41 @@
 #!/usr/bin/env python
-"""bench.py — aLoRA-turn TTFT & E2E vs standard-LoRA recompute, prefill tok/s (BASELINE.json metric).
+"""bench.py -- aLoRA-turn TTFT & E2E vs standard-LoRA recompute, prefill tok/s (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], C2): Llama-3.2-1B geometry (16 layers, d 2048,
-32 q / 8 kv heads, head_dim 64, SwiGLU 8192, vocab 128256, tied lm_head), bf16,
-random-init weights in HBM, 3 activated adapters r=32 on q/k/v, the reference's
-multi_adapter turn algebra (bench.py:1-21): base turn (x=1792 prompt, y=256
-generated) -> eval turn on all 3 adapters (conv + 3-token invocation, 16
-generated tokens) per pipeline instance, `--batch` instances per step, B=16,
-token budget 8192, 2k context. The same turns run twice, in aLoRA mode
-(base-aligned reuse of the 2048 cached tokens) and LoRA mode (full recompute).
+Default workload (--config c3, BASELINE.json configs[2], the north-star configuration): Llama-3-8B
+geometry (32 layers, d 4096, 32 q / 8 kv heads, head_dim 128, SwiGLU 14336, vocab 128256, tied
+lm_head), bf16, random-init weights in HBM, 8 activated adapters r=32 on q/k/v, the reference's
+multi_adapter turn algebra (reference bench.py:1-21, 245-306): per pipeline instance a base turn
+(x = 7932 prompt tokens, y = 256 generated) then an eval turn on all 8 adapters (conversation + EOT +
+3-token invocation = 8k context, 16 generated tokens). 8 instances per replica -> 64 concurrent eval
+requests, B=16, token budget 8192. The same turns run in aLoRA mode (base-aligned reuse of the
+8,176 cached tokens per request) and in LoRA mode (full recompute). --config c2 is configs[1]
+(Llama-3.2-1B, 3 adapters, 4 instances, 2k context).
 
-One timed "step" = the aLoRA eval turn's TTFT-defining forward (all 3*batch
-suffix prefills in one packed varlen step), replayed with its metadata staged
-in HBM; value = eval prompt tokens served per second of that forward
-("effective prefill": cached + computed prompt tokens / TTFT forward time).
-`e2e` = the same metric through the public Engine API (host prompts, per-step
-H2D of packed metadata and D2H of ids), over the turn's wall-clock TTFT.
-Whole-turn TTFT/E2E for both modes and their ratio are in "alora"/"lora"/"speedup".
+One timed "step" = the aLoRA eval turn's TTFT-defining forward (all eval requests' suffix prefills
+in one packed varlen step), replayed with its metadata staged in HBM; `value` = eval prompt tokens
+served per second of that forward ("effective prefill": cached + computed prompt tokens / forward
+time), summed over replicas with the max time over ranks. `e2e` = the same metric through the public
+Engine API (host prompts, per-step H2D of the packed metadata and D2H of the ids) over the turn's
+TTFT from the engine's WallClock stamps (reference metrics.py:69-73). Whole-turn TTFT / E2E for both
+modes and their ratio are in "alora" / "lora" / "speedup_vs_lora" (reference bench.py:422-435,
+525-551).
 
---impl reference times the reference algorithm on the host CPU: the numpy
-oracle (oracle/model_oracle.py, fp64 accumulation like aloraserve) running one
-aLoRA eval request's suffix forward over a 2048-token cached prefix at C2 dims.
+--gpus N (N > 1) without torchrun re-launches itself under torch.distributed.run, one process per
+GPU: N request-parallel replicas (replicas.py; pipeline instance i on replica i mod N, no data-path
+collective), `scaling` weak (each replica serves the config's instances).
+
+--impl reference times the reference algorithm on the host CPU: the numpy oracle
+(oracle/model_oracle.py, fp64 accumulation like aloraserve model.py:95-98) running one aLoRA eval
+request's suffix forward over its cached prefix at the config's dims. A full-depth 8B forward does
+not fit a bounded CPU sample, so 2 layers are timed and the per-layer time is extrapolated to the
+full depth ("extrapolated" in the sample string); the reference loops over spans (model.py:243), so
+one request's tok/s is the turn's.
 """
 
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -39,8 +49,19 @@ sys.path.insert(0, ROOT)
 
 METRIC = "aLoRA-turn TTFT & e2e pipeline latency vs LoRA recompute; prefill tok/s"
 UNIT = "prompt tok/s (eval turn, effective)"
-C2 = dict(arch="llama", n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64, d_model=2048, ffn_dim=8192,
-          vocab_size=128256, max_seq_len=4096, seed=0)
+LLAMA_1B = dict(arch="llama", n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64, d_model=2048, ffn_dim=8192,
+                vocab_size=128256, seed=0)
+LLAMA_8B = dict(arch="llama", n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, ffn_dim=14336,
+                vocab_size=128256, seed=0)
+CONFIGS = {
+    # BASELINE.json configs[1]: 1B + 3 adapters, 2k context, 4 instances x 3 adapters = 12 eval requests
+    "c2": dict(model=LLAMA_1B, n_adapters=3, batch=4, context=2048, name="C2: Llama-3.2-1B + 3 aLoRA adapters r=32"),
+    # BASELINE.json configs[2]: 8B + 8 adapters, 8k context, 8 instances x 8 adapters = 64 eval requests / replica
+    "c3": dict(model=LLAMA_8B, n_adapters=8, batch=8, context=8192, name="C3: Llama-3-8B + 8 aLoRA adapters r=32"),
+}
+B = 16
+BUDGET = 8192
+RANK_R = 32
 
 
 def parse():
@@ -49,21 +70,46 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--batch", type=int, default=4, help="pipeline instances per step (x3 adapters = eval requests)")
-    ap.add_argument("--prompt-len", type=int, default=1792)
-    ap.add_argument("--gen-len", type=int, default=256)
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--gen-len", type=int, default=256, help="base-turn generated tokens (y)")
     ap.add_argument("--adapter-gen", type=int, default=16)
-    ap.add_argument("--rank", type=int, default=32)
-    ap.add_argument("--lora-steps", type=int, default=2, help="timed LoRA-recompute eval turns")
+    ap.add_argument("--lora-steps", type=int, default=5, help="timed LoRA-recompute eval turns")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--profile-json", default=None, help="write per-kernel profile here")
-    ap.add_argument("--sweep", choices=["c3", "c4"], default=None,
-                    help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k); "
-                         "c3: Llama-3-8B + 8 aLoRA adapters, 64 eval requests over 8k contexts (one replica)")
+    ap.add_argument("--profile-json", default=None, help="write the per-kernel profile here")
+    ap.add_argument("--sweep", choices=["c4"], default=None,
+                    help="c4: Llama-3-8B long-context prefix-reuse sweep (aLoRA vs LoRA eval TTFT at 4k-32k)")
     ap.add_argument("--contexts", default="4096,8192,16384,32768")
+    ap.add_argument("--probe-ranks", action="store_true",
+                    help="launch plumbing check only: init the ranks (gloo without CUDA), print each replica's "
+                         "pipeline instances and n_gpus as rank 0 sees it; no model work")
     ap.add_argument("--sync-decode", action="store_true",
                     help="read every decode step's ids back before launching the next (default: pipelined decode)")
     return ap.parse_args()
+
+
+def workload(args):
+    c = CONFIGS[args.config]
+    x = c["context"] - args.gen_len - 4  # conversation + base output + EOT + 3-token invocation = context
+    cached = ((x + args.gen_len - 1) // B) * B  # base-aligned hits ((x+y-1)//B)*B, SURVEY.md Appendix B
+    return dict(c, x=x, cached=cached, suffix=c["context"] - cached)
+
+
+def config_dict(args, world):
+    """The `config` object of both arms' JSON lines (identical for the same flags and world size)."""
+    w = workload(args)
+    n_eval = w["n_adapters"] * w["batch"]
+    return {"workload": f"{w['name']}, multi_adapter pipeline (x={w['x']}, y={args.gen_len}, eval gen "
+                        f"{args.adapter_gen}), {w['batch']} instances x {w['n_adapters']} adapters per replica "
+                        f"= {n_eval} eval requests of {w['context']} tokens ({w['cached']} cached + {w['suffix']} "
+                        f"computed), B={B}, token budget {BUDGET}; metric = eval prompt tokens (cached + computed) "
+                        "per second of the TTFT-defining forward",
+            "config": args.config, "context": w["context"], "eval_requests_per_replica": n_eval,
+            "forward_rows_per_replica": n_eval * w["suffix"],
+            "parallelism": f"replicas x{world} (request-parallel, instance affinity)" if world > 1 else "1 GPU",
+            "l2": "no flush needed: every step streams the weights (>= 2.5 GB) and the cached KV, both far above "
+                  "the 126 MB L2",
+            "decode": "synchronous" if args.sync_decode else "pipelined (Engine pipelined_decode)",
+            **{k: v for k, v in w["model"].items() if k != "seed"}}
 
 
 # ------------------------------------------------------------------- clocks ---
@@ -73,8 +119,10 @@ class ClockSampler:
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, index):
-        self.index = index
+    def __init__(self, local_rank):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        ids = [v.strip() for v in vis.split(",")] if vis else None
+        self.index = ids[local_rank] if ids and local_rank < len(ids) else str(local_rank)
         self.rows = []
         self._stop = threading.Event()
         self._th = threading.Thread(target=self._run, daemon=True)
@@ -82,7 +130,7 @@ class ClockSampler:
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                out = subprocess.run(["nvidia-smi", "-i", self.index, f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
                 self.rows.append([c.strip() for c in out.stdout.strip().split(",")])
             except Exception:
@@ -101,41 +149,21 @@ class ClockSampler:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def eval_split(args, B=16):
-    """(cached, computed) prompt tokens of an aLoRA eval request: hits ((x+y-1)//B)*B, SURVEY.md Appendix B."""
-    total = args.prompt_len + args.gen_len + 4  # conversation + base output + EOT + 3-token invocation
-    cached = ((args.prompt_len + args.gen_len - 1) // B) * B
-    return cached, total - cached
-
-
-def c2_config(args, world):
-    """The workload both arms report (BASELINE.json configs[1])."""
-    return {"workload": "C2: Llama-3.2-1B geometry + 3 aLoRA adapters r=32, multi_adapter pipeline "
-                        f"(x={args.prompt_len}, y={args.gen_len}, eval gen {args.adapter_gen}), "
-                        f"{args.batch} instances x 3 adapters per eval turn, B=16, budget 8192; metric = eval "
-                        "prompt tokens (cached + computed) per second of the TTFT-defining forward",
-            "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-            "l2": "working set (2.5 GB weights + KV) exceeds the 126 MB L2; no flush needed",
-            "decode": "synchronous" if getattr(args, "sync_decode", False) else "pipelined (Engine pipelined_decode)",
-            **{k: v for k, v in C2.items() if k != "seed"}}
-
-
 # --------------------------------------------------------------- reference ---
-def oracle_c2(n_layers=None):
-    """C2 geometry in the numpy oracle; random fp32 weights (values do not change CPU time)."""
+def oracle_setup(args, n_layers=2):
+    """The config's geometry in the numpy oracle at `n_layers` depth; random fp32 weights (values do not
+    change CPU time)."""
     import oracle as O
 
-    dims = dict(C2)
-    if n_layers:
-        dims["n_layers"] = n_layers
-    cfg = O.OracleConfig(**dims, numerics="fp64acc")
+    dims = dict(workload(args)["model"], n_layers=n_layers)
+    cfg = O.OracleConfig(**dims, max_seq_len=workload(args)["context"] + 64, numerics="fp64acc")
     rng = np.random.default_rng(0)
     d, F = cfg.d_model, cfg.ffn
 
@@ -148,53 +176,63 @@ def oracle_c2(n_layers=None):
                     for _ in range(cfg.n_layers)],
          "embed": r(cfg.vocab_size, d), "final_norm": np.ones(d, np.float32), "unembed": None}
     model = O.OracleModel(cfg, w)
-    ad = O.oracle_adapter("adapter0", cfg, 32, seed=0, invocation_tokens=(cfg.vocab_size - 32,
-                                                                          cfg.vocab_size - 31, cfg.vocab_size - 30))
+    V = cfg.vocab_size
+    ad = O.oracle_adapter("adapter0", cfg, RANK_R, seed=0, invocation_tokens=(V - 32, V - 31, V - 30))
     return O, cfg, model, ad
 
 
-def cpu_sample(O, cfg, model, ad, prefix, suffix, B=16):
-    """One aLoRA eval request: suffix forward over a `prefix`-token paged cache (random KV rows). Returns seconds."""
+def cpu_sample(args, setup):
+    """One aLoRA eval request's suffix forward over its cached prefix (random KV rows), timed on the host:
+    (seconds extrapolated to the full depth, seconds measured, layers run)."""
+    O, cfg, model, ad = setup
+    w = workload(args)
+    prefix, suffix = w["cached"], w["suffix"]
     n_blocks = -(-(prefix + suffix) // B)
-    kv = np.random.default_rng(1).standard_normal((n_blocks, cfg.n_layers, 2, B, cfg.kv_width)).astype(np.float32)
+    kv = np.random.default_rng(1).standard_normal((n_blocks, cfg.n_layers, 2, B, cfg.kv_width), dtype=np.float32)
     toks = np.random.default_rng(2).integers(0, cfg.vocab_size - 32, suffix)
-    mask = np.arange(prefix, prefix + suffix) < prefix + suffix - 3  # the base path up to the invocation
+    mask = np.arange(prefix, prefix + suffix) < prefix + suffix - 3  # base path up to the invocation
     span = O.OracleSpan("r", toks, prefix, list(range(n_blocks)), ad, mask)
     t0 = time.perf_counter()
-    model.forward_step([span], kv)
-    return time.perf_counter() - t0
+    hf = model.last_hidden(span, kv)  # embed + the timed layers (model.py:263-271)
+    t1 = time.perf_counter()
+    O.mm(hf, model._unembed())  # lm_head of the last row (model.py:272), fp64 up-cast as in model.py:95-98
+    t2 = time.perf_counter()
+    full = w["model"]["n_layers"]
+    return (t2 - t1) + (t1 - t0) * full / cfg.n_layers, t2 - t0, cfg.n_layers
+
+
+def cpu_baseline_entry(args, times, layers):
+    w = workload(args)
+    t = statistics.median(times)
+    return {"value": w["context"] / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"1 aLoRA eval request per sample ({w['suffix']}-token suffix over {w['cached']} cached tokens) "
+                      f"at {args.config} widths; oracle/model_oracle.py fp64 numpy (OpenBLAS on all host cores); "
+                      f"{layers} of {w['model']['n_layers']} layers timed, per-layer time extrapolated to the full "
+                      f"depth + the measured lm_head (extrapolated); median of {len(times)}: {t:.2f} s/request"}
 
 
 def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
+    if int(os.environ.get("RANK", "0")) != 0:
         return
-    prefix, suffix = eval_split(args)
-    O, cfg, model, ad = oracle_c2()
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    setup = oracle_setup(args)
     for _ in range(args.warmup):
-        cpu_sample(O, cfg, model, ad, prefix, suffix)
-    times = [cpu_sample(O, cfg, model, ad, prefix, suffix) for _ in range(args.steps)]
-    t = statistics.mean(times)
-    value = (prefix + suffix) / t
-    cores = os.cpu_count()
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        cpu_sample(args, setup)
+    samples = [cpu_sample(args, setup) for _ in range(args.steps)]
+    times = [s[0] for s in samples]
+    cpu = cpu_baseline_entry(args, times, samples[0][2])
+    t = statistics.median(times)
+    value = workload(args)["context"] / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-            "config": c2_config(args, int(os.environ.get("WORLD_SIZE", "1"))),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                             "sample": f"1 of the turn's eval requests per step ({suffix}-token suffix over {prefix} "
-                                       "cached tokens; the reference forward loops over spans, model.py:243, so "
-                                       "tok/s per request is the turn's), oracle/model_oracle.py fp64 numpy "
-                                       "(OpenBLAS threads = cores)"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": config_dict(args, world), "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "measured_ms_per_step": 1e3 * statistics.median(s[1] for s in samples)}
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ C4 sweep ---
-C4 = dict(arch="llama", n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, ffn_dim=14336,
-          vocab_size=128256, seed=0)
-
-
 def run_sweep_c4(args):
     """BASELINE.json configs[3]: Llama-3-8B, one base->adapter pipeline per context length; the eval turn's TTFT
     with base-aligned reuse (aLoRA) vs standard-LoRA full recompute (budget 8192, chunked like vLLM)."""
@@ -203,18 +241,20 @@ def run_sweep_c4(args):
 
     torch.cuda.set_device(0)
     rows = []
+    sampler = ClockSampler(0)
+    sampler.__enter__()
     for ctx in [int(c) for c in args.contexts.split(",")]:
         y = 256
         x = ctx - y - 4
-        mcfg = P.ModelConfig(**C4, max_seq_len=ctx + 64, dtype="bf16")
-        model = P.Model(mcfg, init="device", max_tokens=8192, max_seqs=16)
+        mcfg = P.ModelConfig(**LLAMA_8B, max_seq_len=ctx + 64, dtype="bf16")
+        model = P.Model(mcfg, init="device", max_tokens=BUDGET, max_seqs=16)
         res = {"context": ctx}
         for mode in ("alora", "lora"):
             spec = P.PipelineSpec(pipeline="base_adapter", mode=mode, prompt_len=x, gen_len=y, adapter_gen_len=16,
                                   n_adapters=1, batch=1)
-            cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=8192, max_batch_requests=8),
-                                 pool_blocks=2 * (-(-(ctx + 64) // 16)) * 3 + 64, block_size=16,
-                                 adapters=(P.AdapterSpec(adapter_id="adapter0", rank=32, seed=0,
+            cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=BUDGET, max_batch_requests=8),
+                                 pool_blocks=2 * (-(-(ctx + 64) // B)) * 3 + 64, block_size=B,
+                                 adapters=(P.AdapterSpec(adapter_id="adapter0", rank=RANK_R, seed=0,
                                                          invocation_tokens=P.invocation_for(mcfg.vocab_size, 0)),),
                                  comparison_mode=mode)
             eng = P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
@@ -236,83 +276,77 @@ def run_sweep_c4(args):
                     e2e.append(r.e2e_s)
                     comp.append(r.computed_tokens)
                     base_tps.append(b.prompt_len / b.prefill_s)
-            res[mode] = {"ttft_ms": 1e3 * statistics.mean(ttft), "e2e_ms": 1e3 * statistics.mean(e2e),
+            res[mode] = {"ttft_ms_median": 1e3 * statistics.median(ttft), "ttft_ms_min": 1e3 * min(ttft),
+                         "e2e_ms_median": 1e3 * statistics.median(e2e),
                          "computed_tokens": int(statistics.mean(comp)),
-                         "base_prefill_tok_s": statistics.mean(base_tps)}
+                         "base_prefill_tok_s": statistics.median(base_tps), "turns": len(ttft)}
             del eng
             torch.cuda.empty_cache()
-        res["ttft_speedup"] = res["lora"]["ttft_ms"] / res["alora"]["ttft_ms"]
-        res["e2e_speedup"] = res["lora"]["e2e_ms"] / res["alora"]["e2e_ms"]
+        res["ttft_speedup"] = res["lora"]["ttft_ms_median"] / res["alora"]["ttft_ms_median"]
+        res["e2e_speedup"] = res["lora"]["e2e_ms_median"] / res["alora"]["e2e_ms_median"]
         rows.append(res)
         print(json.dumps(res), flush=True)
         del model
         torch.cuda.empty_cache()
+    sampler.__exit__()
     print(json.dumps({"metric": "C4 eval-turn TTFT aLoRA vs LoRA recompute (Llama-3-8B geometry, bf16, 1 B200)",
                       "config": {"workload": "base_adapter pipeline, y=256, eval gen 16, B=16, budget 8192",
-                                 **{k: v for k, v in C4.items() if k != "seed"}},
-                      "data": "synthetic (random-init weights in HBM)", "sweep": rows}), flush=True)
+                                 **{k: v for k, v in LLAMA_8B.items() if k != "seed"}},
+                      "data": "synthetic (random-init weights in HBM)", "clocks": sampler.summary(),
+                      "sweep": rows}), flush=True)
 
 
-def run_c3(args):
-    """BASELINE.json configs[2] on one replica: Llama-3-8B bf16 + 8 activated adapters (r=32), a multi_adapter
-    pipeline over 8 conversations of 8k tokens -> 64 concurrent eval requests (8 adapters x 8 instances),
-    aLoRA (base-aligned reuse) vs LoRA recompute (budget 8192). Replicas scale it weakly (replicas.py)."""
+# ------------------------------------------------------------- multi-rank ---
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(args):
+    """bench.py --gpus N run directly: one process per GPU under torch.distributed.run (127.0.0.1)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def probe_ranks(args):
     import torch
-    import paper_2512_17910_b200 as P
+    import torch.distributed as dist
+    from paper_2512_17910_b200.replicas import replica_instances
 
-    torch.cuda.set_device(0)
-    ctx, y, n_ad, batch = 8192, 256, 8, 8
-    x = ctx - y - 4
-    mcfg = P.ModelConfig(**C4, max_seq_len=ctx + 64, dtype="bf16")
-    model = P.Model(mcfg, init="device", max_tokens=8192, max_seqs=96)
-    out = {}
-    for mode in ("alora", "lora"):
-        spec = P.PipelineSpec(pipeline="multi_adapter", mode=mode, prompt_len=x, gen_len=y, adapter_gen_len=16,
-                              n_adapters=n_ad, batch=batch)
-        blocks = -(-(ctx + 64) // 16)
-        cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=8192, max_batch_requests=96),
-                             pool_blocks=(batch * (n_ad + 1) + 8) * blocks, block_size=16,
-                             adapters=tuple(P.AdapterSpec(adapter_id=f"adapter{k}", rank=32, seed=k,
-                                                          invocation_tokens=P.invocation_for(mcfg.vocab_size, k))
-                                            for k in range(n_ad)),
-                             comparison_mode=mode)
-        eng = P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
-        ph = P.pipeline.pipeline_phases(spec, eng, rid_prefix=f"{mode}-")
-        _, sub = next(ph)
-        P.pipeline.run_phase(eng, sub)
-        _, sub = next(ph)
-        torch.cuda.synchronize()
-        n0 = len(eng.metrics)
-        t0 = time.perf_counter()
-        P.pipeline.run_phase(eng, sub)
-        wall = time.perf_counter() - t0
-        rows = eng.metrics[n0:]
-        out[mode] = {"requests": len(rows), "ttft_ms_mean": 1e3 * statistics.mean(r.ttft_s for r in rows),
-                     "turn_ttft_ms": 1e3 * max(r.ttft_s for r in rows),
-                     "e2e_ms_mean": 1e3 * statistics.mean(r.e2e_s for r in rows), "turn_wall_ms": 1e3 * wall,
-                     "hit_tokens_per_request": statistics.mean(r.hit_tokens for r in rows),
-                     "computed_tokens": int(sum(r.computed_tokens for r in rows)),
-                     "eval_prompt_tok_s": sum(r.prompt_len for r in rows) / max(r.ttft_s for r in rows)}
-        del eng
-        torch.cuda.empty_cache()
-    out["turn_ttft_speedup"] = out["lora"]["turn_ttft_ms"] / out["alora"]["turn_ttft_ms"]
-    out["e2e_speedup"] = out["lora"]["e2e_ms_mean"] / out["alora"]["e2e_ms_mean"]
-    print(json.dumps({"metric": "C3 eval turn, 64 requests: TTFT/E2E aLoRA vs LoRA recompute (1 replica, 1 B200)",
-                      "config": {"workload": "multi_adapter, 8 conversations x 8 adapters, 8k context, y=256, "
-                                             "eval gen 16, B=16, budget 8192",
-                                 **{k: v for k, v in C4.items() if k != "seed"}},
-                      "data": "synthetic (random-init weights in HBM)", **out}), flush=True)
+    world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    w = workload(args)
+    mine = replica_instances(w["batch"] * world, world, rank)
+    every = [None] * world
+    if world > 1:
+        dist.all_gather_object(every, mine)
+    else:
+        every = [mine]
+    if rank == 0:
+        print(json.dumps({"probe": "ranks", "n_gpus": world, "instances_per_rank": every,
+                          "eval_requests_total": sum(len(m) for m in every) * w["n_adapters"],
+                          "config": config_dict(args, world)}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 # --------------------------------------------------------------------- ours ---
 def main():
     args = parse()
-    if args.impl == "reference":
-        return run_reference(args)
     if args.sweep == "c4":
         return run_sweep_c4(args)
-    if args.sweep == "c3":
-        return run_c3(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        if args.impl == "reference":  # the CPU arm runs once (rank 0); no ranks to spawn
+            os.environ["WORLD_SIZE"] = str(args.gpus)
+        else:
+            sys.exit(relaunch_under_torchrun(args))
+    if args.impl == "reference":
+        return run_reference(args)
+    if args.probe_ranks:
+        return probe_ranks(args)
     import torch
     import torch.distributed as dist
 
@@ -321,57 +355,62 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_2512_17910_b200 as P
+    from paper_2512_17910_b200.replicas import replica_instances
 
-    mcfg = P.ModelConfig(**C2, dtype="bf16")
-    n_eval = 3
-    B = 16
-    budget = 8192
-    peak_tokens = args.prompt_len + args.gen_len + 1 + 3 + args.adapter_gen
-    pool_blocks = max(4096, 2 * args.batch * (1 + n_eval) * (-(-peak_tokens // B)) + 64)
+    w = workload(args)
+    mcfg = P.ModelConfig(**w["model"], max_seq_len=w["context"] + args.adapter_gen + 64, dtype="bf16")
+    n_eval = w["n_adapters"]
+    blocks = -(-(w["context"] + args.adapter_gen) // B)
+    # the LoRA arm recomputes every eval request (its own blocks) while the base turn's blocks stay cached
+    pool_blocks = (w["batch"] * (n_eval + 1) + 8) * blocks
+    max_batch = n_eval * w["batch"] + 8
+    model = P.Model(mcfg, init="device", max_tokens=BUDGET, max_seqs=max_batch)
+    mine = replica_instances(w["batch"] * world, world, rank)  # this replica's pipeline instances
 
     def make_engine(mode):
-        spec = P.PipelineSpec(pipeline="multi_adapter", mode=mode, prompt_len=args.prompt_len, gen_len=args.gen_len,
-                              adapter_gen_len=args.adapter_gen, n_adapters=n_eval, batch=args.batch)
-        cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=budget,
-                                                                        max_batch_requests=4 * n_eval * args.batch + 8),
+        spec = P.PipelineSpec(pipeline="multi_adapter", mode=mode, prompt_len=w["x"], gen_len=args.gen_len,
+                              adapter_gen_len=args.adapter_gen, n_adapters=n_eval, batch=w["batch"] * world)
+        cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=BUDGET, max_batch_requests=max_batch),
                              pool_blocks=pool_blocks, block_size=B,
-                             adapters=tuple(P.AdapterSpec(adapter_id=f"adapter{k}", rank=args.rank, seed=k,
+                             adapters=tuple(P.AdapterSpec(adapter_id=f"adapter{k}", rank=RANK_R, seed=k,
                                                           invocation_tokens=P.invocation_for(mcfg.vocab_size, k))
                                             for k in range(n_eval)),
                              comparison_mode=mode)
-        model = P.Model(mcfg, init="device", max_tokens=budget, max_seqs=cfg.scheduler.max_batch_requests)
         return spec, P.Engine(cfg, clock=P.WallClock(), model=model, pipelined_decode=not args.sync_decode)
 
-    # instrument the engine: capture the eval turn's first packed step and count native launches
     class Spy:
+        """Captures the eval turn's first packed step and counts native launches / copies."""
+
         def __init__(self, model):
-            self.model, self.first, self.launches, self.h2d, self.d2h, self.armed = model, None, 0, 0, 0, False
-            orig = model.run_packed
+            self.first, self.launches, self.h2d, self.d2h, self.armed = None, 0, 0, 0, False
+            self.orig_run, self.orig_async = model.run_packed, model.launch_async
 
             def wrapped(p, kv, want_logits=True):
-                out = orig(p, kv, want_logits)
+                out = self.orig_run(p, kv, want_logits)
                 if self.armed:
                     if self.first is None:
                         self.first = p
                         self.h2d, self.d2h = model.last_h2d_bytes, model.last_d2h_bytes
                     self.launches += model.last_launches
                 return out
-            model.run_packed = wrapped
-            orig_async = model.launch_async
 
             def wrapped_async(p, kv):  # pipelined decode steps count too
-                out = orig_async(p, kv)
+                out = self.orig_async(p, kv)
                 if self.armed:
                     self.launches += model.last_launches
                 return out
-            model.launch_async = wrapped_async
+            model.run_packed, model.launch_async = wrapped, wrapped_async
+
+        def detach(self):
+            model.run_packed, model.launch_async = self.orig_run, self.orig_async
 
     def run_turns(engine, spec, step_idx, spy, timed):
-        """Base turn (untimed) then the eval turn; returns eval rows and the turn's wall/device times."""
-        spec_i = P.PipelineSpec(**{**spec.__dict__, "seed": 1000 * rank + step_idx})
-        phases = P.pipeline.pipeline_phases(spec_i, engine, rid_prefix=f"s{step_idx}-")
+        """Base turn (untimed) then the eval turn; returns (base rows, eval rows, eval requests, wall s)."""
+        spec_i = P.PipelineSpec(**{**spec.__dict__, "seed": 1000 + step_idx})
+        phases = P.pipeline.pipeline_phases(spec_i, engine, rid_prefix=f"s{step_idx}-", instances=mine)
         stage, submits = next(phases)
         assert stage == "base"
         n0 = len(engine.metrics)
@@ -384,94 +423,91 @@ def main():
             dist.barrier()
         spy.armed, spy.first, spy.launches = timed, None, 0
         n0 = len(engine.metrics)
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record()
         t0 = time.perf_counter()
         P.pipeline.run_phase(engine, submits)
-        ev1.record()
         torch.cuda.synchronize()
         wall = time.perf_counter() - t0
         spy.armed = False
-        return base_rows, engine.metrics[n0:], wall, ev0.elapsed_time(ev1) / 1e3
+        rows = engine.metrics[n0:]
+        return base_rows, rows, [engine.finished[r.request_id] for r in rows], wall
+
+    def turn_stats(turns):
+        """turns: [(eval rows, eval requests, wall)] of the timed eval turns."""
+        ttft = [r.ttft_s for rows, _, _ in turns for r in rows]
+        turn_ttft = [max(r.ttft_s for r in rows) for rows, _, _ in turns]
+        e2e = [r.e2e_s for rows, _, _ in turns for r in rows]
+        comp = sum(r.prompt_len - r.hit_tokens for rows, _, _ in turns for r in rows)
+        hit = sum(r.hit_tokens for rows, _, _ in turns for r in rows)
+        # prefill tok/s over the turn's prefill wall time: computed prompt tokens / (last prefill end - first start)
+        pf = [sum(q.prompt_len - q.hit_tokens for q in reqs) /
+              max(1e-9, max(q.decode_start for q in reqs) - min(q.prefill_start for q in reqs))
+              for _, reqs, _ in turns]
+        return {"turns": len(turns), "requests_per_turn": len(turns[0][0]),
+                "ttft_ms_mean": 1e3 * statistics.mean(ttft), "turn_ttft_ms_median": 1e3 * statistics.median(turn_ttft),
+                "turn_ttft_ms_min": 1e3 * min(turn_ttft), "e2e_ms_mean": 1e3 * statistics.mean(e2e),
+                "e2e_ms_median": 1e3 * statistics.median(e2e),
+                "turn_wall_ms_median": 1e3 * statistics.median(wl for _, _, wl in turns),
+                "hit_rate": hit / max(1, hit + comp), "hit_tokens_per_request": hit / max(1, len(ttft)),
+                "computed_prompt_tokens_per_turn": comp // len(turns),
+                "prefill_tok_s": statistics.median(pf)}
 
     results = {}
-    device_value = None
     for mode in ("alora", "lora"):
         spec, eng = make_engine(mode)
-        spy = Spy(eng.model)
-        n_steps = args.steps if mode == "alora" else args.lora_steps
+        spy = Spy(model)
+        n_steps = args.steps if mode == "alora" else max(5, args.lora_steps)
         n_warm = args.warmup if mode == "alora" else 1
-        rows_t, walls, base_rows_all = [], [], []
-        sampler = ClockSampler(local) if mode == "alora" else None
         for i in range(n_warm):
             run_turns(eng, spec, i, spy, timed=False)
-        if sampler:
-            sampler.__enter__()
+        sampler = ClockSampler(local).__enter__()
+        turns, base_tps = [], []
         for i in range(n_steps):
-            base_rows, rows, wall, dev = run_turns(eng, spec, n_warm + i, spy, timed=True)
-            rows_t.append(rows)
-            walls.append((wall, dev))
-            base_rows_all.append(base_rows)
-        launches = spy.launches
-        first = spy.first
-        res = {"rows": rows_t, "walls": walls, "base": base_rows_all, "launches": launches, "h2d": spy.h2d,
-               "d2h": spy.d2h}
+            base_rows, rows, reqs, wall = run_turns(eng, spec, n_warm + i, spy, timed=True)
+            turns.append((rows, reqs, wall))
+            breqs = [eng.finished[r.request_id] for r in base_rows]
+            base_tps.append(sum(q.prompt_len for q in breqs) /
+                            max(1e-9, max(q.decode_start for q in breqs) - min(q.prefill_start for q in breqs)))
+        res = {"stats": turn_stats(turns), "base_prefill_tok_s": statistics.median(base_tps),
+               "e2e_launches": spy.launches, "h2d": spy.h2d, "d2h": spy.d2h}
         if mode == "alora":
             # device-resident replay of the TTFT-defining forward (metadata staged in HBM before the events)
-            m = eng.model
-            st = m.stage(first, eng.pool.kv)
+            first = spy.first
+            st = model.stage(first, eng.pool.kv)
             for _ in range(args.warmup):
-                m.launch(st)
+                model.launch(st)
             torch.cuda.synchronize()
-            times = []
+            if world > 1:
+                dist.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
             for _ in range(args.steps):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                m.launch(st)
-                e1.record()
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1) / 1e3)
-            sampler.__exit__()
-            res["clocks"] = sampler.summary()
-            res["forward_s"] = statistics.mean(times)
-            res["prompt_tokens"] = int(sum(r.prompt_len for r in rows_t[0]))
-            res["fwd_rows"] = int(first["M"])
-            res["fwd_launches"] = m.last_launches
-            # per-kernel profile of the same forward (separate pass, not the timed one)
-            m.set_profiling(True)
-            m.launch(st)
+                model.launch(st)
+            e1.record()
             torch.cuda.synchronize()
-            res["profile"] = m.profile_read()
-            m.set_profiling(False)
+            res["forward_s"] = e0.elapsed_time(e1) / 1e3 / args.steps
+            res["prompt_tokens"] = int(sum(r.prompt_len for r in turns[0][0]))
+            res["fwd_rows"] = int(first["M"])
+            res["fwd_launches"] = model.last_launches
+            # per-kernel profile of the same forward (a separate, event-bracketed pass; not the timed one)
+            model.set_profiling(True)
+            model.launch(st)
+            torch.cuda.synchronize()
+            res["profile"] = model.profile_read()
+            res["kernels_launched"] = model.profile_kernels()
+            model.set_profiling(False)
+        sampler.__exit__()
+        res["clocks"] = sampler.summary()
         results[mode] = res
+        spy.detach()
         del eng, spy
         torch.cuda.empty_cache()
 
-    def turn_stats(res):
-        ttft = [r.ttft_s for rows in res["rows"] for r in rows]
-        e2e = [r.e2e_s for rows in res["rows"] for r in rows]
-        turn_ttft = [max(r.ttft_s for r in rows) for rows in res["rows"]]
-        comp = sum(r.computed_tokens for rows in res["rows"] for r in rows)
-        hit = sum(r.hit_tokens for rows in res["rows"] for r in rows)
-        prefill = [r.prefill_s for rows in res["rows"] for r in rows]
-        return {"ttft_ms_mean": 1e3 * statistics.mean(ttft), "turn_ttft_ms": 1e3 * statistics.mean(turn_ttft),
-                "e2e_ms_mean": 1e3 * statistics.mean(e2e), "turn_wall_ms": 1e3 * statistics.mean(w for w, _ in res["walls"]),
-                "hit_rate": hit / (hit + comp), "hit_tokens_per_request": hit / sum(len(r) for r in res["rows"]),
-                "computed_tokens": comp,
-                "prefill_tok_s": sum(r.prompt_len - r.hit_tokens for rows in res["rows"] for r in rows)
-                / max(1e-9, sum(max(r.prefill_s for r in rows) for rows in res["rows"]))}
-
-    a, l = turn_stats(results["alora"]), turn_stats(results["lora"])
-    # base turn: all instances' prompts prefill together; tok/s = prompt tokens / slowest prefill, per step
-    base_prefill_tok_s = statistics.mean(sum(r.prompt_len for r in rows) / max(r.prefill_s for r in rows)
-                                         for rows in results["alora"]["base"])
+    a, l = results["alora"]["stats"], results["lora"]["stats"]
     ra = results["alora"]
-    tokens = ra["prompt_tokens"]
-    fwd = ra["forward_s"]
-    turn_ttft_s = a["turn_ttft_ms"] / 1e3
-    # aggregate over ranks (replicas): tokens summed, times max
+    tokens, fwd = ra["prompt_tokens"], ra["forward_s"]
+    turn_ttft_s = a["turn_ttft_ms_median"] / 1e3
     vals = torch.tensor([tokens, fwd, turn_ttft_s], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if world > 1:  # aggregate over replicas: tokens summed, times max
         tok_sum = vals[0:1].clone()
         dist.all_reduce(tok_sum, op=dist.ReduceOp.SUM)
         tmax = vals[1:].clone()
@@ -513,18 +549,14 @@ def main():
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(dom)
+            traffic = json.load(f).get(args.config, {}).get(dom)
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            O, ocfg, om, oad = oracle_c2()
-            prefix, suffix = eval_split(args)
-            cpu_sample(O, ocfg, om, oad, prefix, suffix)
-            t = min(cpu_sample(O, ocfg, om, oad, prefix, suffix) for _ in range(2))
-            cpu = {"value": (prefix + suffix) / t, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
-                   "sample": f"1 aLoRA eval request ({suffix}-token suffix over {prefix} cached tokens) at C2 dims, "
-                             f"oracle/model_oracle.py fp64 numpy, best of 2 after 1 warm-up: {t:.2f} s"}
+            setup = oracle_setup(args)
+            samples = [cpu_sample(args, setup) for _ in range(2)]
+            cpu = cpu_baseline_entry(args, [s[0] for s in samples], samples[0][2])
         except Exception as e:  # the CPU leg must not sink the GPU line
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "port", "sample": f"failed: {e}"}
 
@@ -533,28 +565,33 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": fwd_max * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights in HBM, random conversations)",
-        "config": {**c2_config(args, world), "eval_requests_per_step": int(tokens / (args.prompt_len + args.gen_len + 4)),
-                   "forward_rows": ra["fwd_rows"]},
+        "config": config_dict(args, world),
         "e2e": {"value": tokens_all / ttft_max, "unit": UNIT, "h2d_bytes_per_step": ra["h2d"],
                 "d2h_bytes_per_step": ra["d2h"],
-                "how": "Engine.submit/run_until_idle (public API), turn TTFT from the engine's WallClock stamps"},
+                "how": "Engine.submit/run_until_idle (public API) from host prompts; median turn TTFT (slowest "
+                       "request's queue + prefill) from the engine's WallClock stamps over the timed eval turns"},
         "alora": a, "lora": l,
-        "speedup_vs_lora": {"ttft_mean": l["ttft_ms_mean"] / a["ttft_ms_mean"], "turn_ttft": l["turn_ttft_ms"] / a["turn_ttft_ms"],
-                            "e2e_mean": l["e2e_ms_mean"] / a["e2e_ms_mean"]},
-        "base_turn_prefill_tok_s": base_prefill_tok_s,
+        "speedup_vs_lora": {"ttft_mean": l["ttft_ms_mean"] / a["ttft_ms_mean"],
+                            "turn_ttft_median": l["turn_ttft_ms_median"] / a["turn_ttft_ms_median"],
+                            "e2e_median": l["e2e_ms_median"] / a["e2e_ms_median"]},
+        "base_turn_prefill_tok_s": ra["base_prefill_tok_s"],
         "lora_recompute_prefill_tok_s": l["prefill_tok_s"],
         "roofline": {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
                      "frac": achieved / peak, "traffic": traffic,
-                     "basis": "algorithmic bytes/flops per launch (runtime.cu tags) / CUDA-event launch time",
+                     "basis": "algorithmic bytes/flops per launch (runtime.cu tags, DESIGN.md §4) / CUDA-event "
+                              "launch time on the launch stream",
                      "peak_source": "MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback"},
         "kernels": kernels,
         "cpu_baseline": cpu,
         "clocks": ra["clocks"],
-        "gpu_launches": ra["launches"],
+        "clocks_lora_arm": results["lora"]["clocks"],
+        "gpu_launches": ra["fwd_launches"] * args.steps,
+        "gpu_launches_e2e_turn": ra["e2e_launches"],
     }
     if args.profile_json:
         with open(args.profile_json, "w") as f:
-            json.dump({"kernels": kernels, "alora": a, "lora": l}, f, indent=1)
+            json.dump({"kernels": kernels, "kernels_launched": ra["kernels_launched"], "alora": a, "lora": l}, f,
+                      indent=1)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

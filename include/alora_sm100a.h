@@ -262,6 +262,11 @@ int32_t alora_model_last_launches(void* handle);
 int alora_model_set_profiling(void* handle, int32_t enable);
 int alora_model_profile_read(void* handle, int32_t max_kinds, char* names, float* ms, int32_t* counts,
                              double* bytes, double* flops);
+/* The kernels behind the profiled launches: one text line per distinct (kind, kernel, grid),
+ * "kind<TAB>demangled kernel name<TAB>grid CTAs<TAB>launches\n", NUL-terminated into buf (cap bytes).
+ * Returns the size the full text needs (call with buf = NULL to size it). Tests use it to assert
+ * which kernel variant (tile width, split count, decode/prefill attention) served a step. */
+int64_t alora_model_profile_kernels(void* handle, char* buf, int64_t cap);
 
 #ifdef __cplusplus
 }

@@ -179,7 +179,7 @@ def oracle_adapter(adapter_id, cfg: OracleConfig, rank, seed=0, targets=("q", "k
 
 def mm(a, b) -> np.ndarray:
     """fp64 accumulation, one rounding to fp32 (model.py:95-98)."""
-    return (np.asarray(a).astype(np.float64) @ np.asarray(b).astype(np.float64)).astype(np.float32)
+    return (np.asarray(a).astype(np.float64, copy=False) @ np.asarray(b).astype(np.float64, copy=False)).astype(np.float32)
 
 
 def rmsnorm(x, weight=None, eps: float = 1e-6) -> np.ndarray:
@@ -240,14 +240,14 @@ def project_qkv_masked(x, wq, wk, wv, adapter: OracleAdapter | None = None, mask
     out = []
     for name in ("q", "k", "v"):
         w = bases[name]
-        base64 = x.astype(np.float64) @ np.asarray(w).astype(np.float64)
+        base64 = x.astype(np.float64) @ np.asarray(w).astype(np.float64, copy=False)
         base = base64.astype(np.float32)
         if adapter is None or name not in adapter.targets:
             out.append(base)
             continue
         if bf16:
             s = bf16_round(mm(x, adapter.down[name]))
-            adapted = (base64 + s.astype(np.float64) @ adapter.up[name].astype(np.float64)).astype(np.float32)
+            adapted = (base64 + s.astype(np.float64) @ adapter.up[name].astype(np.float64, copy=False)).astype(np.float32)
         else:
             adapted = base + mm(mm(x, adapter.down[name]), adapter.up[name])
         if mask is None:
@@ -279,6 +279,18 @@ def paged_attention(q, kv, layer, block_ids, fresh_k, fresh_v, start_pos, n_head
     else:
         keys, vals = np.asarray(fresh_k), np.asarray(fresh_v)
     group = n_heads // hkv
+    if group > 1:  # GQA (llama mode, no reference counterpart): the same math batched per kv head, no K/V repeat
+        qg = q.astype(np.float64).reshape(n, hkv, group, hd).transpose(1, 2, 0, 3).reshape(hkv, group * n, hd)
+        kg = np.asarray(keys, np.float64).reshape(total, hkv, hd).transpose(1, 2, 0)
+        vg = np.asarray(vals, np.float64).reshape(total, hkv, hd).transpose(1, 0, 2)
+        sc = (qg @ kg / np.sqrt(hd)).reshape(hkv, group, n, total)
+        qpos = start_pos + np.arange(n)[:, None]
+        sc = np.where(np.arange(total)[None, :] <= qpos, sc, -np.inf)
+        sc -= sc.max(axis=-1, keepdims=True)
+        w = np.exp(sc)
+        w /= w.sum(axis=-1, keepdims=True)
+        ctx = (w.reshape(hkv, group * n, total) @ vg).reshape(hkv, group, n, hd).transpose(2, 0, 1, 3)
+        return ctx.reshape(n, dq).astype(np.float32)
     q64 = q.astype(np.float64).reshape(n, n_heads, hd)
     k64 = np.repeat(np.asarray(keys, np.float64).reshape(total, hkv, hd), group, axis=1)
     v64 = np.repeat(np.asarray(vals, np.float64).reshape(total, hkv, hd), group, axis=1)
@@ -350,14 +362,39 @@ class OracleModel:
         if cfg.arch == "llama":
             self.cos, self.sin = rope_tables(cfg.max_seq_len, cfg.head_dim, cfg.rope_theta)
 
+    def to_f64(self):
+        """Hold every GEMM weight as float64 (exact: the values are fp32/bf16) so repeated forwards skip the
+        per-call up-cast of model.py:95-98. Same results; for large test geometries only."""
+        for layer in self.w["layers"]:
+            for k in list(layer):
+                if not k.endswith("_norm"):
+                    layer[k] = np.asarray(layer[k]).astype(np.float64)
+        for k in ("embed", "unembed"):
+            if self.w.get(k) is not None:
+                self.w[k] = np.asarray(self.w[k]).astype(np.float64)
+        return self
+
     def new_pool(self, total_blocks, block_size):
         c = self.cfg
         return np.zeros((total_blocks, c.n_layers, 2, block_size, c.kv_width), np.float32)
 
-    def forward_step(self, seqs, kv) -> dict:
-        return {s.request_id: self.forward_one(s, kv) for s in seqs}
+    def forward_step(self, seqs, kv, batch_head: bool = False) -> dict:
+        """batch_head=True runs the lm_head once over every span's last row (the same per-row fp64 math as
+        model.py:272; for large vocabularies in tests) instead of once per span."""
+        if not batch_head:
+            return {s.request_id: self.forward_one(s, kv) for s in seqs}
+        hf = np.concatenate([self.last_hidden(s, kv) for s in seqs])
+        logits = mm(hf, self._unembed())
+        return {s.request_id: logits[i] for i, s in enumerate(seqs)}
+
+    def _unembed(self):
+        return self.w["unembed"] if self.w.get("unembed") is not None else self.w["embed"].T
 
     def forward_one(self, seq: OracleSpan, kv) -> np.ndarray:
+        return mm(self.last_hidden(seq, kv), self._unembed())[0]
+
+    def last_hidden(self, seq: OracleSpan, kv) -> np.ndarray:
+        """Every layer of model.py:263-271 for one span (KV written into kv); the final-normed last row."""
         c = self.cfg
         bf = c.numerics == "bf16"
         rb = bf16_round if bf else (lambda a: np.asarray(a, np.float32))
@@ -374,7 +411,7 @@ class OracleModel:
             mask = seq.mask
         positions = np.arange(seq.start_pos, seq.start_pos + n)
         if c.arch == "ref":
-            x = self.w["embed"][tokens] + self.positions[seq.start_pos:seq.start_pos + n]
+            x = self.w["embed"][tokens].astype(np.float32, copy=False) + self.positions[seq.start_pos:seq.start_pos + n]
         else:
             x = self.w["embed"][tokens].astype(np.float32)
         for li, L in enumerate(self.w["layers"]):
@@ -386,7 +423,7 @@ class OracleModel:
             q, k, v = rb(q), rb(k), rb(v)
             write_kv(kv, li, seq.block_ids, seq.start_pos, k, v)
             attn = rb(paged_attention(q, kv, li, seq.block_ids, k, v, seq.start_pos, c.n_heads, c.kv_heads))
-            x = (x.astype(np.float64) + attn.astype(np.float64) @ L["wo"].astype(np.float64)).astype(np.float32) \
+            x = (x.astype(np.float64) + attn.astype(np.float64) @ L["wo"].astype(np.float64, copy=False)).astype(np.float32) \
                 if bf else x + mm(attn, L["wo"])
             h2 = rb(rmsnorm(x, L.get("mlp_norm"), c.rms_eps))
             if c.arch == "ref":
@@ -397,8 +434,6 @@ class OracleModel:
                 u = mm(h2, L["w_up"]).astype(np.float64)
                 a = rb((g / (1.0 + np.exp(-g)) * u).astype(np.float32))
                 w_down = L["w_down"]
-            x = (x.astype(np.float64) + a.astype(np.float64) @ w_down.astype(np.float64)).astype(np.float32) \
+            x = (x.astype(np.float64) + a.astype(np.float64) @ w_down.astype(np.float64, copy=False)).astype(np.float32) \
                 if bf else x + mm(a, w_down)
-        hf = rb(rmsnorm(x[-1:], self.w.get("final_norm"), c.rms_eps))
-        unembed = self.w["unembed"] if self.w.get("unembed") is not None else self.w["embed"].T
-        return mm(hf, unembed)[0]
+        return rb(rmsnorm(x[-1:], self.w.get("final_norm"), c.rms_eps))

@@ -128,6 +128,7 @@ EXPORTS = {
     "alora_model_set_profiling": _sig("alora_model_set_profiling", c_i32, c_void_p, c_i32),
     "alora_model_profile_read": _sig("alora_model_profile_read", c_i32, c_void_p, c_i32, c_void_p, c_void_p,
                                      c_void_p, c_void_p, c_void_p),
+    "alora_model_profile_kernels": _sig("alora_model_profile_kernels", c_i64, c_void_p, c_void_p, c_i64),
 }
 
 

@@ -1,6 +1,8 @@
 // Shared helpers for the sm_100a kernels of libalora_sm100a.so.
 #pragma once
 
+#include <vector>
+
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -51,10 +53,22 @@ inline bool pdl_on() {
   return on;
 }
 
+// Launch log (profiling only): while the executor profiles, every kernel launched through launch_pdl is
+// recorded with its grid, so tests and the bench can tell which kernel variant served each step.
+struct LaunchNote {
+  const void* fn;
+  unsigned grid;
+};
+inline thread_local std::vector<LaunchNote>* g_launch_log = nullptr;
+inline void note_launch(const void* fn, dim3 grid) {
+  if (g_launch_log) g_launch_log->push_back({fn, grid.x * grid.y * grid.z});
+}
+
 // cudaLaunchKernelEx with the PDL attribute (plus optional extra attributes).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               const cudaLaunchAttribute* extra, int n_extra, Args&&... args) {
+  note_launch(reinterpret_cast<const void*>(kernel), grid);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;

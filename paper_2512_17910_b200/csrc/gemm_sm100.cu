@@ -618,6 +618,7 @@ int launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& s, con
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    note_launch(reinterpret_cast<const void*>(gemm_bf16_kernel<BN>), grid);
     if (cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<BN>, a, b, s, u, targs) != cudaSuccess) return ALORA_ECUDA;
   } else if (launch_pdl(gemm_bf16_kernel<BN>, grid, dim3(kThreads), C::kSmem, st, nullptr, 0, a, b, s, u, targs) !=
              cudaSuccess) {

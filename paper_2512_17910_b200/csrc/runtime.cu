@@ -6,6 +6,8 @@
 // kernels are launched from here, on the caller's stream, with no host sync.
 
 #include <algorithm>
+#include <cxxabi.h>
+#include <string>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -38,6 +40,7 @@ struct ProfRec {
   const char* kind;
   int ev0, ev1;
   double bytes, flops;
+  std::vector<LaunchNote> kernels;  // what the launcher actually launched (function, grid size)
 };
 
 struct Profiler {
@@ -100,12 +103,15 @@ struct Launcher {
   int operator()(const char* kind, double bytes, double flops, F&& fn) {
     if (skipped(kind)) return ALORA_OK;
     int e0 = m.prof.on ? m.prof.event(st) : -1;
+    std::vector<LaunchNote> log;
+    if (m.prof.on) g_launch_log = &log;
     const int rc = fn();
+    g_launch_log = nullptr;
     if (rc != ALORA_OK) return rc;
     ++n;
     if (m.prof.on) {
       const int e1 = m.prof.event(st);
-      if (e0 >= 0 && e1 >= 0) m.prof.recs.push_back({kind, e0, e1, bytes, flops});
+      if (e0 >= 0 && e1 >= 0) m.prof.recs.push_back({kind, e0, e1, bytes, flops, std::move(log)});
     }
     return ALORA_OK;
   }
@@ -652,6 +658,42 @@ int alora_model_profile_read(void* handle, int32_t max_kinds, char* names, float
     flops[k] += r.flops;
   }
   return (int)kinds.size();
+}
+
+int64_t alora_model_profile_kernels(void* handle, char* buf, int64_t cap) {
+  if (!handle) return ALORA_EINVAL;
+  Profiler& p = static_cast<Model*>(handle)->prof;
+  // one line per distinct (kind, kernel, grid): "kind<TAB>demangled kernel<TAB>grid CTAs<TAB>launches"
+  std::vector<std::tuple<std::string, std::string, unsigned, int>> rows;
+  for (const ProfRec& r : p.recs)
+    for (const LaunchNote& k : r.kernels) {
+      const char* raw = nullptr;
+      std::string name = "?";
+      if (cudaFuncGetName(&raw, k.fn) == cudaSuccess && raw) {
+        int status = 0;
+        char* dm = abi::__cxa_demangle(raw, nullptr, nullptr, &status);
+        name = (status == 0 && dm) ? dm : raw;
+        free(dm);
+      }
+      bool found = false;
+      for (auto& row : rows)
+        if (std::get<0>(row) == r.kind && std::get<1>(row) == name && std::get<2>(row) == k.grid) {
+          ++std::get<3>(row);
+          found = true;
+          break;
+        }
+      if (!found) rows.emplace_back(r.kind, name, k.grid, 1);
+    }
+  std::string out;
+  for (auto& row : rows)
+    out += std::get<0>(row) + "\t" + std::get<1>(row) + "\t" + std::to_string(std::get<2>(row)) + "\t" +
+           std::to_string(std::get<3>(row)) + "\n";
+  if (buf && cap > 0) {
+    const int64_t n = std::min<int64_t>(cap - 1, (int64_t)out.size());
+    std::memcpy(buf, out.data(), n);
+    buf[n] = 0;
+  }
+  return (int64_t)out.size() + 1;
 }
 
 }  // extern "C"

@@ -563,6 +563,21 @@ class Model:
             out[name] = {"ms": float(ms[i]), "launches": int(cnt[i]), "bytes": float(by[i]), "flops": float(fl[i])}
         return out
 
+    def profile_kernels(self) -> list:
+        """[(kind, kernel name, grid CTAs, launches)] of the launches recorded since set_profiling(True)."""
+        if self._handle is None:
+            return []
+        n = _native.lib.alora_model_profile_kernels(self._handle, None, 0)
+        if n < 0:
+            _native.check(int(n), "profile_kernels")
+        buf = ctypes.create_string_buffer(int(n))
+        _native.lib.alora_model_profile_kernels(self._handle, buf, int(n))
+        rows = []
+        for line in buf.value.decode().splitlines():
+            kind, name, grid, cnt = line.split("\t")
+            rows.append((kind, name, int(grid), int(cnt)))
+        return rows
+
     def forward_step(self, seqs, kv) -> dict:
         """Run every span of a step; returns {request_id: float32[V] logits of the span's last row}."""
         p = self.pack(seqs, int(kv.shape[3]))

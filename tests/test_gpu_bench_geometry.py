@@ -1,0 +1,209 @@
+"""Parity at the geometries bench.py measures (C2: Llama-3.2-1B, C3: Llama-3-8B), reduced depth.
+
+The bench times one aLoRA eval turn: every request of the turn computes only its suffix (the 16-20
+tokens after the base-aligned cached prefix) over thousands of cached tokens, in one packed step, and
+then decodes. These tests run that exact step shape through Model.forward_step (the reference's
+model.py:233-272 surface) at the full C2 / C3 widths -- d 2048 / 4096, 32 q / 8 kv heads, head_dim
+64 / 128, SwiGLU 8192 / 14336, vocab 128256, 3 / 8 adapters r=32 -- with 2 layers, against the oracle's
+bf16 numerics (oracle/model_oracle.py, the restatement of model.py:95-272 plus the llama deltas):
+
+  * logits |d| <= 5e-2 and KV rel-L2 <= 1e-2 (SURVEY.md §8(c) tolerances), per request;
+  * greedy ids teacher-forced and margin-aware: wherever the oracle's top-1 / top-2 margin exceeds
+    2 x the logit tolerance, the device id must equal the oracle id (zero disagreements allowed);
+  * the kernels that served each step are read back from the executor's launch log
+    (Model.profile_kernels), so the test proves the bench-only variants ran: the two-row-tile
+    weight-streaming GEMM with deferred split-K partials (C2, M=240), the persistent GEMM (C3, M=1024),
+    the D=64 / D=128 tcgen05 prefill attention, the swap-AB decode GEMM and the decode attention.
+
+The cached prefix is random bf16 KV written into the paged pool (the same values on both sides), so
+the oracle only computes the suffix -- at these widths a CPU base prefill of 2k-8k tokens would not
+finish in test time. Requests of one conversation share its prefix blocks, as in the bench (eval
+requests on different adapters reuse the base turn's blocks). Counts go to $ALORA_PARITY_OUT
+(default gpurun_out/parity_bench_geometry.json; copied to profiles/ when committed).
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+P = pytest.importorskip("paper_2512_17910_b200")
+
+LOGIT_TOL = 5e-2
+KV_REL_L2 = 1e-2
+B = 16
+
+C2 = dict(arch="llama", n_heads=32, n_kv_heads=8, head_dim=64, d_model=2048, ffn_dim=8192, vocab_size=128256)
+C3 = dict(arch="llama", n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, ffn_dim=14336, vocab_size=128256)
+
+_RESULTS = {}
+
+
+def _record(name, res):
+    _RESULTS[name] = res
+    out = os.environ.get("ALORA_PARITY_OUT", os.path.join("gpurun_out", "parity_bench_geometry.json"))
+    os.makedirs(os.path.dirname(out) or ".", exist_ok=True)
+    with open(out, "w") as f:
+        json.dump(_RESULTS, f, indent=1)
+
+
+def _weights(dims, n_layers, seed):
+    """Random llama weights, bf16-valued fp32, fan-in ranges as weights.generate_weights (fast generator:
+    at 8B widths the Philox streams would dominate the test). Returns (device-model weights, oracle dict)."""
+    rng = np.random.default_rng(seed)
+    d, F, V = dims["d_model"], dims["ffn_dim"], dims["vocab_size"]
+    qw, kvw = dims["n_heads"] * dims["head_dim"], dims["n_kv_heads"] * dims["head_dim"]
+
+    def u(shape, bound):
+        return O.bf16_round((rng.random(shape, dtype=np.float32) * 2 - 1) * np.float32(bound))
+
+    def gain():
+        return (1 + 0.1 * (rng.random(d, dtype=np.float32) * 2 - 1)).astype(np.float32)
+
+    bd, bq, bf = np.sqrt(3.0 / d), np.sqrt(3.0 / qw), np.sqrt(3.0 / F)
+    layers, olayers = [], []
+    for _ in range(n_layers):
+        lw = P.LayerWeights(attn_norm=gain(), wq=u((d, qw), bd), wk=u((d, kvw), bd), wv=u((d, kvw), bd),
+                            wo=u((qw, d), bq), mlp_norm=gain(), w_in=u((d, F), bd), w_up=u((d, F), bd),
+                            w_out=u((F, d), bf))
+        layers.append(lw)
+        olayers.append({"attn_norm": lw.attn_norm, "wq": lw.wq, "wk": lw.wk, "wv": lw.wv, "wo": lw.wo,
+                        "mlp_norm": lw.mlp_norm, "w_gate": lw.w_in, "w_up": lw.w_up, "w_down": lw.w_out})
+    embed = u((V, d), bd)
+    final = gain()
+    pw = P.BaseWeights(embed=embed, layers=layers, unembed=None, final_norm=final)
+    ow = {"layers": olayers, "embed": embed, "final_norm": final, "unembed": None}
+    return pw, ow
+
+
+def _margin_ok(ref_logits, got_id, tol=LOGIT_TOL):
+    """(decided, agree): decided iff the oracle's top-1 / top-2 margin exceeds 2 * tol."""
+    top2 = np.partition(ref_logits, -2)[-2:]
+    decided = float(top2[1] - top2[0]) > 2 * tol
+    return decided, int(np.argmax(ref_logits)) == int(got_id)
+
+
+def _kernels(model):
+    return [(k, n) for k, n, _, _ in model.profile_kernels()]
+
+
+def _has(kernels, kind, needle):
+    return any(k == kind and needle in n for k, n in kernels)
+
+
+def _run_eval_turn(dims, n_layers, n_conv, n_adapters, cached, suffix, n_decode, seed):
+    cfg_kw = dict(dims, n_layers=n_layers, max_seq_len=cached + suffix + n_decode + 64)
+    pcfg = P.ModelConfig(**cfg_kw, dtype="bf16")
+    ocfg = O.OracleConfig(**cfg_kw, numerics="bf16")
+    pw, ow = _weights(dims, n_layers, seed)
+    n_req = n_conv * n_adapters
+    model = P.Model(pcfg, weights=pw, max_tokens=max(256, n_req * suffix), max_seqs=max(64, n_req))
+    om = O.OracleModel(ocfg, ow).to_f64()
+    del pw
+    V = pcfg.vocab_size
+    pads, oads = [], []
+    for k in range(n_adapters):
+        inv = P.invocation_for(V, k)
+        pads.append(P.generate_adapter(f"adapter{k}", pcfg.d_model, 32, seed=k, invocation_tokens=inv,
+                                       kv_width=pcfg.kv_width, q_width=pcfg.q_width))
+        oads.append(O.oracle_adapter(f"adapter{k}", ocfg, 32, seed=k, invocation_tokens=inv))
+    # paged pool: conversation c owns `cached // B` shared prefix blocks; every request adds its private tail
+    pre_blocks = cached // B
+    tail_blocks = -(-(cached + suffix + n_decode) // B) - pre_blocks
+    nb = n_conv * pre_blocks + n_req * tail_blocks + 4
+    rng = np.random.default_rng(seed + 1)
+    okv = np.zeros((nb, n_layers, 2, B, ocfg.kv_width), np.float32)
+    okv[: n_conv * pre_blocks] = O.bf16_round(rng.standard_normal((n_conv * pre_blocks, n_layers, 2, B,
+                                                                    ocfg.kv_width), dtype=np.float32))
+    pool = P.BlockPool(nb, B, n_layers, pcfg.d_model, kv_width=pcfg.kv_width, dtype="bf16")
+    pool.kv.copy_(torch.as_tensor(okv).to(torch.bfloat16))
+    convs = [rng.integers(0, V - 32, cached + suffix - 4) for _ in range(n_conv)]
+    reqs = []  # (rid, tokens, table, adapter index, inv_start)
+    for c in range(n_conv):
+        for k in range(n_adapters):
+            i = len(reqs)
+            table = list(range(c * pre_blocks, (c + 1) * pre_blocks)) + \
+                list(range(n_conv * pre_blocks + i * tail_blocks, n_conv * pre_blocks + (i + 1) * tail_blocks))
+            toks = np.concatenate([convs[c], [V - 1], P.invocation_for(V, k)]).astype(np.int64)
+            reqs.append((f"c{c}-a{k}", toks, table, k, len(toks) - 3))
+    res = {"requests": n_req, "rows_per_step": [n_req * suffix] + [n_req] * n_decode, "max_abs_dlogit": [],
+           "kv_rel_l2": [], "greedy_decided": 0, "greedy_agree_decided": 0, "greedy_undecided": 0,
+           "greedy_agree_all": 0}
+    toks_next = {}
+    kinds = []
+    for step in range(1 + n_decode):
+        pseqs, oseqs = [], []
+        for rid, toks, table, k, inv_start in reqs:
+            if step == 0:
+                start, span = cached, toks[cached:]
+            else:
+                start, span = cached + suffix + step - 1, np.asarray([toks_next[rid]], np.int64)
+            mask = np.arange(start, start + len(span)) < inv_start
+            pseqs.append(P.SeqInput(rid, span, start, table, pads[k], mask))
+            oseqs.append(O.OracleSpan(rid, span, start, table, oads[k], mask))
+        model.set_profiling(True)
+        got = model.forward_step(pseqs, pool.kv)
+        kinds.append(_kernels(model))
+        model.set_profiling(False)
+        want = om.forward_step(oseqs, okv, batch_head=True)
+        worst = max(float(np.max(np.abs(got[r] - want[r]))) for r in want)
+        res["max_abs_dlogit"].append(worst)
+        for rid in want:
+            decided, agree = _margin_ok(want[rid], int(np.argmax(got[rid])))
+            res["greedy_decided"] += decided
+            res["greedy_agree_decided"] += decided and agree
+            res["greedy_undecided"] += not decided
+            res["greedy_agree_all"] += agree
+            toks_next[rid] = int(np.argmax(want[rid]))  # teacher forcing: both sides continue with the oracle id
+        # KV rows written this step, every layer, per request
+        kvd = pool.kv.float().cpu().numpy()
+        rels = []
+        for (rid, toks, table, k, inv_start), ps in zip(reqs, pseqs):
+            pos = np.arange(ps.start_pos, ps.start_pos + len(ps.tokens))
+            ids = np.asarray(table)[pos // B]
+            a, b = kvd[ids, :, :, pos % B], okv[ids, :, :, pos % B]
+            rels.append(float(np.linalg.norm(a - b) / np.linalg.norm(b)))
+        res["kv_rel_l2"].append(max(rels))
+        print(f"[parity] step {step}: M={sum(len(s.tokens) for s in pseqs)} max|dlogit| {worst:.3g} "
+              f"KV rel-L2 {max(rels):.3g}")
+    res["kernels"] = [sorted({f"{k}: {n.split('(')[0]}" for k, n in ks}) for ks in kinds]
+    return res, kinds
+
+
+def _assert_parity(res):
+    assert max(res["max_abs_dlogit"]) <= LOGIT_TOL, res["max_abs_dlogit"]
+    assert max(res["kv_rel_l2"]) <= KV_REL_L2, res["kv_rel_l2"]
+    assert res["greedy_agree_decided"] == res["greedy_decided"], "greedy id differs where the margin decides it"
+    assert res["greedy_decided"] >= 0.5 * (res["greedy_decided"] + res["greedy_undecided"])
+
+
+def test_c2_geometry_eval_turn_and_decode_vs_oracle():
+    """C2 (Llama-3.2-1B widths, 2 layers): 4 conversations x 3 adapters = 12 eval requests, each 20 suffix
+    rows over 2,032 cached tokens (M = 240, the bench's TTFT step), then 3 decode steps."""
+    res, kinds = _run_eval_turn(C2, n_layers=2, n_conv=4, n_adapters=3, cached=2032, suffix=20, n_decode=3, seed=7)
+    _record("c2_2layers", res)
+    _assert_parity(res)
+    pre, dec = kinds[0], kinds[1]
+    assert _has(pre, "gemm_qkv", "gemm_ws_kernel<") and _has(pre, "gemm_mlp_in", "gemm_ws_kernel<")
+    assert _has(pre, "attention", "attn_tc_kernel<64>")
+    assert _has(pre, "rmsnorm", "residual_rmsnorm_kernel")
+    assert _has(dec, "gemm_qkv", "gemm_dec_kernel") and _has(dec, "attention", "attn_decode_kernel<64")
+    assert _has(dec, "gemm_lm_head", "gemm_dec_kernel")
+
+
+def test_c3_geometry_eval_turn_and_decode_vs_oracle():
+    """C3 (Llama-3-8B widths, 2 layers): 8 conversations x 8 adapters = 64 eval requests, each 16 suffix rows
+    over 8,176 cached tokens (M = 1,024, the bench's TTFT step), then 2 decode steps."""
+    res, kinds = _run_eval_turn(C3, n_layers=2, n_conv=8, n_adapters=8, cached=8176, suffix=16, n_decode=2, seed=11)
+    _record("c3_2layers", res)
+    _assert_parity(res)
+    pre, dec = kinds[0], kinds[1]
+    assert _has(pre, "gemm_qkv", "gemm_bf16_persist_kernel") or _has(pre, "gemm_qkv", "gemm_bf16_kernel")
+    assert _has(pre, "attention", "attn_tc_kernel<128>")
+    assert _has(dec, "attention", "attn_decode_kernel<128")

@@ -170,3 +170,24 @@ def test_llama_oracle_chunked_equals_whole_and_gqa_shapes():
     np.testing.assert_allclose(part, whole, rtol=1e-5, atol=1e-5)
     np.testing.assert_array_equal(kv1[:6, :, :, :, :], kv2[:6])
     assert kv1.shape[-1] == 32
+
+
+def test_oracle_gqa_attention_matches_per_head_dense():
+    """The oracle's batched GQA attention (llama mode) equals the per-head dense fp64 reference."""
+    from conftest import dense_reference_attention
+    rng = np.random.default_rng(5)
+    H, Hkv, D, B, start, n = 8, 2, 16, 4, 13, 6
+    total = start + n
+    nb = -(-total // B)
+    kv = rng.standard_normal((nb + 2, 1, 2, B, Hkv * D)).astype(np.float32)
+    ids = list(rng.permutation(nb + 2)[:nb])
+    k = rng.standard_normal((n, Hkv * D)).astype(np.float32)
+    v = rng.standard_normal((n, Hkv * D)).astype(np.float32)
+    q = rng.standard_normal((n, H * D)).astype(np.float32)
+    import oracle as O
+    got = O.paged_attention(q, kv, 0, ids, k, v, start, H, Hkv)
+    pos = np.arange(start)
+    kc = np.concatenate([kv[np.asarray(ids)[pos // B], 0, 0, pos % B], k])
+    vc = np.concatenate([kv[np.asarray(ids)[pos // B], 0, 1, pos % B], v])
+    want = dense_reference_attention(q, kc, vc, H, start, Hkv)
+    assert np.max(np.abs(got - want)) < 1e-6

@@ -82,3 +82,20 @@ def test_two_replicas_gloo_match_single_engine_and_keep_reuse():
     for rid, (hit, comp, stage) in got.items():
         if stage == "eval":
             assert hit == ((x + y - 1) // B) * B, rid  # the adapter turn reuses the base turn's blocks
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """bench.py --gpus 2 run directly (no torchrun) re-launches itself with one process per rank; on CPU the
+    --probe-ranks plumbing check inits gloo and rank 0 reports n_gpus 2 with the instance-affinity split."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--probe-ranks"],
+                         capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["instances_per_rank"] == [list(range(0, 16, 2)), list(range(1, 16, 2))]
+    assert line["eval_requests_total"] == 128
