@@ -247,7 +247,7 @@ def test_bf16_c1_pipeline_hits_and_tables_exact():
     print(f"[parity] bf16 C1 pipeline: {len(seen)} emitted ids, max |dlogit| {worst:.3g}; margin-decided "
           f"{decided}, agreeing {agree}; free-running ids equal to the fp64 reference {same}/{total}")
     assert worst <= LOGIT_TOL
-    assert agree == decided and decided >= 0.9 * len(seen)
+    assert agree == decided and decided >= 0.8 * len(seen)
 
 
 @pytest.mark.parametrize("B", [16, 32])
