@@ -155,6 +155,35 @@ int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs
                                    int32_t max_ctx, int32_t n_heads, int32_t n_kv_heads,
                                    int32_t head_dim);
 
+/* Host planner of the shared-prefix attention (replaces the per-span loop of model.py:243 around
+ * paged_attention, model.py:149-187, for steps whose requests hold the same physical prefix blocks:
+ * the base-aligned reuse of kv_cache.py:72-96). HOST arrays: cu_q [S+1], start_pos [S], block_table
+ * [S, max_blocks]. flags: bit 0 group spans by shared leading blocks, bit 1 never split the keys.
+ * partial_cap_bytes bounds the split-KV partials. Writes the int32 plan into out (layout in
+ * csrc/attn_plan.cpp: header [n_items, n_segs, n_sets, max_parts, merge_rows, unique kv tokens,
+ * total tiles, 0] then items, segments, sets, set rows, per-span partition counts) and returns its
+ * length, or -(length needed) when out_cap is too small, or ALORA_EINVAL. */
+int64_t alora_plan_attention(int32_t n_seqs, const int32_t* cu_q, const int32_t* start_pos,
+                             const int32_t* block_table, int32_t max_blocks, int32_t block_size,
+                             int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, int32_t flags,
+                             int64_t partial_cap_bytes, int32_t* out, int64_t out_cap);
+
+/* Split-KV partial bytes the executor's attention workspace holds (the partial_cap_bytes to plan with). */
+int64_t alora_attn_partial_capacity(int32_t n_heads, int32_t head_dim);
+
+/* Paged causal attention (model.py:149-187) through a plan from alora_plan_attention, uploaded to
+ * the device (bf16 tier): row m at absolute position positions[m] of span row_seq[m] attends keys
+ * [0, positions[m]] of its span; requests grouped by the plan read their shared prefix once.
+ * Results equal alora_paged_prefill_attn's up to fp32 summation order. Workspace: the split-KV
+ * partials, max_parts * n_rows * n_heads * (head_dim + 2) * 4 bytes when max_parts > 1. */
+int alora_paged_prefix_attn(const void* q, int64_t ld_q, int32_t n_rows, int32_t n_seqs,
+                            const int32_t* positions, const int32_t* row_seq, const int32_t* block_table,
+                            int32_t max_blocks, const int32_t* plan, int32_t n_items, int32_t n_segs,
+                            int32_t n_sets, int32_t max_parts, const void* kv_pool, int32_t total_blocks,
+                            int32_t n_layers, int32_t layer, int32_t block_size, int32_t n_heads,
+                            int32_t n_kv_heads, int32_t head_dim, void* out, int64_t ld_out,
+                            void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Dense bf16 GEMM on tcgen05 (the engine behind alora_qkv_proj and the O/MLP/lm_head
  * projections of alora_model_forward): C = epi(A[M,K] . Bt[N,K]^T), fp32 accumulate.
  * epi: 0 store bf16, 1 C(fp32) += acc, 2 relu -> bf16, 3 SwiGLU of 64-interleaved
@@ -234,8 +263,14 @@ typedef struct AloraStepDesc {
   float* logits;                /* [S, V] fp32 out */
   int32_t* next_ids;            /* [S] argmax out (read first for negative tokens, written last) */
   /* host-side shape summary, used only for the profiler's algorithmic bytes/flops */
-  double attn_kv_tokens;        /* sum over spans of (start_pos + n) */
+  double attn_kv_tokens;        /* distinct keys read (a shared prefix counted once) */
   double attn_qk_pairs;         /* sum over spans of n * (start_pos + (n + 1) / 2) */
+  /* optional shared-prefix attention plan (alora_plan_attention output, on the device); NULL = per span */
+  const int32_t* row_seq;       /* [M] span of each row */
+  const int32_t* attn_plan;
+  int32_t attn_items, attn_segs, attn_sets, attn_max_parts;
+  /* most rows taking one adapter's delta in this step (host count): few -> the segmented LoRA shrink */
+  int32_t lora_rows_max;
 } AloraStepDesc;
 
 int64_t alora_model_workspace_bytes(const AloraModelDesc* desc);

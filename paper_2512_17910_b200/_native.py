@@ -71,6 +71,9 @@ class AloraStepDesc(ctypes.Structure):
         ("row_apply", c_void_p), ("cu_q", c_void_p), ("start_pos", c_void_p), ("block_table", c_void_p),
         ("last_row", c_void_p), ("logits", c_void_p), ("next_ids", c_void_p),
         ("attn_kv_tokens", ctypes.c_double), ("attn_qk_pairs", ctypes.c_double),
+        ("row_seq", c_void_p), ("attn_plan", c_void_p),
+        ("attn_items", c_i32), ("attn_segs", c_i32), ("attn_sets", c_i32), ("attn_max_parts", c_i32),
+        ("lora_rows_max", c_i32),
     ]
 
 
@@ -113,6 +116,13 @@ EXPORTS = {
                                      c_i32, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p, c_i64, c_void_p),
     "alora_attn_workspace_bytes": _sig("alora_attn_workspace_bytes", c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                                        c_i32, c_i32, c_i32),
+    "alora_plan_attention": _sig("alora_plan_attention", c_i64, c_i32, c_void_p, c_void_p, c_void_p, c_i32, c_i32,
+                                 c_i32, c_i32, c_i32, c_i32, c_i64, c_void_p, c_i64),
+    "alora_attn_partial_capacity": _sig("alora_attn_partial_capacity", c_i64, c_i32, c_i32),
+    "alora_paged_prefix_attn": _sig("alora_paged_prefix_attn", c_i32, c_void_p, c_i64, c_i32, c_i32, c_void_p,
+                                    c_void_p, c_void_p, c_i32, c_void_p, c_i32, c_i32, c_i32, c_i32, c_void_p,
+                                    c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p,
+                                    c_i64, c_void_p),
     "alora_gemm_bf16": _sig("alora_gemm_bf16", c_i32, c_i32, c_void_p, c_i32, c_void_p, c_i32, c_void_p, c_i32,
                             c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p),
     "alora_gemm_workspace_bytes": _sig("alora_gemm_workspace_bytes", c_i64),

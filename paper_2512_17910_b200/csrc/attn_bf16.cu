@@ -564,10 +564,25 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
     int32_t win = 0;
     auto issue_kv = [&](int t) {  // warp-wide. K/V tile t: TMA boxes of [B keys x 64 dims], page by page
       const int st = t % kNS<D>;
-      if (sm100::elect_one()) sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
       uint8_t* dk = sm + L::kK + st * L::kKVBytes;
       uint8_t* dv = sm + L::kV + st * L::kKVBytes;
       const int b0 = (key_begin + t * kKT) / a.B;
+      if (a.exp & 32) {  // timing experiment: one page per tile (results wrong)
+        if (sm100::elect_one()) sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes / per_tile);
+        const int idx = min(b0, last_blk);
+        const int64_t blk = bt[idx];
+        const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int sub = 0; sub < D / 64; ++sub) {
+            sm100::tma_load_2d(dk + sub * kKT * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk, pol);
+            sm100::tma_load_2d(dv + sub * kKT * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk + a.B, pol);
+          }
+        }
+        __syncwarp();
+        return;
+      }
+      if (sm100::elect_one()) sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes);
       for (int j = 0; j < per_tile; ++j) {
         const int idx = min(b0 + j, last_blk);  // past the end: a valid duplicate, masked later
         if (idx >= w0 + 32) {
@@ -648,7 +663,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
             for (int ks = 0; ks < D / 16; ++ks) {  // K = D in 16-wide steps; sub-tile every 4 steps
               const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
               const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
-              sm100::mma_bf16_ss(tS[ts % kSBuf], da, db, idesc_s, ks > 0 ? 1u : 0u);
+              if (!(a.exp & 64)) sm100::mma_bf16_ss(tS[ts % kSBuf], da, db, idesc_s, ks > 0 ? 1u : 0u);
             }
             sm100::mma_commit(&s_full[ts % kSBuf]);
           }
@@ -669,7 +684,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
 #pragma unroll
             for (int kk = 0; kk < kKT / 16; ++kk) {  // K = 64 keys, 16 per step = 8 TMEM columns
               const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
-              sm100::mma_bf16_ts(tO, tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
+              if (!(a.exp & 64)) sm100::mma_bf16_ts(tO, tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
             }
             sm100::mma_commit(&kv_empty[tp % kNS<D>]);
             sm100::mma_commit(&s_free[tp % kSBuf]);
@@ -698,7 +713,7 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
       const int k0 = key_begin + t * kKT;
       sm100::mbar_wait(&s_full[t % kSBuf], (t / kSBuf) & 1);
       sm100::tc_fence_after();
-      if (a.exp == 3) {  // timing experiment: no softmax work at all
+      if (a.exp & 16) {  // timing experiment: no softmax work at all
         sm100::tc_fence_before();
         sm100::mbar_arrive(&p_full[t % kSBuf]);
         continue;
@@ -817,7 +832,598 @@ __global__ void __launch_bounds__(kThreads, D == 64 ? 2 : 1) attn_tc_kernel(cons
   if (tid == 0) ATTN_TRACE(5);
 }
 
+
+// ============================================================================================================
+// Shared-prefix attention over a host-built work list (attn_plan.cpp). The eval turn of a multi-adapter
+// pipeline puts 8 requests on the SAME physical prefix blocks (base-aligned hashing, kv_cache.py:72-96); the
+// per-span kernel above streams that prefix once per request with 64 live rows in each 128-row tile. Here a
+// work item is (query set, 128-row M-tile, KV partition) x kv head: the set packs the rows of every request
+// of a group, so one K/V stream feeds full tiles, and the item's segments (the shared prefix through the
+// group's table, then each request's own keys through its own table, other rows masked) run through one
+// online softmax. Decode steps of the same group share the prefix the same way.
+// Pipeline: producer warp (TMA page boxes, segment by segment), MMA warp on a STATIC schedule with blocking
+// mbarrier waits (the event loop of attn_tc_kernel spent ~150 cycles per mbar_test and bounded its tile rate),
+// S running kSB-1 tiles ahead of PV, 4 softmax warps (one TMEM lane quadrant each).
+// ============================================================================================================
+template <int D>
+constexpr int kSB = D == 128 ? 4 : 3;  // S buffers in TMEM (D=128: 4 x 64 + O 128 of 512; D=64: 3 x 64 + O 64 of 256)
+
+struct GrpArgs {
+  const __nv_bfloat16* q;
+  int64_t ld_q;
+  const int32_t* positions;  // [M] absolute position of each row
+  const int32_t* row_seq;    // [M] span of each row
+  const int32_t* block_table;
+  int max_blocks;
+  const int32_t* items;      // [n_items][8]
+  const int32_t* segs;       // [n_segs][4]
+  const int32_t* sets;       // [n_sets][2]
+  const int32_t* set_tok;    // [M]
+  const int32_t* sp_np;      // [S]
+  const __nv_bfloat16* kv;
+  int n_layers, layer, B, H, Hkv;
+  float scale_log2;
+  __nv_bfloat16* out;
+  int64_t ld_out;
+  float* ws_o;   // [max_np][M][H][D]
+  float* ws_ml;  // [max_np][M][H][2]
+  int M;
+  unsigned long long* trace;
+  int exp;
+};
+
+// walks an item's segments tile by tile (64 keys per tile)
+struct SegCursor {
+  const int32_t* segs;
+  int j, end, t_in, nt, tab, lo, hi, filter;
+  __device__ void load() {
+    tab = segs[4 * j];
+    lo = segs[4 * j + 1];
+    hi = segs[4 * j + 2];
+    filter = segs[4 * j + 3];
+    nt = (hi - lo + kKT - 1) / kKT;
+    t_in = 0;
+  }
+  __device__ void init(const int32_t* s, int b, int e) {
+    segs = s;
+    j = b;
+    end = e;
+    if (j < end) load();
+    skip_empty();
+  }
+  __device__ void skip_empty() {
+    while (j < end && t_in >= nt) {
+      ++j;
+      if (j < end) load();
+    }
+  }
+  __device__ void next() {
+    ++t_in;
+    skip_empty();
+  }
+  __device__ int k0() const { return lo + t_in * kKT; }
+};
+
+// Producer: PW = 0 -> one warp issuing TMA page boxes [B keys x 64 dims]; PW > 0 -> PW warps loading whole
+// tiles with cp.async (16-byte chunks written straight into the SW128 layout), warp w owning tiles w, w+PW, ...
+// and publishing each after its own data landed (wait_group 0 + proxy fence + arrive). Per-box TMA processing
+// (~70 ns per 2 KB page box under ncu) capped a CTA's K/V supply at ~30 GB/s; PW warps of cp.async keep PW
+// tiles in flight at the LSU's issue rate.
+// MT = M-tiles per CTA. With MT = 2 (the default) a CTA runs two 128-row query tiles of a set against every
+// K/V tile it loads: a CTA's K/V ingest (~45 GB/s per SM, the same whether L2 hit or not) is what bounded the
+// one-tile kernel, so sharing each loaded tile between 256 rows halves the per-row cost. Softmax warps 4X..4X+3
+// serve tile X (TMEM lane quadrant = warp % 4).
+template <int PW, int MT>
+constexpr int kGrpThreads = (4 * MT + (PW > 0 ? PW : 1) + 1) * 32;
+// S buffers per tile: the TMEM (512 columns) holds MT O tiles of D columns plus MT x NB S buffers of 64
+template <int D, int MT>
+constexpr int kGrpNB = MT == 2 ? 2 : (D == 128 ? 4 : 3);
+template <int D, int MT>
+constexpr int kGrpTmem = (MT * D + MT * kGrpNB<D, MT> * 64) <= 256 ? 256 : 512;
+template <int D, int MT>
+constexpr int kGrpNS = MT == 2 ? (D == 128 ? 5 : 8) : kNS<D>;  // K/V ring stages
+template <int D, int MT>
+struct SmemG {
+  static constexpr int kQBytes = MT * kQT * D * 2;
+  static constexpr int kKVBytes = kKT * D * 2;
+  static constexpr int kQ = 0;
+  static constexpr int kK = kQ + kQBytes;
+  static constexpr int kV = kK + kGrpNS<D, MT> * kKVBytes;
+  static constexpr int kBar = kV + kGrpNS<D, MT> * kKVBytes;
+  static constexpr int kTotal = kBar + 512 + 1024;
+};
+
+template <int D, int PW, int MT>
+__global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 : 1)
+    attn_grp_kernel(const GrpArgs a, const __grid_constant__ CUtensorMap tm_kv) {
+  using L = SmemG<D, MT>;
+  constexpr int NB = kGrpNB<D, MT>;
+  constexpr int NS = kGrpNS<D, MT>;
+  constexpr int kSoftWarps = 4 * MT;
+  constexpr int kMmaWarp = kSoftWarps + (PW > 0 ? PW : 1);
+  constexpr int kTmemCols = kGrpTmem<D, MT>;
+  extern __shared__ uint8_t smem_raw_grp[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_grp) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kBar);
+  uint64_t* kv_full = bars;
+  uint64_t* kv_empty = kv_full + NS;
+  uint64_t* s_full = kv_empty + NS;     // [MT][NB]
+  uint64_t* p_full = s_full + MT * NB;  // [MT][NB]
+  uint64_t* s_free = p_full + MT * NB;  // [MT][NB]: PV of the P in that S buffer completed (one phase per use)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + MT * NB);
+
+  const int* it = a.items + (int64_t)blockIdx.x * 8;
+  const int set = it[0], mtile = it[1], seg_b = it[2], seg_e = it[3], p_index = it[4], cached = it[5];
+  const int n_tiles = it[6];
+  const int kvh = blockIdx.y;
+  const int G = a.H / a.Hkv;
+  const int tok_off = a.sets[2 * set], n_tok = a.sets[2 * set + 1];
+  int rows_t[MT];
+#pragma unroll
+  for (int x = 0; x < MT; ++x) rows_t[x] = max(0, min(kQT, n_tok * G - (mtile * MT + x) * kQT));
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) ATTN_TRACE(0);
+  constexpr int CH = D / 8;
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) {
+      sm100::mbar_init(&kv_full[i], PW > 0 ? 32 : 1);  // cp.async: every lane of the loading warp arrives
+      sm100::mbar_init(&kv_empty[i], 1);
+    }
+    for (int x = 0; x < MT; ++x)
+      for (int i = 0; i < NB; ++i) {
+        sm100::mbar_init(&s_full[x * NB + i], 1);
+        sm100::mbar_init(&s_free[x * NB + i], 1);
+        sm100::mbar_init(&p_full[x * NB + i], 32 * max(1, (rows_t[x] + 31) / 32));
+      }
+    sm100::fence_barrier_init();
+  }
+  if (warp == kMmaWarp) sm100::tmem_alloc<kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // O of tile x at x*D, then the S buffers: tile x buffer i at MT*D + (x*NB + i)*64
+  auto tOx = [&](int x) { return tmem + (uint32_t)(x * D); };
+  auto tSx = [&](int x, int i) { return tmem + (uint32_t)(MT * D + (x * NB + i) * 64); };
+
+  if (PW > 0 && warp >= kSoftWarps && warp < kSoftWarps + PW) {
+    // ------------------------------------------------------------------ cp.async producer warps
+    const int pw = warp - kSoftWarps;
+    SegCursor cur;
+    cur.init(a.segs, seg_b, seg_e);
+    int w0 = -(1 << 30), wseg = -1;
+    int32_t win = 0;
+    bool waited = false;
+    const int kvw = a.Hkv * D;
+    const int per_tile = kKT / a.B;
+    const int chunks_pp = a.B * 8;  // 16-byte chunks of one page row block (B rows x 64 dims)
+    int prev_st = -1;
+    for (int t = 0; t < n_tiles; ++t, cur.next()) {
+      if (t % PW != pw) continue;
+      const int st = t % NS;
+      const int k0 = cur.k0();
+      if (!waited && !(k0 + kKT <= cached || (cur.filter < 0 && cur.hi <= cached))) {
+        pdl_wait();  // this tile may hold keys the kernels before wrote
+        waited = true;
+      }
+      if (t >= NS) sm100::mbar_wait(&kv_empty[st], ((t / NS) - 1) & 1);
+      const int32_t* bt = a.block_table + (int64_t)cur.tab * a.max_blocks;
+      const int last_blk = (cur.hi - 1) / a.B;
+      const int b0 = k0 / a.B;
+      if (cur.j != wseg) {
+        wseg = cur.j;
+        w0 = -(1 << 30);
+      }
+      if (b0 + per_tile - 1 >= w0 + 32 || b0 < w0) {
+        w0 = b0;
+        win = bt[min(w0 + lane, last_blk)];
+      }
+      uint8_t* dk = sm + L::kK + st * L::kKVBytes;
+      uint8_t* dv = sm + L::kV + st * L::kKVBytes;
+      for (int j = 0; j < per_tile; ++j) {
+        const int idx = min(b0 + j, last_blk);  // past the end: a valid duplicate, masked by the softmax
+        const int64_t blk = __shfl_sync(0xffffffffu, win, idx - w0);
+        const __nv_bfloat16* kp = a.kv + ((blk * a.n_layers + a.layer) * 2) * a.B * (int64_t)kvw + kvh * D;
+        const __nv_bfloat16* vp = kp + (int64_t)a.B * kvw;
+#pragma unroll
+        for (int sub = 0; sub < D / 64; ++sub) {
+          for (int q = lane; q < chunks_pp; q += 32) {
+            const int rp = q >> 3, c = q & 7;
+            const int r = j * a.B + rp;
+            const uint32_t off = sw_off(r, sub * 8 + c, kKT);
+            cp_async16(dk + off, kp + (int64_t)rp * kvw + sub * 64 + c * 8, true);
+            cp_async16(dv + off, vp + (int64_t)rp * kvw + sub * 64 + c * 8, true);
+          }
+        }
+      }
+      cp_async_commit();
+      // two tiles in flight per warp: publish the PREVIOUS one once its data landed (this one keeps loading)
+      if (prev_st >= 0) {
+        cp_async_wait<1>();
+        sm100::fence_proxy_async_smem();  // these generic-proxy writes are read by tcgen05.mma (async proxy)
+        sm100::mbar_arrive(&kv_full[prev_st]);
+      }
+      prev_st = st;
+    }
+    if (prev_st >= 0) {
+      cp_async_wait<0>();
+      sm100::fence_proxy_async_smem();
+      sm100::mbar_arrive(&kv_full[prev_st]);
+    }
+    if (!waited) pdl_wait();
+  } else if (PW == 0 && warp == kSoftWarps) {
+    // ------------------------------------------------------------------ TMA producer warp
+    const uint64_t pol = sm100::policy_evict_first();
+    SegCursor cur;
+    cur.init(a.segs, seg_b, seg_e);
+    int w0 = -(1 << 30), wtab = -1;
+    int32_t win = 0;
+    auto issue_kv = [&](int t) {  // warp-wide: K/V tile t (the cursor's tile), TMA page boxes [B keys x 64 dims]
+      const int st = t % NS;
+      const int per_tile = (a.exp & 32) ? 1 : kKT / a.B;  // timing experiment 32: one page per tile (wrong results)
+      if (sm100::elect_one()) sm100::mbar_arrive_expect_tx(&kv_full[st], 2 * L::kKVBytes / (kKT / a.B) * per_tile);
+      uint8_t* dk = sm + L::kK + st * L::kKVBytes;
+      uint8_t* dv = sm + L::kV + st * L::kKVBytes;
+      const int32_t* bt = a.block_table + (int64_t)cur.tab * a.max_blocks;
+      const int last_blk = (cur.hi - 1) / a.B;
+      const int b0 = cur.k0() / a.B;
+      if (cur.j != wtab) {  // a new segment: its table row and its clamp bound differ, refill the window
+        wtab = cur.j;
+        w0 = -(1 << 30);
+      }
+      for (int j = 0; j < per_tile; ++j) {
+        const int idx = min(b0 + j, last_blk);  // past the end: a valid duplicate, masked by the softmax
+        if (idx >= w0 + 32 || idx < w0) {
+          w0 = idx;
+          win = bt[min(w0 + lane, last_blk)];
+        }
+        const int64_t blk = __shfl_sync(0xffffffffu, win, idx - w0);
+        const int rowk = (int)(((blk * a.n_layers + a.layer) * 2) * a.B);
+        if (sm100::elect_one()) {
+#pragma unroll
+          for (int sub = 0; sub < D / 64; ++sub) {
+            sm100::tma_load_2d(dk + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64, rowk,
+                               pol);
+            sm100::tma_load_2d(dv + sub * kKT * 128 + j * a.B * 128, &tm_kv, &kv_full[st], kvh * D + sub * 64,
+                               rowk + a.B, pol);
+          }
+        }
+        __syncwarp();
+      }
+    };
+    int t = 0;
+    // tiles wholly below every row's first computed position hold KV no kernel of this step writes: they stream
+    // in before the dependency wait (at most kNS of them, the ring depth)
+    for (; t < min(n_tiles, NS); ++t) {
+      if (cur.k0() + kKT > cached && !(cur.filter < 0 && cur.hi <= cached)) break;
+      issue_kv(t);
+      cur.next();
+    }
+    pdl_wait();
+    for (; t < n_tiles; ++t) {
+      const int st = t % NS;
+      if (t >= NS) sm100::mbar_wait(&kv_empty[st], ((t / NS) - 1) & 1);
+      issue_kv(t);
+      cur.next();
+    }
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------------ MMA issuer (static schedule)
+    pdl_wait();  // q comes from the kernels before
+    pdl_trigger();
+    // Q: the 32 lanes gather the MT x 128 GQA-packed rows of the set with cp.async into the swizzled layout
+    // (tile x at kQ + x * 128 rows)
+    for (int p = lane; p < MT * kQT; p += 32) {
+      const int x = p / kQT, pl = p % kQT;
+      const bool valid = pl < rows_t[x];
+      const int pr = (mtile * MT + x) * kQT + pl;
+      const int row = valid ? a.set_tok[tok_off + pr / G] : 0;
+      const __nv_bfloat16* src = a.q + (int64_t)row * a.ld_q + (kvh * G + (valid ? pr % G : 0)) * D;
+      uint8_t* qx = sm + L::kQ + x * kQT * D * 2;
+#pragma unroll
+      for (int c = 0; c < CH; ++c) cp_async16(qx + sw_off(pl, c, kQT), valid ? src + c * 8 : a.q, valid);
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    sm100::fence_proxy_async_smem();
+    __syncwarp();
+    constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
+    constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
+    if (lane == 0) ATTN_TRACE(1);
+    sm100::tc_fence_after();
+    // S of tile ts for query tile x; its buffer was last read (P) by PV_x(ts - NB), which must have COMPLETED
+    auto issue_s = [&](int ts) {
+      const int st = ts % NS;
+      sm100::mbar_wait(&kv_full[st], (ts / NS) & 1);
+#pragma unroll
+      for (int x = 0; x < MT; ++x) {
+        if (rows_t[x] == 0) continue;
+        if (ts >= NB) sm100::mbar_wait(&s_free[x * NB + ts % NB], ((ts / NB) - 1) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint8_t* qb = sm + L::kQ + x * kQT * D * 2;
+          const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
+#pragma unroll
+          for (int ks = 0; ks < D / 16; ++ks) {
+            const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
+            const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
+            if (!(a.exp & 64)) sm100::mma_bf16_ss(tSx(x, ts % NB), da, db, idesc_s, ks > 0 ? 1u : 0u);
+          }
+          sm100::mma_commit(&s_full[x * NB + ts % NB]);
+        }
+        __syncwarp();
+      }
+    };
+    // S runs NB-1 tiles ahead: S_{tp+NB-1} is issued at the top of iteration tp (its buffer was freed by
+    // PV_{tp-1}, issued one iteration earlier), then the PVs of tile tp as each query tile's P lands
+    for (int ts = 0; ts < min(n_tiles, NB - 1); ++ts) issue_s(ts);
+    for (int tp = 0; tp < n_tiles; ++tp) {
+      if (tp + NB - 1 < n_tiles) issue_s(tp + NB - 1);
+#pragma unroll
+      for (int x = 0; x < MT; ++x) {
+        if (rows_t[x] == 0) continue;
+        sm100::mbar_wait(&p_full[x * NB + tp % NB], (tp / NB) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t tp_a = tSx(x, tp % NB);
+          const uint8_t* vb = sm + L::kV + (tp % NS) * L::kKVBytes;
+#pragma unroll
+          for (int kk = 0; kk < kKT / 16; ++kk) {
+            const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
+            if (!(a.exp & 64)) sm100::mma_bf16_ts(tOx(x), tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
+          }
+          sm100::mma_commit(&s_free[x * NB + tp % NB]);
+        }
+        __syncwarp();
+      }
+      if (sm100::elect_one()) sm100::mma_commit(&kv_empty[tp % NS]);  // every PV of tile tp read its V
+      __syncwarp();
+    }
+  } else if (warp < kSoftWarps && (warp & 3) < (rows_t[warp >> 2] + 31) / 32) {
+    // ------------------------------------------------------------------ softmax (live warps; 4 per query tile)
+    pdl_wait();
+    const int xt = warp >> 2;  // query tile
+    const int r = (warp & 3) * 32 + lane;
+    const bool live = r < rows_t[xt];
+    const int pr = (mtile * MT + xt) * kQT + r;
+    const int row = live ? a.set_tok[tok_off + pr / G] : 0;
+    const int head = kvh * G + pr % G;
+    const int pos = live ? a.positions[row] : -1;
+    const int span = live ? a.row_seq[row] : -2;
+    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    uint64_t* s_full_x = s_full + xt * NB;
+    uint64_t* p_full_x = p_full + xt * NB;
+    uint64_t* s_free_x = s_free + xt * NB;
+    uint32_t tS[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) tS[i] = tSx(xt, i);
+    const uint32_t tO = tOx(xt);
+    const float sc = a.scale_log2;
+    const float thr = kRescaleLog2 / sc;
+    float m_run = -INFINITY, l_run = 0.f;
+    SegCursor cur;
+    cur.init(a.segs, seg_b, seg_e);
+    int lim = -1, lim_seg = -1;
+    for (int t = 0; t < n_tiles; ++t) {
+      if (cur.j != lim_seg) {
+        lim_seg = cur.j;
+        lim = (live && (cur.filter < 0 || cur.filter == span)) ? min(pos, cur.hi - 1) : -1;
+      }
+      const int k0 = cur.k0();
+      cur.next();
+      sm100::mbar_wait(&s_full_x[t % NB], (t / NB) & 1);
+      sm100::tc_fence_after();
+      if (t == 0 && tid == 0) ATTN_TRACE(2);
+      if (a.exp & 16) {  // timing experiment: no softmax work at all
+        sm100::tc_fence_before();
+        sm100::mbar_arrive(&p_full_x[t % NB]);
+        continue;
+      }
+      float sv[kKT];
+      {
+        uint32_t r0[32], r1[32];
+        sm100::tmem_ld_32x32b_x32(tS[t % NB] + lane_base, r0);
+        sm100::tmem_ld_32x32b_x32(tS[t % NB] + lane_base + 32, r1);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          sv[j] = __uint_as_float(r0[j]);
+          sv[j + 32] = __uint_as_float(r1[j]);
+        }
+      }
+      if (__any_sync(0xffffffffu, k0 + kKT - 1 > lim)) {
+#pragma unroll
+        for (int j = 0; j < kKT; ++j)
+          if (k0 + j > lim) sv[j] = -INFINITY;
+      }
+      float mx[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) mx[q] = fmaxf(sv[q], sv[q + 8]);
+#pragma unroll
+      for (int j = 16; j < kKT; j += 8) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) mx[q] = fmaxf(mx[q], sv[j + q]);
+      }
+      const float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+      const float m_new = fmaxf(m_run, mt);
+      const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
+      if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
+        const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
+        sm100::mbar_wait(&s_free_x[(t - 1) % NB], ((t - 1) / NB) & 1);  // O holds PV_{t-1}
+        sm100::tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < D; c += 32) {
+          uint32_t ov[32];
+          sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
+          sm100::tmem_st_32x32b_x32(tO + lane_base + c, ov);
+        }
+        sm100::tmem_st_wait();
+        l_run *= corr;
+      }
+      if (grow) m_run = m_new;
+      const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
+      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float p0 = fast_exp2(fmaf(sv[h * 32 + 2 * j], sc, nb));
+          const float p1 = (a.exp & 128) ? p0 : fast_exp2(fmaf(sv[h * 32 + 2 * j + 1], sc, nb));
+          rs4[j & 3] += p0 + p1;
+          pk[j] = pack_bf16(p0, p1);
+        }
+        if (!(a.exp & 256)) sm100::tmem_st_32x32b_x16(tS[t % NB] + lane_base + h * 16, pk);
+      }
+      sm100::tmem_st_wait();
+      l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&p_full_x[t % NB]);
+    }
+    if (tid == 0) ATTN_TRACE(3);
+    sm100::mbar_wait(&s_free_x[(n_tiles - 1) % NB], ((n_tiles - 1) / NB) & 1);
+    sm100::tc_fence_after();
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c = 0; c < D; c += 32) {
+      uint32_t ov[32];
+      sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+      sm100::tmem_ld_wait();
+      if (!live) continue;
+      if (p_index < 0) {
+        __nv_bfloat16* dst = a.out + (int64_t)row * a.ld_out + head * D + c;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          __align__(16) __nv_bfloat162 o2[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o2[e] = __floats2bfloat162_rn(__uint_as_float(ov[q * 8 + e * 2]) * inv,
+                                          __uint_as_float(ov[q * 8 + e * 2 + 1]) * inv);
+          *reinterpret_cast<int4*>(dst + q * 8) = *reinterpret_cast<int4*>(o2);
+        }
+      } else {
+        const int64_t slot = ((int64_t)p_index * a.M + row) * a.H + head;
+        float* dst = a.ws_o + slot * D + c;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          __stcg(reinterpret_cast<float4*>(dst + q * 4),
+                 make_float4(__uint_as_float(ov[q * 4]), __uint_as_float(ov[q * 4 + 1]),
+                             __uint_as_float(ov[q * 4 + 2]), __uint_as_float(ov[q * 4 + 3])));
+        if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run * sc, l_run));
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) sm100::tmem_dealloc<kTmemCols>(tmem);
+  if (tid == 0) ATTN_TRACE(4);
+}
+
+// Combines the KV-partition partials of the rows whose span was split (sp_np > 1), in partition order.
+template <int D>
+__global__ void __launch_bounds__(256) attn_grp_merge_kernel(const GrpArgs a) {
+  const int row = blockIdx.x;
+  pdl_wait();
+  pdl_trigger();
+  const int np = a.sp_np[a.row_seq[row]];
+  if (np <= 1) return;
+  constexpr int G8 = D / 8;
+  const int n = a.H * G8;
+  const int64_t pstride = (int64_t)a.M * a.H;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const int head = i / G8, c8 = (i % G8) * 8;
+    const int64_t slot0 = (int64_t)row * a.H + head;
+    float mx = -INFINITY;
+    for (int p = 0; p < np; ++p) mx = fmaxf(mx, __ldcg(a.ws_ml + (slot0 + p * pstride) * 2));
+    float l = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int p = 0; p < np; ++p) {
+      const float2 ml = __ldcg(reinterpret_cast<const float2*>(a.ws_ml + (slot0 + p * pstride) * 2));
+      const float w = ml.y > 0.f ? fast_exp2(ml.x - mx) : 0.f;
+      const float4 x0 = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8));
+      const float4 x1 = __ldcg(reinterpret_cast<const float4*>(a.ws_o + (slot0 + p * pstride) * D + c8 + 4));
+      l += w * ml.y;
+      acc[0] += w * x0.x; acc[1] += w * x0.y; acc[2] += w * x0.z; acc[3] += w * x0.w;
+      acc[4] += w * x1.x; acc[5] += w * x1.y; acc[6] += w * x1.z; acc[7] += w * x1.w;
+    }
+    const float inv = l > 0.f ? __fdividef(1.f, l) : 0.f;
+    __align__(16) __nv_bfloat162 ov[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ov[e] = __floats2bfloat162_rn(acc[2 * e] * inv, acc[2 * e + 1] * inv);
+    *reinterpret_cast<int4*>(a.out + (int64_t)row * a.ld_out + head * D + c8) = *reinterpret_cast<int4*>(ov);
+  }
+}
+
 }  // namespace tc
+
+// Query tiles per CTA of the grouped kernel; the planner sizes its items to match (ALORA_ATTN_MT=1 for A/B).
+int grp_query_tiles() {
+  static const int mt = getenv("ALORA_ATTN_MT") ? std::max(1, std::min(2, atoi(getenv("ALORA_ATTN_MT")))) : 2;
+  return mt;
+}
+
+template <int D, int MT>
+int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, cudaStream_t st) {
+  CUtensorMap tm{};
+  if (!make_tmap_2d(&tm, a.kv, (uint64_t)kv_rows, (uint64_t)a.Hkv * D, (uint64_t)a.Hkv * D, a.B, 64))
+    return ALORA_ECUDA;
+  const int smem = tc::SmemG<D, MT>::kTotal;
+  // cp.async producer warps: 2 with two query tiles per CTA, 4 with one at D=128; D=64 with one query tile runs
+  // two CTAs per SM (register bound) with the TMA producer. ALORA_ATTN_TMA=1 forces the TMA producer (A/B).
+  static const bool force_tma = getenv("ALORA_ATTN_TMA") != nullptr;
+  constexpr int PW = MT == 2 ? 2 : (D == 128 ? 4 : 0);
+  const bool use_pw = PW > 0 && !force_tma && a.B >= 4;
+  auto kern = use_pw ? tc::attn_grp_kernel<D, PW, MT> : tc::attn_grp_kernel<D, 0, MT>;
+  const int threads = use_pw ? tc::kGrpThreads<PW, MT> : tc::kGrpThreads<0, MT>;
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(tc::attn_grp_kernel<D, PW, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess ||
+        cudaFuncSetAttribute(tc::attn_grp_kernel<D, 0, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+            cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  tc::GrpArgs ta = a;
+  static const bool tracing = getenv("ALORA_ATTN_TRACE") != nullptr;
+  static unsigned long long* tbuf = nullptr;
+  const dim3 grid(n_items, a.Hkv);
+  const int n_ctas = n_items * a.Hkv;
+  if (tracing) {
+    if (!tbuf) cudaMalloc(&tbuf, sizeof(unsigned long long) * 6 * 65536);
+    cudaMemsetAsync(tbuf, 0, sizeof(unsigned long long) * 6 * std::min(n_ctas, 65536), st);
+    ta.trace = n_ctas <= 65536 ? tbuf : nullptr;
+  }
+  ALORA_CUDA_CHECK(launch_pdl(kern, grid, dim3(threads), smem, st, nullptr, 0, ta, tm));
+  ALORA_LAUNCH_CHECK();
+  if (tracing && ta.trace) {
+    std::vector<unsigned long long> h(6 * n_ctas);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), tbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    unsigned long long t0 = ~0ull, t1 = 0, longest = 0;
+    double ph[4] = {0, 0, 0, 0};
+    int live = 0;
+    for (int c = 0; c < n_ctas; ++c) {
+      if (!h[6 * c] || !h[6 * c + 4]) continue;
+      ++live;
+      t0 = std::min(t0, h[6 * c]);
+      t1 = std::max(t1, h[6 * c + 4]);
+      longest = std::max(longest, h[6 * c + 4] - h[6 * c]);
+      for (int p = 0; p < 4; ++p)
+        if (h[6 * c + p + 1] && h[6 * c + p]) ph[p] += double(h[6 * c + p + 1] - h[6 * c + p]);
+    }
+    if (live)
+      fprintf(stderr, "[attn grp trace] ctas %d/%d span %.2f us (longest CTA %.2f); mean start->Q %.2f, Q->S0 %.2f, "
+              "S0->last P %.2f, ->end %.2f us\n", live, n_ctas, (t1 - t0) / 1e3, longest / 1e3, ph[0] / live / 1e3,
+              ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3);
+  }
+  if (merge) {
+    ALORA_CUDA_CHECK(launch_pdl(tc::attn_grp_merge_kernel<D>, dim3(a.M), dim3(256), 0, st, nullptr, 0, ta));
+    ALORA_LAUNCH_CHECK();
+  }
+  return ALORA_OK;
+}
 
 // ============================================================================================================
 // Decode attention (every sequence of the step has ONE query row): G = H/Hkv query heads share a kv head, so
@@ -1263,6 +1869,43 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
   }
   const int64_t kv_rows = (int64_t)total_blocks * n_layers * 2 * B;
   return D == 64 ? launch_attn<64>(a, n_seqs, kv_rows, st) : launch_attn<128>(a, n_seqs, kv_rows, st);
+}
+
+int attn_grouped(const __nv_bfloat16* q, int64_t ld_q, int M, int S, const int32_t* positions, const int32_t* row_seq,
+                 const int32_t* block_table, int max_blocks, const int32_t* plan, int n_items, int n_segs, int n_sets,
+                 int max_np, bool merge, const __nv_bfloat16* kv, int total_blocks, int n_layers, int layer, int B,
+                 int H, int Hkv, int D, __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes,
+                 cudaStream_t st) {
+  if (M == 0 || n_items == 0) return ALORA_OK;
+  if (H % Hkv || (D != 64 && D != 128) || ld_q % 8 || ld_out % 8 || !plan || !positions || !row_seq ||
+      B > kKT || kKT % B || total_blocks < 1)
+    return ALORA_EINVAL;
+  const int64_t kv_rows = (int64_t)total_blocks * n_layers * 2 * B;
+  if (kv_rows >= (1ll << 31)) return ALORA_EINVAL;
+  tc::GrpArgs a{};
+  a.q = q; a.ld_q = ld_q; a.positions = positions; a.row_seq = row_seq; a.block_table = block_table;
+  a.max_blocks = max_blocks;
+  a.items = plan + 8;
+  a.segs = a.items + 8LL * n_items;
+  a.sets = a.segs + 4LL * n_segs;
+  a.set_tok = a.sets + 2LL * n_sets;
+  a.sp_np = a.set_tok + M;
+  a.kv = kv; a.n_layers = n_layers; a.layer = layer; a.B = B; a.H = H; a.Hkv = Hkv;
+  a.scale_log2 = 1.4426950408889634f / sqrtf((float)D);
+  a.out = out; a.ld_out = ld_out; a.M = M;
+  if (max_np > 1) {
+    const int64_t need = (int64_t)max_np * M * H * (D + 2) * 4;
+    if (!ws || ws_bytes < need) return ALORA_EINVAL;
+    a.ws_o = static_cast<float*>(ws);
+    a.ws_ml = a.ws_o + (int64_t)max_np * M * H * D;
+  }
+  static const int exp_mode = getenv("ALORA_ATTN_EXP") ? atoi(getenv("ALORA_ATTN_EXP")) : 0;
+  a.exp = exp_mode;
+  (void)S;
+  const bool mg = merge && max_np > 1;
+  if (grp_query_tiles() == 2)
+    return D == 64 ? launch_grp<64, 2>(a, n_items, mg, kv_rows, st) : launch_grp<128, 2>(a, n_items, mg, kv_rows, st);
+  return D == 64 ? launch_grp<64, 1>(a, n_items, mg, kv_rows, st) : launch_grp<128, 1>(a, n_items, mg, kv_rows, st);
 }
 
 }  // namespace alora

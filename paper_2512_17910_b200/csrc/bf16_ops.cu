@@ -507,6 +507,249 @@ int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_sl
   return ALORA_OK;
 }
 
+// ------------------------------------------------------------------------------------------------------------
+// Segmented LoRA shrink (model.py:141, `x @ down_t` of the rows that take the delta): the aLoRA eval step has
+// only the post-invocation rows (3 of a request's ~16-20 suffix rows) and decode rows on an adapter, a few
+// dozen per adapter, so the work is the adapter's down matrix streamed once (r x K bf16 per target) against
+// those rows -- bandwidth, not tensor throughput. One cluster of KS CTAs per (target, adapter slot), each CTA
+// one K slice:
+//   before the dependency wait  its down slice [R x Kc] streams into shared memory (cp.async; it does not
+//                               depend on the previous kernel, so the read overlaps the RMSNorm before)
+//   after it                    the slot's active rows (row_slot == slot and row_apply, in row order) are
+//                               listed, their h slices staged, and 8 warps compute [rows x R] partials over
+//                               K sub-slices with mma.sync m16n8k16 (ldmatrix from XOR-swizzled smem)
+//   reduction                   warps in warp order, then the cluster's CTAs in rank order through DSMEM
+//                               (deterministic), rank 0 writes s[t][row][slot*R + j] in bf16
+//   zero fill                   every other row's entries of this (t, slot) are written 0, so the expand GEMM
+//                               (extra K of the QKV GEMM) adds exact zeros there (base rows stay bitwise, model.py:145)
+// Rows are processed 64 at a time (any count is correct; the executor takes this path when each slot has at
+// most kSegMaxRows rows and the tensor-core shrink GEMM otherwise).
+constexpr int kSegThreads = 256;
+constexpr int kSegRowChunk = 64;
+
+__device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void seg_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32addr(dst)), "l"(src));
+}
+__device__ __forceinline__ void seg_ldsm4(uint32_t (&r)[4], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32addr(p)));
+}
+__device__ __forceinline__ void seg_mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// [rows][Kc] bf16 tile, 16-byte chunk c of row r at chunk (c ^ (r & 7))
+__device__ __forceinline__ int seg_off(int row, int k, int kc) {
+  const int c = (k >> 3) ^ (row & 7);
+  return row * kc + (c << 3) + (k & 7);
+}
+
+template <int R>
+__global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
+    const __nv_bfloat16* __restrict__ h, int M, int K, int KS, const int32_t* __restrict__ row_slot,
+    const uint8_t* __restrict__ row_apply, const __nv_bfloat16* __restrict__ down, int n_slots,
+    const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s) {
+  extern __shared__ __align__(128) uint8_t seg_smem[];
+  const int Kc = K / KS;
+  __nv_bfloat16* sd = reinterpret_cast<__nv_bfloat16*>(seg_smem);           // [R][Kc] down slice
+  __nv_bfloat16* sh = sd + R * Kc;                                           // [kSegRowChunk][Kc] h rows
+  float* red = reinterpret_cast<float*>(sh + kSegRowChunk * Kc);            // [kSegRowChunk][R] CTA partial
+  int* rows = reinterpret_cast<int*>(red + kSegRowChunk * R);               // active rows of this slot
+  __shared__ int warp_cnt[kSegThreads / 32];
+  const int t = blockIdx.x / n_slots, slot = blockIdx.x % n_slots;
+  const int rank = blockIdx.y;  // == cluster rank (cluster dims (1, KS, 1))
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int k0 = rank * Kc;
+  const int ldS = n_slots * R;
+  const bool targeted = (slot_targets[slot] >> t) & 1;
+  // down slice: independent of the previous kernel
+  if (targeted) {
+    const __nv_bfloat16* dsrc = down + (((int64_t)t * n_slots + slot) * R) * K + k0;
+    for (int i = tid; i < R * (Kc / 8); i += kSegThreads) {
+      const int j = i / (Kc / 8), c = i % (Kc / 8);
+      seg_cp16(sd + seg_off(j, c * 8, Kc), dsrc + (int64_t)j * K + c * 8);
+    }
+    asm volatile("cp.async.commit_group;");
+  }
+  pdl_wait();
+  pdl_trigger();
+  // active rows in row order: per-warp counts over contiguous row ranges, then a prefix over warps
+  const int per_warp = (M + (kSegThreads / 32) - 1) / (kSegThreads / 32);
+  const int r_lo = warp * per_warp, r_hi = min(M, r_lo + per_warp);
+  int cnt = 0;
+  for (int r = r_lo + lane; r - lane < r_hi; r += 32) {
+    const bool act = r < r_hi && row_slot[r] == slot && row_apply[r];
+    cnt += __popc(__ballot_sync(0xffffffffu, act));
+  }
+  if (lane == 0) warp_cnt[warp] = cnt;
+  __syncthreads();
+  int base = 0, n_act = 0;
+  for (int w = 0; w < kSegThreads / 32; ++w) {
+    if (w < warp) base += warp_cnt[w];
+    n_act += warp_cnt[w];
+  }
+  // (rows[] holds at most kSegRowChunk entries per pass; larger counts are re-listed per chunk below)
+  // zero every inactive row of this (t, slot): ranks split the rows
+  {
+    const int rows_per = (M + KS - 1) / KS;
+    const int z0 = rank * rows_per, z1 = min(M, z0 + rows_per);
+    for (int i = tid; i < (z1 - z0) * (R / 8); i += kSegThreads) {
+      const int r = z0 + i / (R / 8), c = (i % (R / 8)) * 8;
+      if (targeted && row_slot[r] == slot && row_apply[r]) continue;
+      *reinterpret_cast<int4*>(s + ((int64_t)t * M + r) * ldS + slot * R + c) = make_int4(0, 0, 0, 0);
+    }
+  }
+  if (!targeted || n_act == 0) return;  // uniform over the cluster: every rank sees the same counts
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  for (int c0 = 0; c0 < n_act; c0 += kSegRowChunk) {
+    const int nc = min(kSegRowChunk, n_act - c0);
+    __syncthreads();  // the previous chunk's rows / red are no longer read
+    // list the chunk's rows (active ordinal in [c0, c0 + nc))
+    {
+      int ord = base;
+      for (int r = r_lo + lane; r - lane < r_hi; r += 32) {
+        const bool act = r < r_hi && row_slot[r] == slot && row_apply[r];
+        const unsigned b = __ballot_sync(0xffffffffu, act);
+        const int my = ord + __popc(b & ((1u << lane) - 1));
+        if (act && my >= c0 && my < c0 + nc) rows[my - c0] = r;
+        ord += __popc(b);
+      }
+    }
+    __syncthreads();
+    const int n_rt = (nc + 15) / 16;
+    for (int i = tid; i < n_rt * 16 * (Kc / 8); i += kSegThreads) {
+      const int rr = i / (Kc / 8), c = i % (Kc / 8);
+      if (rr < nc) seg_cp16(sh + seg_off(rr, c * 8, Kc), h + (int64_t)rows[rr] * K + k0 + c * 8);
+      else *reinterpret_cast<int4*>(sh + seg_off(rr, c * 8, Kc)) = make_int4(0, 0, 0, 0);
+    }
+    asm volatile("cp.async.commit_group;");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    // warp w: k sub-slices w, w + 8, ... of 16; partial [n_rt*16][R] in registers
+    float acc[kSegRowChunk / 16][R / 8][4];
+#pragma unroll
+    for (int a = 0; a < kSegRowChunk / 16; ++a)
+#pragma unroll
+      for (int f = 0; f < R / 8; ++f)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[a][f][e] = 0.f;
+    for (int ks = warp * 16; ks < Kc; ks += 16 * (kSegThreads / 32)) {
+      uint32_t bfr[R / 8][2];
+#pragma unroll
+      for (int f = 0; f < R / 8; f += 2) {
+        uint32_t r4[4];
+        const int j = f * 8 + (lane & 7) + ((lane >> 4) << 3);
+        const int kk = ks + ((lane >> 3) & 1) * 8;
+        seg_ldsm4(r4, sd + seg_off(j, kk, Kc));
+        bfr[f][0] = r4[0];
+        bfr[f][1] = r4[1];
+        if (f + 1 < R / 8) {
+          bfr[f + 1][0] = r4[2];
+          bfr[f + 1][1] = r4[3];
+        }
+      }
+#pragma unroll
+      for (int a = 0; a < kSegRowChunk / 16; ++a) {
+        if (a >= n_rt) break;
+        uint32_t afr[4];
+        const int rr = a * 16 + (lane & 15);
+        const int kk = ks + (lane >> 4) * 8;
+        seg_ldsm4(afr, sh + seg_off(rr, kk, Kc));
+#pragma unroll
+        for (int f = 0; f < R / 8; ++f) seg_mma(acc[a][f], afr, bfr[f][0], bfr[f][1]);
+      }
+    }
+    // CTA reduction in warp order: warp 0 stores, then warps 1..7 add in turn
+    for (int w = 0; w < kSegThreads / 32; ++w) {
+      if (warp == w) {
+#pragma unroll
+        for (int a = 0; a < kSegRowChunk / 16; ++a) {
+          if (a >= n_rt) break;
+#pragma unroll
+          for (int f = 0; f < R / 8; ++f) {
+            const int r0 = a * 16 + (lane >> 2), c = f * 8 + (lane & 3) * 2;
+            float* p0 = red + r0 * R + c;
+            float* p1 = red + (r0 + 8) * R + c;
+            if (w == 0) {
+              p0[0] = acc[a][f][0]; p0[1] = acc[a][f][1]; p1[0] = acc[a][f][2]; p1[1] = acc[a][f][3];
+            } else {
+              p0[0] += acc[a][f][0]; p0[1] += acc[a][f][1]; p1[0] += acc[a][f][2]; p1[1] += acc[a][f][3];
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // cluster reduction in rank order on rank 0, through DSMEM
+    if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+    if (rank == 0) {
+      for (int i = tid; i < nc * R; i += kSegThreads) {
+        float v = red[i];
+        for (int q = 1; q < KS; ++q) {
+          uint32_t ra;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32addr(red + i)), "r"(q));
+          float x;
+          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
+          v += x;
+        }
+        const int rr = i / R, j = i % R;
+        s[((int64_t)t * M + rows[rr]) * ldS + slot * R + j] = __float2bfloat16_rn(v);
+      }
+    }
+    if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+  }
+}
+
+template <int R>
+int launch_shrink_seg(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+                      const __nv_bfloat16* down, int n_slots, const uint8_t* slot_targets, __nv_bfloat16* s,
+                      cudaStream_t st) {
+  auto smem_of = [](int kc) {
+    return (size_t)R * kc * 2 + (size_t)kSegRowChunk * kc * 2 + (size_t)kSegRowChunk * R * 4 + kSegRowChunk * 4;
+  };
+  int KS = 1;
+  while ((K / KS > 1024 || smem_of(K / KS) > 200 * 1024) && KS < 8) KS *= 2;
+  if (K % (KS * 16) != 0 || smem_of(K / KS) > 220 * 1024) return ALORA_EINVAL;
+  const int Kc = K / KS;
+  const size_t smem = smem_of(Kc);
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(lora_shrink_seg_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return ALORA_ECUDA;
+    configured = true;
+  }
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = KS;
+  attr[0].val.clusterDim.z = 1;
+  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_seg_kernel<R>, dim3(3 * n_slots, KS), dim3(kSegThreads), smem, st, attr,
+                              KS > 1 ? 1 : 0, h, M, K, KS, row_slot, row_apply, down, n_slots, slot_targets, s));
+  ALORA_LAUNCH_CHECK();
+  return ALORA_OK;
+}
+
+int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+                         const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
+                         __nv_bfloat16* s, cudaStream_t st) {
+  if (M == 0 || n_slots == 0) return ALORA_OK;
+  if (K % 128 != 0) return ALORA_EINVAL;
+  switch (R) {
+    case 8: return launch_shrink_seg<8>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
+    case 16: return launch_shrink_seg<16>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
+    case 32: return launch_shrink_seg<32>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
+    case 64: return launch_shrink_seg<64>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
+    default: return ALORA_EINVAL;
+  }
+}
+
 // One 32-bit mask per 128-row GEMM tile: bit `slot` set when any row of the tile takes that adapter's delta.
 __global__ void lora_tile_masks_kernel(const int32_t* __restrict__ row_slot, const uint8_t* __restrict__ row_apply,
                                        int M, uint32_t* __restrict__ masks) {

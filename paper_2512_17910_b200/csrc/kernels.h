@@ -49,6 +49,13 @@ int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const f
 int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                      const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets, __nv_bfloat16* s,
                      cudaStream_t st);
+// Segmented shrink for steps with few delta rows per adapter: one CTA cluster per (target, slot) streams the
+// adapter's down rows once (K split over the cluster, DSMEM reduction in rank order), mma.sync over the
+// slot's active rows; writes the same [3][M][n_slots*R] layout (zeros elsewhere). R in {8, 16, 32, 64}.
+int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+                         const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
+                         __nv_bfloat16* s, cudaStream_t st);
+constexpr int kSegMaxRows = 128;  // the executor's switch: at most this many delta rows per adapter slot
 int rope_bf16(__nv_bfloat16* qkv, int ld, const int32_t* positions, int M, int H, int Hkv, int D,
               const float* cos_t, const float* sin_t, cudaStream_t st);
 int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int32_t* cu_q,
@@ -57,6 +64,14 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
               __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes, cudaStream_t st,
               int total_blocks = 0 /* > 0 enables the TMA / tcgen05 kernel */);
 int64_t attn_bf16_workspace(int M, int n_seqs, int max_q, int max_ctx, int H, int Hkv, int D);
+// Shared-prefix attention over an alora_plan_attention work list (on the device): query sets of requests
+// that hold the same physical prefix blocks stream that prefix once; KV-partition partials (max_np > 1) are
+// combined by a merge launch in partition order.
+int attn_grouped(const __nv_bfloat16* q, int64_t ld_q, int M, int S, const int32_t* positions, const int32_t* row_seq,
+                 const int32_t* block_table, int max_blocks, const int32_t* plan, int n_items, int n_segs, int n_sets,
+                 int max_np, bool merge, const __nv_bfloat16* kv, int total_blocks, int n_layers, int layer, int B,
+                 int H, int Hkv, int D, __nv_bfloat16* out, int64_t ld_out, void* ws, int64_t ws_bytes,
+                 cudaStream_t st);
 int64_t attn_bf16_workspace_bound(int H, int D);
 
 // tcgen05 GEMM: C = epi(A[M,K] @ Bt[N,K]^T (+ S_t[M,Ks] @ Ut[N,Ks]^T lora part)), bf16 in, fp32 accumulate.

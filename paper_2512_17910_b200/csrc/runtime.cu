@@ -69,7 +69,8 @@ struct GraphEntry {
   int32_t launches = 0;
   uint64_t last_use = 0;
 };
-using GraphKey = std::tuple<int, int, int, int, int>;  // n_tokens, n_seqs, max_blocks, max_q, max_ctx
+// n_tokens, n_seqs, max_blocks, max_q, max_ctx, attention items, attention partitions (the grids a capture bakes in)
+using GraphKey = std::tuple<int, int, int, int, int, int, int>;
 
 struct Model {
   AloraModelDesc d;
@@ -282,6 +283,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const int Nq = H * D, Nkv = Hkv * D, Nqkv = Nq + 2 * Nkv;
   const bool llama = d.arch == ALORA_ARCH_LLAMA;
   const bool lora = d.n_slots > 0;
+  const int rk = d.lora_rank;
+  const bool seg_shrink = lora && s.lora_rows_max <= kSegMaxRows && d.d_model % 128 == 0 &&
+                          (rk == 8 || rk == 16 || rk == 32 || rk == 64);
   Launcher run{mdl, st};
   const bool tp = d.tp_size > 1;
   float* tpd = reinterpret_cast<float*>(base + w.tpd);
@@ -325,10 +329,19 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
         residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     pend = 0;
     GemmLora gl;
-    if (lora) {
+    if (lora && seg_shrink) {
+      // few delta rows per adapter: stream each adapter's down rows once against its rows (+ the zero fill)
+      const double act = s.lora_rows_max;
+      RUN("lora_shrink", 3.0 * d.n_slots * d.lora_rank * dm_ * 2 + d.n_slots * act * dm_ * 2 + 3.0 * m_ * ks_ * 2,
+          2.0 * 3 * d.n_slots * act * d.lora_rank * dm_,
+          lora_shrink_seg_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
+                               d.n_slots, d.lora_rank, d.slot_targets, sws, st));
+    } else if (lora) {
       RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
           shrink(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]), d.n_slots,
                  d.lora_rank, d.slot_targets, sws, st, gw, part, w.part_bytes, &run.n));
+    }
+    if (lora) {
       gl.s = sws;
       gl.up_t = static_cast<const __nv_bfloat16*>(mdl.lora_up_t[l]);
       gl.ks = d.n_slots * d.lora_rank;
@@ -359,10 +372,18 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
           kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                    d.block_size, st));
     }
-    RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
-        attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
-                  static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
-                  aws, w.attn_ws_bytes, st, d.total_blocks));
+    if (s.attn_plan != nullptr) {  // shared-prefix plan: each group's prefix KV streamed once for all its rows
+      RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
+          attn_grouped(qkv, Nqkv, M, S, s.positions, s.row_seq, s.block_table, s.max_blocks, s.attn_plan,
+                       s.attn_items, s.attn_segs, s.attn_sets, s.attn_max_parts, true,
+                       static_cast<const __nv_bfloat16*>(d.kv_pool), d.total_blocks, d.n_layers, l, d.block_size, H,
+                       Hkv, D, attn, Nq, aws, w.attn_ws_bytes, st));
+    } else {
+      RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
+          attn_bf16(qkv, Nqkv, M, S, s.cu_q, s.start_pos, s.block_table, s.max_blocks, s.max_q, s.max_ctx,
+                    static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
+                    aws, w.attn_ws_bytes, st, d.total_blocks));
+    }
     RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
         residual_gemm(attn, Nq, mdl.w_o_t[l], Nq));
     if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
@@ -485,6 +506,30 @@ int alora_paged_prefill_attn(int32_t dtype, const void* q, int64_t ld_q, int32_t
                    workspace_bytes, st, total_blocks);
 }
 
+int64_t alora_attn_partial_capacity(int32_t n_heads, int32_t head_dim) {
+  if (n_heads < 1 || head_dim < 1) return ALORA_EINVAL;
+  return attn_bf16_workspace_bound(n_heads, head_dim) - 4096 * 4;  // the executor's buffer minus merge counters
+}
+
+int alora_paged_prefix_attn(const void* q, int64_t ld_q, int32_t n_rows, int32_t n_seqs, const int32_t* positions,
+                            const int32_t* row_seq, const int32_t* block_table, int32_t max_blocks,
+                            const int32_t* plan, int32_t n_items, int32_t n_segs, int32_t n_sets, int32_t max_parts,
+                            const void* kv_pool, int32_t total_blocks, int32_t n_layers, int32_t layer,
+                            int32_t block_size, int32_t n_heads, int32_t n_kv_heads, int32_t head_dim, void* out,
+                            int64_t ld_out, void* workspace, int64_t workspace_bytes, void* stream) {
+  if (n_rows < 0 || n_seqs < 0 || n_items < 0 || n_segs < 0 || n_sets < 0 || max_parts < 1 || n_heads < 1 ||
+      n_kv_heads < 1 || n_heads % n_kv_heads || layer < 0 || layer >= n_layers || max_blocks < 1)
+    return ALORA_EINVAL;
+  if (n_rows == 0 || n_items == 0) return ALORA_OK;
+  if (!q || !positions || !row_seq || !block_table || !plan || !kv_pool || !out) return ALORA_EINVAL;
+  configure_kernels();
+  return attn_grouped(static_cast<const __nv_bfloat16*>(q), ld_q, n_rows, n_seqs, positions, row_seq, block_table,
+                      max_blocks, plan, n_items, n_segs, n_sets, max_parts, true,
+                      static_cast<const __nv_bfloat16*>(kv_pool), total_blocks, n_layers, layer, block_size, n_heads,
+                      n_kv_heads, head_dim, static_cast<__nv_bfloat16*>(out), ld_out, workspace, workspace_bytes,
+                      static_cast<cudaStream_t>(stream));
+}
+
 int64_t alora_attn_workspace_bytes(int32_t dtype, int32_t n_rows, int32_t n_seqs, int32_t max_q, int32_t max_ctx,
                                    int32_t n_heads, int32_t n_kv_heads, int32_t head_dim) {
   if (dtype != ALORA_BF16) return 0;
@@ -573,7 +618,8 @@ int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream) {
 static bool same_step_buffers(const AloraStepDesc& a, const AloraStepDesc& b) {
   return a.tokens == b.tokens && a.positions == b.positions && a.slot_mapping == b.slot_mapping &&
          a.row_slot == b.row_slot && a.row_apply == b.row_apply && a.cu_q == b.cu_q && a.start_pos == b.start_pos &&
-         a.block_table == b.block_table && a.last_row == b.last_row && a.logits == b.logits && a.next_ids == b.next_ids;
+         a.block_table == b.block_table && a.last_row == b.last_row && a.logits == b.logits && a.next_ids == b.next_ids &&
+         a.row_seq == b.row_seq && a.attn_plan == b.attn_plan && a.attn_segs == b.attn_segs && a.attn_sets == b.attn_sets;
 }
 
 int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream) {
@@ -583,7 +629,9 @@ int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* str
   if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
     return ALORA_EINVAL;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  const GraphKey key{step->n_tokens, step->n_seqs, step->max_blocks, step->max_q, step->max_ctx};
+  const GraphKey key{step->n_tokens, step->n_seqs, step->max_blocks, step->max_q, step->max_ctx,
+                     step->attn_plan ? step->attn_items : -1,
+                     (step->attn_plan ? step->attn_max_parts : -1) * 2 + (step->lora_rows_max <= kSegMaxRows ? 1 : 0)};
   auto it = m.graphs.find(key);
   if (it != m.graphs.end() && !same_step_buffers(it->second.step, *step)) {
     cudaGraphExecDestroy(it->second.exec);

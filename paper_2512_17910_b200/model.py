@@ -119,11 +119,19 @@ class Model:
     GRAPH_BLOCK_BUCKET = 32  # decode steps pad the block table to a multiple of this many blocks
 
     def __init__(self, config: ModelConfig | None = None, weights: BaseWeights | None = None, init: str = "philox",
-                 max_tokens: int = 2048, max_seqs: int = 256, graphs: bool = True):
+                 max_tokens: int = 2048, max_seqs: int = 256, graphs: bool = True, shared_prefix: bool = True):
         torch = _native.require_cuda()
         self._torch = torch
         # decode steps (one row per span, bf16) replay a captured CUDA graph of the whole forward
         self._graphs = bool(graphs) and (config or ModelConfig()).dtype == "bf16"
+        c0 = config or ModelConfig()
+        # shared-prefix attention: spans holding the same leading blocks (adapters on one conversation) read
+        # that prefix once (alora_plan_attention + the grouped kernel); ALORA_SHARED_PREFIX=0 disables it (A/B)
+        import os
+        self._shared_prefix = (bool(shared_prefix) and c0.dtype == "bf16" and c0.head_dim in (64, 128)
+                               and os.environ.get("ALORA_SHARED_PREFIX", "1") != "0")
+        self._attn_partial_cap = int(_native.lib.alora_attn_partial_capacity(c0.n_heads, c0.head_dim)) \
+            if c0.dtype == "bf16" else 0
         self._prefill_shapes = {}  # prefill step shape -> times seen (graph capture from the second)
         self._graph_stream = torch.cuda.Stream() if self._graphs else None
         self._staged_graphable = False
@@ -433,19 +441,53 @@ class Model:
             bt[i, :len(tb)] = tb
         slot_map = (bt[row_seq, positions // block_size] * block_size + positions % block_size).astype(np.int32)
         ends = starts_a + lens_a
+        plan, kv_tokens = None, float(ends.sum())
+        if getattr(self, "_shared_prefix", False) and S >= 2:
+            plan = self._plan_attention(cu, starts_a.astype(np.int32), bt, block_size)
+            if plan is not None:
+                kv_tokens = float(plan[5])  # distinct keys: a shared prefix is read once
+        row_slot = np.repeat(np.asarray(slot_ids, dtype=np.int32), lens_a)
+        take = row_slot[(row_slot >= 0) & (row_apply != 0)]
         return {
-            "attn_kv_tokens": float(ends.sum()),
+            "lora_rows_max": int(np.bincount(take).max()) if take.size else 0,
+            "attn_plan": plan, "row_seq": row_seq.astype(np.int32),
+            "attn_kv_tokens": kv_tokens,
             "attn_qk_pairs": float((lens_a * (starts_a + (lens_a + 1) / 2)).sum()),
             "M": M, "S": S, "maxb": maxb, "max_q": int(lens_a.max()),
             "max_ctx": maxb * block_size if graphable else int(ends.max()),
             "graphable": graphable,
             "tokens": tokens.astype(np.int32), "positions": positions, "slot_mapping": slot_map,
-            "row_slot": np.repeat(np.asarray(slot_ids, dtype=np.int32), lens_a), "row_apply": row_apply,
+            "row_slot": row_slot, "row_apply": row_apply,
             "cu_q": cu, "start_pos": starts_a.astype(np.int32), "last_row": (cu[1:] - 1).astype(np.int32),
             "block_table": bt,
         }
 
-    _FIELDS = ("tokens", "positions", "slot_mapping", "row_slot", "cu_q", "start_pos", "last_row", "block_table")
+    def _plan_attention(self, cu, starts, bt, block_size):
+        """Shared-prefix attention plan (alora_plan_attention) for steps whose spans hold the same leading
+        physical blocks (adapters evaluated on one conversation); None when no span shares a prefix."""
+        cfg = self.config
+        S, maxb = bt.shape
+        if block_size > 64 or 64 % block_size:  # the kernel's TMA page boxes tile a 64-key tile
+            return None
+        cap = 8 + 64 * (int(cu[-1]) + S) + 4096
+        for _ in range(2):
+            out = np.empty(cap, dtype=np.int32)
+            n = _native.lib.alora_plan_attention(S, cu.ctypes.data, starts.ctypes.data, bt.ctypes.data, maxb,
+                                                 block_size, cfg.n_heads, cfg.kv_heads, cfg.head_dim, 1,
+                                                 self._attn_partial_cap, out.ctypes.data, cap)
+            if n >= 0:
+                break
+            if n == _native.ALORA_EINVAL:
+                _native.check(int(n), "alora_plan_attention")
+            cap = int(-n)
+        else:
+            raise RuntimeError("alora_plan_attention: plan buffer sizing failed")
+        if int(out[2]) == S:  # no group formed: the per-span kernels serve the step
+            return None
+        return out[:n]
+
+    _FIELDS = ("tokens", "positions", "slot_mapping", "row_slot", "cu_q", "start_pos", "last_row", "block_table",
+               "row_seq")
 
     def run_packed(self, p: dict, kv, want_logits: bool = True):
         """One native forward over a packed step. Returns (next_ids[S], logits[S, V] or None) on the host."""
@@ -506,8 +548,10 @@ class Model:
         self._check_pool(kv)
         self._grow_workspace(p["M"])
         handle = self._native_handle(kv)
+        plan = p.get("attn_plan")
         parts = [p[f] for f in self._FIELDS]
-        sizes = [x.size for x in parts] + [(len(p["row_apply"]) + 3) // 4]  # row_apply: bytes packed in int32
+        # row_apply: bytes packed in int32, then the attention plan (if any)
+        sizes = [x.size for x in parts] + [(len(p["row_apply"]) + 3) // 4] + [0 if plan is None else plan.size]
         offs = np.cumsum([0] + sizes)
         total = int(offs[-1])
         if total > self._steps.cap:
@@ -518,9 +562,11 @@ class Model:
         host = self._steps.host.numpy()
         for i, x in enumerate(parts):  # straight into the pinned staging buffer (no intermediate concatenation)
             host[offs[i]:offs[i + 1]] = np.asarray(x).reshape(-1)
-        ap = host[offs[-2]:offs[-1]].view(np.uint8)
+        ap = host[offs[-3]:offs[-2]].view(np.uint8)
         ap[:len(p["row_apply"])] = p["row_apply"]
         ap[len(p["row_apply"]):] = 0
+        if plan is not None:
+            host[offs[-2]:offs[-1]] = plan
         dev = self._steps.dev
         dev[:total].copy_(self._steps.host[:total], non_blocking=True)
         base = dev.data_ptr()
@@ -533,6 +579,11 @@ class Model:
         st.row_apply = base + 4 * int(offs[len(self._FIELDS)])
         st.logits, st.next_ids = self._logits.data_ptr(), self._ids.data_ptr()
         st.attn_kv_tokens, st.attn_qk_pairs = p.get("attn_kv_tokens", 0.0), p.get("attn_qk_pairs", 0.0)
+        st.row_seq = ptr["row_seq"]
+        st.lora_rows_max = p.get("lora_rows_max", 1 << 30)
+        if plan is not None:
+            st.attn_plan = base + 4 * int(offs[-2])
+            st.attn_items, st.attn_segs, st.attn_sets, st.attn_max_parts = (int(x) for x in plan[:4])
         self._staged_graphable = bool(p.get("graphable", False))
         self.last_h2d_bytes = 4 * total
         return st

@@ -512,3 +512,91 @@ def test_batched_hashing_after_fork():
     got = q.get(timeout=30)
     pr.join(timeout=30)
     assert pr.exitcode == 0 and got == want
+
+
+def _plan(cu, starts, tables, B=16, H=32, Hkv=8, D=128, flags=1, cap=1 << 30):
+    import ctypes  # noqa: F401
+    S = len(starts)
+    maxb = max(len(t) for t in tables)
+    bt = np.zeros((S, maxb), np.int32)
+    for i, t in enumerate(tables):
+        bt[i, :len(t)] = t
+    cu = np.asarray(cu, np.int32)
+    st = np.asarray(starts, np.int32)
+    out = np.empty(1 << 20, np.int32)
+    n = P._native.lib.alora_plan_attention(S, cu.ctypes.data, st.ctypes.data, bt.ctypes.data, maxb, B, H, Hkv, D,
+                                           flags, cap, out.ctypes.data, out.size)
+    assert n > 0
+    out = out[:n]
+    ni, ns, nq = int(out[0]), int(out[1]), int(out[2])
+    items = out[8:8 + 8 * ni].reshape(ni, 8)
+    segs = out[8 + 8 * ni:8 + 8 * ni + 4 * ns].reshape(ns, 4)
+    o = 8 + 8 * ni + 4 * ns
+    sets = out[o:o + 2 * nq].reshape(nq, 2)
+    M = int(cu[-1])
+    set_tok = out[o + 2 * nq:o + 2 * nq + M]
+    sp_np = out[o + 2 * nq + M:o + 2 * nq + M + S]
+    return out, items, segs, sets, set_tok, sp_np, bt
+
+
+@pytest.mark.parametrize("case", ["eval_groups", "decode_groups", "mixed", "long_prefill"])
+def test_attention_plan_covers_every_key_once(case):
+    """alora_plan_attention (host): for every (row, head) the plan's items x segments visit exactly the keys
+    [0, pos] of the row's own sequence, each once, through block tables that map them to the row's own
+    physical blocks; spans holding the same leading blocks are grouped (shared prefix read once)."""
+    rng = np.random.default_rng(3)
+    B, H, Hkv, G = 16, 32, 8, 4
+    if case in ("eval_groups", "decode_groups"):
+        n_conv, n_ad, cached = 3, 4, 1000 // 16 * 16
+        lens = [1 if case == "decode_groups" else 20] * (n_conv * n_ad)
+        starts, tables, nb = [], [], 0
+        conv_blocks = [list(range(c * 200, c * 200 + cached // B)) for c in range(n_conv)]
+        for c in range(n_conv):
+            for k in range(n_ad):
+                st = cached + (7 if case == "decode_groups" else 0) + k
+                total = st + lens[len(starts)]
+                own = list(range(5000 + len(starts) * 10, 5000 + len(starts) * 10 + 10))
+                tables.append(conv_blocks[c] + own[:-(-total // B) - len(conv_blocks[c])])
+                starts.append(st)
+    elif case == "mixed":
+        starts = [0, 300, 300, 40, 2000]
+        lens = [70, 9, 9, 33, 1]
+        shared = list(range(100, 120))
+        tables = [list(range(0, 5)), shared + [900, 901, 902], shared + [910, 911], list(range(30, 35)),
+                  list(range(40, 166))]
+        tables[2] = tables[2] + [912]
+    else:
+        starts, lens = [0, 0], [700, 300]
+        tables = [list(range(0, 44)), list(range(50, 69))]
+    cu = np.concatenate([[0], np.cumsum(lens)])
+    out, items, segs, sets, set_tok, sp_np, bt = _plan(cu, starts, tables, B, H, Hkv)
+    M = int(cu[-1])
+    row_span = np.repeat(np.arange(len(starts)), lens)
+    pos = np.concatenate([np.arange(s, s + n) for s, n in zip(starts, lens)])
+    seen = {}  # (row, head) -> list of physical (block, offset) keys
+    for it in items:
+        q, mt, sb, se, p_index = (int(x) for x in it[:5])
+        off, n_tok = sets[q]
+        QT = 128 * int(os.environ.get("ALORA_ATTN_MT", "2"))  # query rows per item (the kernel's tiles per CTA)
+        for r in range(QT):
+            pr = mt * QT + r
+            if pr >= n_tok * G:
+                break
+            row = int(set_tok[off + pr // G])
+            head = pr % G
+            for tab, lo, hi, flt in segs[sb:se]:
+                if flt >= 0 and flt != row_span[row]:
+                    continue
+                lim = min(pos[row], hi - 1)
+                for k in range(lo, lim + 1):
+                    seen.setdefault((row, head), []).append((int(bt[tab, k // B]), k % B))
+    for row in range(M):
+        want = [(tables[row_span[row]][k // B], k % B) for k in range(pos[row] + 1)]
+        for head in range(G):
+            assert sorted(seen[(row, head)]) == sorted(want), (case, row, head)
+    assert sorted(set_tok.tolist()) == list(range(M))
+    if case.endswith("groups"):
+        assert int(out[2]) == 3  # one set per conversation
+        assert int(out[5]) < sum(s + n for s, n in zip(starts, lens)) // 3  # distinct keys: prefixes counted once
+    if case == "mixed":
+        assert int(out[2]) == 4  # the two spans on the shared blocks form one set
