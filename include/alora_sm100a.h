@@ -108,6 +108,40 @@ int32_t alora_pool_index_get(void* pool, const uint8_t* digest);
 /* Index entries (cap <= 0: just the count). */
 int64_t alora_pool_index_dump(void* pool, uint8_t* digests, int32_t* ids, int64_t cap);
 
+/* ------------------------------------------------------ native admission ---- */
+/* The engine's scheduler and per-request block tables on top of a block manager (csrc/sched_core.cpp):
+ * scheduler.py:139-265 (intake, schedule_step, prefix lookup, block allocation, on_span_done) and the
+ * per-request half of kv_cache.py:154-271 (lookup walk, set_fill, commit_and_free, release). */
+void* alora_sched_create(void* pool, int32_t block_size, int32_t token_budget, int32_t max_batch,
+                         int32_t chunked, int32_t prefix_caching, int32_t hash_threads);
+void alora_sched_destroy(void* sched);
+/* Thread-safe intake (ticket order = call order). mode: 0 base, 1 standard LoRA, 2 activated (inv_start
+ * = invocation start). key = the adapter id (block-hash extra key). Returns the request handle (>= 0). */
+int32_t alora_sched_submit(void* sched, const int64_t* prompt, int64_t n, int32_t max_new, int32_t mode,
+                           const char* key, int32_t key_len, int64_t inv_start);
+int32_t alora_sched_has_work(void* sched);
+/* One schedule_step. spans[i] = {handle, start, end, kind} (kind: 0 prefill, 1 decode, +256 = the request's
+ * first scheduled work); failed = requests failed this step (pool exhausted during decode); looked = requests
+ * whose prefix lookup ran this step; counts = {n_spans, n_failed, n_looked, budget_used}; blocks/block_off =
+ * each span's block table (the request's block ids in position order), concatenated. */
+int alora_sched_step(void* sched, int32_t* spans, int32_t span_cap, int32_t* failed, int32_t failed_cap,
+                     int32_t* looked, int32_t looked_cap, int32_t* counts, int32_t* blocks, int64_t block_cap,
+                     int64_t* block_off);
+/* The step's spans are done (on_span_done + set_fill for each): emitted token (if has_emitted; a
+ * placeholder is fixed later with alora_sched_set_token). flags_out: bit 0 prompt completed (-> decoding),
+ * bit 1 finished. */
+int alora_sched_step_done(void* sched, int32_t n, const int32_t* handles, const int32_t* starts,
+                          const int32_t* ends, const int64_t* emitted, const uint8_t* has_emitted,
+                          uint8_t* flags_out);
+int alora_sched_set_token(void* sched, int32_t handle, int64_t gen_index, int64_t token);
+/* Retire a finished request: commit_and_free (publish its full blocks, release tail first) or, for a
+ * failed request, release. */
+int alora_sched_retire(void* sched, int32_t handle);
+/* {processed, hit tokens, computed tokens, generated, state, blocks held, blocks reused, failed} */
+int alora_sched_info(void* sched, int32_t handle, int64_t* out8);
+int64_t alora_sched_blocks(void* sched, int32_t handle, int32_t* out, int64_t cap);
+int64_t alora_sched_owned_total(void* sched);
+
 /* ------------------------------------------------------ hot-path kernels ---- */
 
 /* Masked multi-adapter aLoRA Q/K/V projection (model.py:117-146).

@@ -106,6 +106,20 @@ EXPORTS = {
     "alora_pool_free_list": _sig("alora_pool_free_list", c_i64, c_void_p, c_void_p, c_i64),
     "alora_pool_index_get": _sig("alora_pool_index_get", c_i32, c_void_p, c_void_p),
     "alora_pool_index_dump": _sig("alora_pool_index_dump", c_i64, c_void_p, c_void_p, c_void_p, c_i64),
+    "alora_sched_create": _sig("alora_sched_create", c_void_p, c_void_p, c_i32, c_i32, c_i32, c_i32, c_i32, c_i32),
+    "alora_sched_destroy": _sig("alora_sched_destroy", None, c_void_p),
+    "alora_sched_submit": _sig("alora_sched_submit", c_i32, c_void_p, c_void_p, c_i64, c_i32, c_i32, ctypes.c_char_p,
+                               c_i32, c_i64),
+    "alora_sched_has_work": _sig("alora_sched_has_work", c_i32, c_void_p),
+    "alora_sched_step": _sig("alora_sched_step", c_i32, c_void_p, c_void_p, c_i32, c_void_p, c_i32, c_void_p, c_i32,
+                             c_void_p, c_void_p, c_i64, c_void_p),
+    "alora_sched_step_done": _sig("alora_sched_step_done", c_i32, c_void_p, c_i32, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, c_void_p, c_void_p),
+    "alora_sched_set_token": _sig("alora_sched_set_token", c_i32, c_void_p, c_i32, c_i64, c_i64),
+    "alora_sched_retire": _sig("alora_sched_retire", c_i32, c_void_p, c_i32),
+    "alora_sched_info": _sig("alora_sched_info", c_i32, c_void_p, c_i32, c_void_p),
+    "alora_sched_blocks": _sig("alora_sched_blocks", c_i64, c_void_p, c_i32, c_void_p, c_i64),
+    "alora_sched_owned_total": _sig("alora_sched_owned_total", c_i64, c_void_p),
     "alora_qkv_proj": _sig("alora_qkv_proj", c_i32, c_i32, c_void_p, c_i32, c_i32, c_void_p, c_i32, c_i32,
                            c_void_p, c_void_p, c_void_p, c_void_p, c_i32, c_i32, c_void_p, c_void_p, c_void_p,
                            c_i32, c_void_p),

@@ -129,14 +129,13 @@ def test_pipeline_parity_with_reference(name):
     sink = {}
     eng.on_logits = lambda rid, pos, row: sink.__setitem__(f"{rid}@{pos}", np.array(row, copy=True))
     tables = {}
-    orig = eng.scheduler._cache_lookup
+    orig = eng.scheduler._lookup_done
 
-    def spy(req):
-        orig(req)
-        bt = eng.pool.block_table(req.request_id)
-        tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
+    def spy(req, hits):
+        orig(req, hits)
+        tables[req.request_id] = {"block_ids": [int(b) for b in hits], "reused": [True] * len(hits)}
 
-    eng.scheduler._cache_lookup = spy
+    eng.scheduler._lookup_done = spy
     rows = P.run_sync_pipeline(spec, eng)
     n_tok = 0
     for rid, r in g["requests"].items():

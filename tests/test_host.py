@@ -256,14 +256,13 @@ def _run_golden(name):
     sink = {}
     eng.on_logits = lambda rid, pos, row: sink.__setitem__(f"{rid}@{pos}", np.array(row, copy=True))
     tables = {}
-    orig = eng.scheduler._cache_lookup
+    orig = eng.scheduler._lookup_done
 
-    def spy(req):
-        orig(req)
-        bt = eng.pool.block_table(req.request_id)
-        tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
+    def spy(req, hits):
+        orig(req, hits)
+        tables[req.request_id] = {"block_ids": [int(b) for b in hits], "reused": [True] * len(hits)}
 
-    eng.scheduler._cache_lookup = spy
+    eng.scheduler._lookup_done = spy
     rows = P.run_sync_pipeline(spec, eng)
     return g, logits, eng, rows, sink, tables
 
@@ -313,8 +312,7 @@ def test_activation_mask_layout():
     inv = list(eng.adapters["adapter0"].invocation_tokens)
     eng.submit(np.asarray([5, 6] + inv), adapter_id="adapter0", max_new_tokens=1, request_id="a")
     eng.submit(np.asarray([9, 9, 9]), max_new_tokens=1, request_id="b")
-    eng.scheduler._drain_intake()
-    ra, rb = list(eng.scheduler.waiting)
+    ra, rb = eng.scheduler.requests["a"], eng.scheduler.requests["b"]
     mask = P.build_activation_mask([P.ScheduledSpan(ra, 0, 5, "prefill"), P.ScheduledSpan(rb, 1, 3, "prefill")])
     assert mask.values.tolist() == [True, True, False, False, False, True, True]
     assert mask.slices == {"a": slice(0, 5), "b": slice(5, 7)}
@@ -380,14 +378,13 @@ def test_pipelined_decode_engine_matches_reference_pipeline(name):
                          pipelined_decode=True, **g["engine"])
     assert eng.pipelined_decode
     tables = {}
-    orig = eng.scheduler._cache_lookup
+    orig = eng.scheduler._lookup_done
 
-    def spy(req):
-        orig(req)
-        bt = eng.pool.block_table(req.request_id)
-        tables[req.request_id] = {"block_ids": list(bt.block_ids), "reused": list(bt.reused)}
+    def spy(req, hits):
+        orig(req, hits)
+        tables[req.request_id] = {"block_ids": [int(b) for b in hits], "reused": [True] * len(hits)}
 
-    eng.scheduler._cache_lookup = spy
+    eng.scheduler._lookup_done = spy
     rows = P.run_sync_pipeline(spec, eng)
     for rid, r in g["requests"].items():
         mine = eng.finished[rid]
