@@ -279,6 +279,16 @@ typedef struct AloraModelDesc {
   int32_t tp_size;
   void* tp_ctx;
   alora_allreduce_fn tp_allreduce;
+  /* aLoRA on the O / MLP projections: an extension of the reference, whose adapters target q/k/v only
+   * (adapters.py:26, 61-63). bf16 tier. NULL arrays = no adapter targets that projection. The delta is
+   * the same masked base + (x . down) . up of model.py:141-145, fused as extra K of the O / gate|up /
+   * down GEMM. slot_targets bits: q 0, k 1, v 2, o 3, gate 4, up 5, down 6. */
+  const void* const* lora_o_down;    /* [L] -> [1, n_slots, rank, Nq] */
+  const void* const* lora_o_up_t;    /* [L] -> [d, n_slots*rank] */
+  const void* const* lora_in_down;   /* [L] -> [P, n_slots, rank, d]; P = 2 (llama: gate, up) or 1 (ref: up) */
+  const void* const* lora_in_up_t;   /* [L] -> [rows of w_in_t, P*n_slots*rank], plane p in columns p*n_slots*rank.. */
+  const void* const* lora_out_down;  /* [L] -> [1, n_slots, rank, F] */
+  const void* const* lora_out_up_t;  /* [L] -> [d, n_slots*rank] */
 } AloraModelDesc;
 
 /* One engine step: all spans packed back to back (varlen). Device arrays. */

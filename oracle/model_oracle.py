@@ -22,6 +22,10 @@ reference file pins them, they are checked only through the shared pieces):
     inputs, q/k/v, KV cache, attention output are bf16 values; every
     accumulation here is fp64, the GPU's is fp32), so GPU-vs-oracle error is
     accumulation order only.
+  * adapter targets "o", "gate", "up", "down" (the reference accepts q/k/v only,
+    adapters.py:26, 61-63): the same masked base + (x @ down) @ up of
+    model.py:141-145 applied to the O-projection and MLP projections
+    (`_adapted`). Parity unpinned: an extension checked GPU vs this oracle.
 """
 
 import hashlib
@@ -164,12 +168,13 @@ class OracleAdapter:
 def oracle_adapter(adapter_id, cfg: OracleConfig, rank, seed=0, targets=("q", "k", "v"),
                    invocation_tokens=None, mode=MODE_ACTIVATED) -> OracleAdapter:
     """generate_adapter (adapters.py:68-101); out width per target for GQA."""
-    d = cfg.d_model
-    out_w = {"q": cfg.q_width, "k": cfg.kv_width, "v": cfg.kv_width}
+    d, q, kv, f = cfg.d_model, cfg.q_width, cfg.kv_width, cfg.ffn
+    shapes = {"q": (d, q), "k": (d, kv), "v": (d, kv), "o": (q, d), "gate": (d, f), "up": (d, f), "down": (f, d)}
     down, up = {}, {}
     for t in targets:
-        dn = _tensor_rng(f"adapter:{adapter_id}:{seed}:{t}:down").uniform(-0.1, 0.1, (d, rank)).astype(np.float32)
-        upm = _tensor_rng(f"adapter:{adapter_id}:{seed}:{t}:up").uniform(-0.1, 0.1, (rank, out_w[t])).astype(np.float32)
+        n_in, n_out = shapes[t]
+        dn = _tensor_rng(f"adapter:{adapter_id}:{seed}:{t}:down").uniform(-0.1, 0.1, (n_in, rank)).astype(np.float32)
+        upm = _tensor_rng(f"adapter:{adapter_id}:{seed}:{t}:up").uniform(-0.1, 0.1, (rank, n_out)).astype(np.float32)
         if cfg.numerics == "bf16":
             dn, upm = bf16_round(dn), bf16_round(upm)
         down[t], up[t] = dn, upm
@@ -255,6 +260,23 @@ def project_qkv_masked(x, wq, wk, wv, adapter: OracleAdapter | None = None, mask
         else:
             out.append(np.where(mask[:, None], base, adapted))
     return tuple(out)
+
+
+def _adapted(x, w, name, adapter: OracleAdapter | None, mask, bf16: bool) -> np.ndarray:
+    """x @ w with the adapter's masked delta on target `name` (model.py:141-145 at another projection), as
+    fp64 (the caller rounds where the GPU rounds: the delta shares the base product's accumulator)."""
+    out = np.asarray(x).astype(np.float64, copy=False) @ np.asarray(w).astype(np.float64, copy=False)
+    if adapter is None or name not in adapter.targets:
+        return out
+    if bf16:
+        s = bf16_round(mm(x, adapter.down[name]))
+        delta = s.astype(np.float64) @ adapter.up[name].astype(np.float64, copy=False)
+    else:  # reference rounding: base and delta are fp32 (mm) before the add
+        out = out.astype(np.float32).astype(np.float64)
+        delta = (mm(mm(x, adapter.down[name]), adapter.up[name])).astype(np.float64)
+    if mask is None:
+        return out + delta
+    return np.where(np.asarray(mask, bool)[:, None], out, out + delta)
 
 
 def paged_attention(q, kv, layer, block_ids, fresh_k, fresh_v, start_pos, n_heads, n_kv_heads=None):
@@ -423,17 +445,18 @@ class OracleModel:
             q, k, v = rb(q), rb(k), rb(v)
             write_kv(kv, li, seq.block_ids, seq.start_pos, k, v)
             attn = rb(paged_attention(q, kv, li, seq.block_ids, k, v, seq.start_pos, c.n_heads, c.kv_heads))
-            x = (x.astype(np.float64) + attn.astype(np.float64) @ L["wo"].astype(np.float64, copy=False)).astype(np.float32) \
-                if bf else x + mm(attn, L["wo"])
+            ad = seq.adapter
+            o = _adapted(attn, L["wo"], "o", ad, mask, bf)
+            x = (x.astype(np.float64) + o).astype(np.float32) if bf else x + o.astype(np.float32)
             h2 = rb(rmsnorm(x, L.get("mlp_norm"), c.rms_eps))
             if c.arch == "ref":
-                a = rb(np.maximum(mm(h2, L["w_in"]), 0.0))
+                a = rb(np.maximum(_adapted(h2, L["w_in"], "up", ad, mask, bf).astype(np.float32), 0.0))
                 w_down = L["w_out"]
             else:
-                g = mm(h2, L["w_gate"]).astype(np.float64)
-                u = mm(h2, L["w_up"]).astype(np.float64)
+                g = _adapted(h2, L["w_gate"], "gate", ad, mask, bf).astype(np.float32).astype(np.float64)
+                u = _adapted(h2, L["w_up"], "up", ad, mask, bf).astype(np.float32).astype(np.float64)
                 a = rb((g / (1.0 + np.exp(-g)) * u).astype(np.float32))
                 w_down = L["w_down"]
-            x = (x.astype(np.float64) + a.astype(np.float64) @ w_down.astype(np.float64, copy=False)).astype(np.float32) \
-                if bf else x + mm(a, w_down)
+            dn = _adapted(a, w_down, "down", ad, mask, bf)
+            x = (x.astype(np.float64) + dn).astype(np.float32) if bf else x + dn.astype(np.float32)
         return rb(rmsnorm(x[-1:], self.w.get("final_norm"), c.rms_eps))

@@ -57,6 +57,9 @@ class AloraModelDesc(ctypes.Structure):
         ("kv_pool", c_void_p), ("total_blocks", c_i32), ("block_size", c_i32),
         ("workspace", c_void_p), ("workspace_bytes", c_i64),
         ("tp_size", c_i32), ("tp_ctx", c_void_p), ("tp_allreduce", c_void_p),
+        ("lora_o_down", ctypes.POINTER(c_void_p)), ("lora_o_up_t", ctypes.POINTER(c_void_p)),
+        ("lora_in_down", ctypes.POINTER(c_void_p)), ("lora_in_up_t", ctypes.POINTER(c_void_p)),
+        ("lora_out_down", ctypes.POINTER(c_void_p)), ("lora_out_up_t", ctypes.POINTER(c_void_p)),
     ]
 
 

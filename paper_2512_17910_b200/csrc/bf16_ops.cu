@@ -373,6 +373,7 @@ int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv,
 // Deferred epilogue of a split-K shrink: the kEpiLoraSelect row/slot/target select on the summed splits.
 __global__ void __launch_bounds__(128) lora_select_finalize_kernel(const float* __restrict__ part, int nparts,
                                                                    int64_t pstride, int M, int SR, int rank,
+                                                                   int P, int tbit0,
                                                                    const int32_t* __restrict__ row_slot,
                                                                    const uint8_t* __restrict__ row_apply,
                                                                    const uint8_t* __restrict__ targets,
@@ -382,9 +383,9 @@ __global__ void __launch_bounds__(128) lora_select_finalize_kernel(const float* 
   const int m = blockIdx.x;
   const int slot = row_slot[m];
   const bool takes = slot >= 0 && row_apply[m];
-  const uint32_t tbits = takes ? targets[slot] : 0u;
-  const float* row = part + (int64_t)m * 3 * SR;
-  for (int c = threadIdx.x * 4; c < 3 * SR; c += blockDim.x * 4) {
+  const uint32_t tbits = takes ? (uint32_t)targets[slot] >> tbit0 : 0u;
+  const float* row = part + (int64_t)m * P * SR;
+  for (int c = threadIdx.x * 4; c < P * SR; c += blockDim.x * 4) {
     const int t = c / SR, off = c % SR;  // SR % 4 == 0: a 4-column group stays in one plane
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if ((tbits >> t) & 1u) acc = sum_parts4(row + c, pstride, nparts);
@@ -400,11 +401,13 @@ __global__ void __launch_bounds__(128) lora_select_finalize_kernel(const float* 
 
 int lora_select_finalize_bf16(const float* partials, int nparts, int M, int SR, int rank, const int32_t* row_slot,
                               const uint8_t* row_apply, const uint8_t* slot_targets, __nv_bfloat16* s,
-                              cudaStream_t st) {
+                              cudaStream_t st, int n_planes, int tbit0) {
   if (M == 0) return ALORA_OK;
-  if (nparts < 1 || nparts > 8 || SR % 4 || rank < 1) return ALORA_EINVAL;
+  if (nparts < 1 || nparts > 8 || SR % 4 || rank < 1 || n_planes < 1 || tbit0 < 0 || tbit0 + n_planes > 8)
+    return ALORA_EINVAL;
   ALORA_CUDA_CHECK(launch_pdl(lora_select_finalize_kernel, dim3(M), dim3(128), 0, st, nullptr, 0, partials, nparts,
-                              (int64_t)M * 3 * SR, M, SR, rank, row_slot, row_apply, slot_targets, s));
+                              (int64_t)M * n_planes * SR, M, SR, rank, n_planes, tbit0, row_slot, row_apply,
+                              slot_targets, s));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -445,7 +448,7 @@ constexpr int kShrinkThreads = 256;
 __global__ void __launch_bounds__(kShrinkThreads) lora_shrink_bf16_kernel(
     const __nv_bfloat16* __restrict__ h, int M, int K, const int32_t* __restrict__ row_slot,
     const uint8_t* __restrict__ row_apply, const __nv_bfloat16* __restrict__ down, int n_slots, int R,
-    const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s) {
+    const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s, int P, int tbit0) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(smem_raw);
   pdl_wait();  // h comes from the RMSNorm before
@@ -454,10 +457,11 @@ __global__ void __launch_bounds__(kShrinkThreads) lora_shrink_bf16_kernel(
   const int KS = n_slots * R;
   const int slot = row_slot[m];
   const bool take = slot >= 0 && row_apply[m];
-  // zero the row's 3 * KS entries (other slots, untargeted projections)
-  for (int i = threadIdx.x; i < 3 * KS; i += blockDim.x) {
+  const uint32_t tb = take ? (uint32_t)slot_targets[slot] >> tbit0 : 0u;
+  // zero the row's P * KS entries (other slots, untargeted projections)
+  for (int i = threadIdx.x; i < P * KS; i += blockDim.x) {
     const int t = i / KS, c = i % KS;
-    const bool mine = take && (c / R == slot) && ((slot_targets[slot] >> t) & 1);
+    const bool mine = take && (c / R == slot) && ((tb >> t) & 1);
     if (!mine) s[((int64_t)t * M + m) * KS + c] = __float2bfloat16_rn(0.f);
   }
   if (!take) return;
@@ -465,9 +469,9 @@ __global__ void __launch_bounds__(kShrinkThreads) lora_shrink_bf16_kernel(
   for (int i = threadIdx.x * 8; i < K; i += blockDim.x * 8) *reinterpret_cast<int4*>(xs + i) = *reinterpret_cast<const int4*>(xr + i);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
-  for (int o = warp; o < 3 * R; o += nwarps) {
+  for (int o = warp; o < P * R; o += nwarps) {
     const int t = o / R, j = o % R;
-    if (!((slot_targets[slot] >> t) & 1)) continue;
+    if (!((tb >> t) & 1)) continue;
     const __nv_bfloat16* dn = down + (((int64_t)t * n_slots + slot) * R + j) * K;
     float acc = 0.f;
     for (int k = lane * 8; k < K; k += 256) {
@@ -489,9 +493,9 @@ __global__ void __launch_bounds__(kShrinkThreads) lora_shrink_bf16_kernel(
 
 int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                      const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets, __nv_bfloat16* s,
-                     cudaStream_t st) {
+                     cudaStream_t st, int n_planes, int tbit0) {
   if (M == 0 || n_slots == 0) return ALORA_OK;
-  if (K % 8 != 0) return ALORA_EINVAL;
+  if (K % 8 != 0 || n_planes < 1 || tbit0 < 0 || tbit0 + n_planes > 8) return ALORA_EINVAL;
   if (K * 2 > 48 * 1024) {
     static bool configured = false;
     if (!configured) {
@@ -502,7 +506,7 @@ int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_sl
     }
   }
   ALORA_CUDA_CHECK(launch_pdl(lora_shrink_bf16_kernel, dim3(M), dim3(kShrinkThreads), (size_t)K * 2, st, nullptr, 0, h,
-                              M, K, row_slot, row_apply, down, n_slots, R, slot_targets, s));
+                              M, K, row_slot, row_apply, down, n_slots, R, slot_targets, s, n_planes, tbit0));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
@@ -554,7 +558,7 @@ template <int R>
 __global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
     const __nv_bfloat16* __restrict__ h, int M, int K, int KS, const int32_t* __restrict__ row_slot,
     const uint8_t* __restrict__ row_apply, const __nv_bfloat16* __restrict__ down, int n_slots,
-    const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s) {
+    const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s, int tbit0) {
   extern __shared__ __align__(128) uint8_t seg_smem[];
   const int Kc = K / KS;
   __nv_bfloat16* sd = reinterpret_cast<__nv_bfloat16*>(seg_smem);           // [R][Kc] down slice
@@ -567,7 +571,7 @@ __global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = rank * Kc;
   const int ldS = n_slots * R;
-  const bool targeted = (slot_targets[slot] >> t) & 1;
+  const bool targeted = (slot_targets[slot] >> (tbit0 + t)) & 1;
   // down slice: independent of the previous kernel
   if (targeted) {
     const __nv_bfloat16* dsrc = down + (((int64_t)t * n_slots + slot) * R) * K + k0;
@@ -707,45 +711,57 @@ __global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
 }
 
 template <int R>
+size_t seg_smem_of(int kc) {
+  return (size_t)R * kc * 2 + (size_t)kSegRowChunk * kc * 2 + (size_t)kSegRowChunk * R * 4 + kSegRowChunk * 4;
+}
+// K slices of one cluster: the smallest power of two <= 8 whose slice is <= 1024 wide and fits shared memory
+template <int R>
+int seg_split(int K) {
+  int KS = 1;
+  while ((K / KS > 1024 || seg_smem_of<R>(K / KS) > 200 * 1024) && KS < 8) KS *= 2;
+  return (K % (KS * 16) != 0 || seg_smem_of<R>(K / KS) > 220 * 1024) ? -1 : KS;
+}
+
+bool lora_shrink_seg_fits(int K) { return K % 128 == 0 && seg_split<64>(K) > 0; }
+
+template <int R>
 int launch_shrink_seg(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                       const __nv_bfloat16* down, int n_slots, const uint8_t* slot_targets, __nv_bfloat16* s,
-                      cudaStream_t st) {
-  auto smem_of = [](int kc) {
-    return (size_t)R * kc * 2 + (size_t)kSegRowChunk * kc * 2 + (size_t)kSegRowChunk * R * 4 + kSegRowChunk * 4;
-  };
-  int KS = 1;
-  while ((K / KS > 1024 || smem_of(K / KS) > 200 * 1024) && KS < 8) KS *= 2;
-  if (K % (KS * 16) != 0 || smem_of(K / KS) > 220 * 1024) return ALORA_EINVAL;
+                      cudaStream_t st, int P, int tbit0) {
+  auto smem_of = [](int kc) { return seg_smem_of<R>(kc); };
+  const int KS = seg_split<R>(K);
+  if (KS < 1) return ALORA_EINVAL;
   const int Kc = K / KS;
   const size_t smem = smem_of(Kc);
-  static bool configured = false;
-  if (!configured) {
+  static size_t configured = 0;
+  if (smem > configured) {
     if (cudaFuncSetAttribute(lora_shrink_seg_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return ALORA_ECUDA;
-    configured = true;
+    configured = smem;
   }
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = KS;
   attr[0].val.clusterDim.z = 1;
-  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_seg_kernel<R>, dim3(3 * n_slots, KS), dim3(kSegThreads), smem, st, attr,
-                              KS > 1 ? 1 : 0, h, M, K, KS, row_slot, row_apply, down, n_slots, slot_targets, s));
+  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_seg_kernel<R>, dim3(P * n_slots, KS), dim3(kSegThreads), smem, st, attr,
+                              KS > 1 ? 1 : 0, h, M, K, KS, row_slot, row_apply, down, n_slots, slot_targets, s,
+                              tbit0));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
 
 int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                          const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
-                         __nv_bfloat16* s, cudaStream_t st) {
+                         __nv_bfloat16* s, cudaStream_t st, int P, int tbit0) {
   if (M == 0 || n_slots == 0) return ALORA_OK;
-  if (K % 128 != 0) return ALORA_EINVAL;
+  if (K % 128 != 0 || P < 1 || tbit0 < 0 || tbit0 + P > 8) return ALORA_EINVAL;
   switch (R) {
-    case 8: return launch_shrink_seg<8>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
-    case 16: return launch_shrink_seg<16>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
-    case 32: return launch_shrink_seg<32>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
-    case 64: return launch_shrink_seg<64>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st);
+    case 8: return launch_shrink_seg<8>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
+    case 16: return launch_shrink_seg<16>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
+    case 32: return launch_shrink_seg<32>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
+    case 64: return launch_shrink_seg<64>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
     default: return ALORA_EINVAL;
   }
 }

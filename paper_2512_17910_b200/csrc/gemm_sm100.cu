@@ -55,7 +55,8 @@ struct GemmArgs {
   int epi;        // Epi | 16 => fp32 output for kEpiStore
   int ks;         // LoRA K (n_slots * rank), 0 = none
   int rank;
-  int n_q, n_kv;  // q | k | v column ranges
+  int n_q, n_kv;  // q | k | v column ranges (select mode)
+  int lora_planes; // > 1: concat mode, every tile reads all planes (up_t columns [p*ks, (p+1)*ks) for plane p)
   const uint32_t* tile_slot_mask;
   const int32_t* positions;  // kEpiRope
   const float* rope_cos;
@@ -65,6 +66,7 @@ struct GemmArgs {
   const uint8_t* sel_row_apply;
   const uint8_t* sel_targets;
   int sel_sr, sel_rank;
+  int sel_tbit0;  // target bit of plane 0 in sel_targets
   unsigned long long* argmax;  // fused greedy argmax of the fp32-store epilogue (ws kernel, S == 1)
   int splits;                 // K splits (blockIdx.z); grid <= SM count, cooperative launch
   float* partial;             // [splits][m_tiles*128][N] fp32 when splits > 1
@@ -100,6 +102,29 @@ __device__ __forceinline__ bool lora_block_present(int j, int rank, uint32_t mas
   for (int s = s0; s <= s1 && s < 32; ++s)
     if ((mask >> s) & 1u) return true;
   return false;
+}
+
+// The LoRA K range of an output tile. Select mode (lora_planes <= 1, the q|k|v projection): one plane of the
+// shrink output, chosen by the tile's column range. Concat mode (lora_planes = P > 1, e.g. the SwiGLU gate|up
+// GEMM whose tiles hold both targets' columns): all P planes in turn against up_t columns [p*ks + j*64, +64).
+template <typename Args>
+__device__ __forceinline__ int lora_np(const Args& a) { return a.lora_planes > 1 ? a.lora_planes : 1; }
+template <typename Args>
+__device__ __forceinline__ int lora_target(const Args& a, int n0) {
+  return n0 < a.n_q ? 0 : (n0 < a.n_q + a.n_kv ? 1 : 2);
+}
+// K block i of the tile's LoRA range (i < np * nkl): S plane and up_t column of block j = i % nkl
+template <typename Args>
+__device__ __forceinline__ void lora_block(const Args& a, int i, int nkl, int target, int& j, int& plane, int& ucol) {
+  const int p = i / nkl;
+  j = i - p * nkl;
+  plane = a.lora_planes > 1 ? p : target;
+  ucol = p * a.ks + j * 64;
+}
+__device__ __forceinline__ int lora_blocks_present(int nkl, int np, int rank, uint32_t mask) {
+  int n = 0;
+  for (int j = 0; j < nkl; ++j) n += lora_block_present(j, rank, mask) ? 1 : 0;
+  return n * np;
 }
 
 // fast SiLU: __fdividef (MUFU.RCP + FMUL, no IEEE-division slow path / divergence); -> 0 for very negative g
@@ -177,7 +202,7 @@ __device__ __forceinline__ void emit_unit(const GemmArgs& a, int n0, int row, in
     const int slot = a.sel_row_slot[row];
     const bool takes = slot >= 0 && a.sel_row_apply[row];
     const int t = col / a.sel_sr, off = col % a.sel_sr;  // 32-col units never straddle a plane
-    const bool tgt = takes && ((a.sel_targets[slot] >> t) & 1u);
+    const bool tgt = takes && ((a.sel_targets[slot] >> (a.sel_tbit0 + t)) & 1u);
 #pragma unroll
     for (int e = 0; e < 32; ++e)
       if (!(tgt && (off + e) / a.sel_rank == slot)) v[e] = 0.f;
@@ -227,7 +252,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   int target = 0, nkl = 0;
   uint32_t mask = 0;
   if (args.ks > 0 && split == S - 1) {
-    target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+    target = lora_target(args, n0);
     nkl = (args.ks + kBK - 1) / kBK;
     mask = args.tile_slot_mask[m_tile];
   }
@@ -248,7 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   int n_iters = kb1 - kb0;
-  for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+  n_iters += lora_blocks_present(nkl, lora_np(args), args.rank, mask);
 
   // warp-converged loops, one elected lane per operation (see gemm_ws_kernel / gemm_bf16_persist_kernel)
   if (warp == 0) {
@@ -268,14 +293,16 @@ __global__ void __launch_bounds__(kThreads, 1)
       __syncwarp();
       next();
     }
-    for (int j = 0; j < nkl; ++j) {
+    for (int i = 0; i < lora_np(args) * nkl; ++i) {
+      int j, plane, ucol;
+      lora_block(args, i, nkl, target, j, plane, ucol);
       if (!lora_block_present(j, args.rank, mask)) continue;
       sm100::mbar_wait(&empty[s], phase ^ 1);
       if (sm100::elect_one()) {
         uint8_t* sa = smem + s * C::kStage;
         sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
-        sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, target, pol_act);
-        sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
+        sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, plane, pol_act);
+        sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], ucol, n0, pol_w);
       }
       __syncwarp();
       next();
@@ -482,16 +509,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         next();
       }
       if (nkl > 0) {
-        const int target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+        const int target = lora_target(args, n0);
         const uint32_t mask = args.tile_slot_mask[m_tile];
-        for (int j = 0; j < nkl; ++j) {
+        for (int i = 0; i < lora_np(args) * nkl; ++i) {
+          int j, plane, ucol;
+          lora_block(args, i, nkl, target, j, plane, ucol);
           if (!lora_block_present(j, args.rank, mask)) continue;
           sm100::mbar_wait(&empty[s], phase ^ 1);
           if (sm100::elect_one()) {
             uint8_t* sa = smem + s * C::kStage;
             sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
-            sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, target, pol_act);
-            sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
+            sm100::tma_load_3d(sa, &tm_s, &full[s], j * kBK, m0, plane, pol_act);
+            sm100::tma_load_2d(sa + C::kABytes, &tm_u, &full[s], ucol, n0, pol_w);
           }
           __syncwarp();
           next();
@@ -512,8 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t acc_t = tmem + (uint32_t)(b * BN);
       int n_iters = nkb;
       if (nkl > 0) {
-        const uint32_t mask = args.tile_slot_mask[m_tile];
-        for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+        n_iters += lora_blocks_present(nkl, lora_np(args), args.rank, args.tile_slot_mask[m_tile]);
       }
       for (int it = 0; it < n_iters; ++it) {
         sm100::mbar_wait(&full[s], phase);
@@ -706,7 +734,7 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
   // run ~nkl blocks longer than the others, keeping at least one base block in it
   int per = (nkb_all + S - 1) / S;
   if (args.ks > 0 && S > 1) {
-    const int nkl_all = (args.ks + kBK - 1) / kBK;
+    const int nkl_all = lora_np(args) * ((args.ks + kBK - 1) / kBK);
     per = max(per, min((nkb_all + nkl_all + S - 1) / S, (nkb_all - 1) / (S - 1)));
   }
   const int kb0 = min(nkb_all, split * per), kb1 = split == S - 1 ? nkb_all : min(nkb_all, kb0 + per);
@@ -749,7 +777,7 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
     int target = 0, nkl = 0;
     uint32_t mask = 0;
     if (args.ks > 0 && split == S - 1) {
-      target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
+      target = lora_target(args, n0);
       nkl = (args.ks + kBK - 1) / kBK;
       for (int mt = 0; mt < MT; ++mt) mask |= args.tile_slot_mask[mt];
     }
@@ -778,16 +806,18 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
       __syncwarp();
       next();
     }
-    for (int j = 0; j < nkl; ++j) {
+    for (int i = 0; i < lora_np(args) * nkl; ++i) {
+      int j, plane, ucol;
+      lora_block(args, i, nkl, target, j, plane, ucol);
       if (!lora_block_present(j, args.rank, mask)) continue;
       sm100::mbar_wait(&empty[s], phase ^ 1);
       if (sm100::elect_one()) {
         uint8_t* sa = smem + s * C::kStage;
         sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
-        sm100::tma_load_2d(sa + MT * C::kABytes, &tm_u, &full[s], j * kBK, n0, pol_w);
+        sm100::tma_load_2d(sa + MT * C::kABytes, &tm_u, &full[s], ucol, n0, pol_w);
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt)
-          sm100::tma_load_3d(sa + mt * C::kABytes, &tm_s, &full[s], j * kBK, mt * kBM, target, pol_act);
+          sm100::tma_load_3d(sa + mt * C::kABytes, &tm_s, &full[s], j * kBK, mt * kBM, plane, pol_act);
       }
       __syncwarp();
       next();
@@ -799,8 +829,7 @@ __global__ void __launch_bounds__(WsCfg<BN, MT>::kThreads, 1)
       if (args.ks > 0 && split == S - 1) {
         uint32_t mask = 0;
         for (int mt = 0; mt < MT; ++mt) mask |= args.tile_slot_mask[mt];
-        const int nkl = (args.ks + kBK - 1) / kBK;
-        for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+        n_iters += lora_blocks_present((args.ks + kBK - 1) / kBK, lora_np(args), args.rank, mask);
       }
       constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
       int s = 0;
@@ -985,6 +1014,7 @@ struct DecArgs {
   int ld_bf16;
   unsigned long long* argmax;
   int ks, rank, n_q, n_kv;  // LoRA expand as extra K (last split)
+  int lora_planes;
   const uint32_t* tile_slot_mask;
 };
 
@@ -1072,15 +1102,17 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
         next();
       }
-      const int target = n0 < args.n_q ? 0 : (n0 < args.n_q + args.n_kv ? 1 : 2);
-      for (int j = 0; j < nkl; ++j) {
+      const int target = lora_target(args, n0);
+      for (int i = 0; i < lora_np(args) * nkl; ++i) {
+        int j, plane, ucol;
+        lora_block(args, i, nkl, target, j, plane, ucol);
         if (!lora_block_present(j, args.rank, mask)) continue;
         sm100::mbar_wait(&empty[st], phase ^ 1);
         if (sm100::elect_one()) {
           uint8_t* sa = smem + st * C::kStage;
           sm100::mbar_arrive_expect_tx(&full[st], C::kStage);
-          sm100::tma_load_2d(sa, &tm_u, &full[st], j * kBK, n0, pol_w);
-          sm100::tma_load_3d(sa + C::kWBytes, &tm_s, &full[st], j * kBK, 0, target, pol_act);
+          sm100::tma_load_2d(sa, &tm_u, &full[st], ucol, n0, pol_w);
+          sm100::tma_load_3d(sa + C::kWBytes, &tm_s, &full[st], j * kBK, 0, plane, pol_act);
         }
         __syncwarp();
         next();
@@ -1090,9 +1122,7 @@ __global__ void __launch_bounds__(192, 1)
     pdl_wait();
     int n_iters = n_base;
     if (lora_here) {
-      const uint32_t mask = args.tile_slot_mask[0];
-      const int nkl = (args.ks + kBK - 1) / kBK;
-      for (int j = 0; j < nkl; ++j) n_iters += lora_block_present(j, args.rank, mask) ? 1 : 0;
+      n_iters += lora_blocks_present((args.ks + kBK - 1) / kBK, lora_np(args), args.rank, args.tile_slot_mask[0]);
     }
     constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, MN);
     int st = 0;
@@ -1338,27 +1368,31 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   }
   if (base_epi == kEpiLoraSelect) {
     if (!lora || !lora->sel_row_slot || !lora->sel_row_apply || !lora->sel_targets || lora->sel_sr % 32 ||
-        lora->sel_rank < 1 || N != 3 * lora->sel_sr)
+        lora->sel_rank < 1 || lora->sel_planes < 1 || N != lora->sel_planes * lora->sel_sr)
       return ALORA_EINVAL;
     args.sel_row_slot = lora->sel_row_slot;
     args.sel_row_apply = lora->sel_row_apply;
     args.sel_targets = lora->sel_targets;
     args.sel_sr = lora->sel_sr;
     args.sel_rank = lora->sel_rank;
+    args.sel_tbit0 = lora->sel_tbit0;
   }
   CUtensorMap ta, tb, ts, tu;
+  const int up_planes = lora && lora->planes > 1 ? lora->planes : 1;  // up_t width = up_planes * ks
   if (!make_tmap_2d(&ta, A, M, K, lda, kBM, kBK)) return ALORA_ECUDA;
   if (!make_tmap_2d(&tb, Bt, N, K, ldb, BN, kBK)) return ALORA_ECUDA;
   ts = ta;
   tu = tb;
   if (lora != nullptr && lora->s != nullptr && lora->ks > 0) {
     if (lora->ks % 8 || (lora->n_q % BN) || (lora->n_kv % BN) || lora->rank < 1) return ALORA_EINVAL;
-    if (!make_tmap_3d(&ts, lora->s, 3, M, lora->ks, kBM, kBK)) return ALORA_ECUDA;
-    if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks, lora->ks, BN, kBK)) return ALORA_ECUDA;
+    if (lora->s_planes < 1 || lora->planes > lora->s_planes) return ALORA_EINVAL;
+    if (!make_tmap_3d(&ts, lora->s, lora->s_planes, M, lora->ks, kBM, kBK)) return ALORA_ECUDA;
+    if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks * up_planes, lora->ks * up_planes, BN, kBK)) return ALORA_ECUDA;
     args.ks = lora->ks;
     args.rank = lora->rank;
     args.n_q = lora->n_q;
     args.n_kv = lora->n_kv;
+    args.lora_planes = lora->planes;
     args.tile_slot_mask = lora->tile_slot_mask;
   }
   static const bool no_dec = getenv("ALORA_GEMM_NO_DEC") != nullptr;  // A/B switch off the swap-AB decode GEMM
@@ -1398,12 +1432,13 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
       tsm = tx;
       if (lora != nullptr && lora->s != nullptr && lora->ks > 0) {
         if (lora->ks % 8 || (lora->n_q % kBM) || (lora->n_kv % kBM) || lora->rank < 1) return ALORA_EINVAL;
-        if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks, lora->ks, kBM, kBK)) return ALORA_ECUDA;
-        if (!make_tmap_3d(&tsm, lora->s, 3, M, lora->ks, MN, kBK)) return ALORA_ECUDA;
+        if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks * up_planes, lora->ks * up_planes, kBM, kBK)) return ALORA_ECUDA;
+        if (!make_tmap_3d(&tsm, lora->s, lora->s_planes, M, lora->ks, MN, kBK)) return ALORA_ECUDA;
         da.ks = lora->ks;
         da.rank = lora->rank;
         da.n_q = lora->n_q;
         da.n_kv = lora->n_kv;
+        da.lora_planes = lora->planes;
         da.tile_slot_mask = lora->tile_slot_mask;
       }
       return MN == 16 ? launch_dec<16>(tw, tx, tu, tsm, da, st) : launch_dec<32>(tw, tx, tu, tsm, da, st);
@@ -1444,7 +1479,8 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
       if (base_epi == kEpiRope && (lora->rope_cols % best.bn || best.bn % lora->head_dim)) return ALORA_EINVAL;
       CUtensorMap tb2, tu2 = tu;
       if (!make_tmap_2d(&tb2, Bt, N, K, ldb, best.bn, kBK)) return ALORA_ECUDA;
-      if (args.ks > 0 && !make_tmap_2d(&tu2, lora->up_t, N, lora->ks, lora->ks, best.bn, kBK)) return ALORA_ECUDA;
+      if (args.ks > 0 && !make_tmap_2d(&tu2, lora->up_t, N, lora->ks * up_planes, lora->ks * up_planes, best.bn, kBK))
+        return ALORA_ECUDA;
       if (args.ks == 0) tu2 = tb2;
       args.splits = best.splits;
       if (best.splits > 1) {

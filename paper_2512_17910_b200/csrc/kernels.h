@@ -46,15 +46,18 @@ int embed_bf16(const int32_t* tokens, const int32_t* positions, const __nv_bfloa
 // out_bf16[r] = bf16( rmsnorm(x[rows[r]]) * w )
 int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const float* w, float eps,
                  __nv_bfloat16* out, cudaStream_t st);
+// Shrink planes: down [P][n_slots][R][K] -> s [P][M][n_slots*R]; plane t serves target bit tbit0 + t of
+// slot_targets (q 0, k 1, v 2 | o 3 | gate 4, up 5 | down 6).
 int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                      const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets, __nv_bfloat16* s,
-                     cudaStream_t st);
+                     cudaStream_t st, int n_planes = 3, int tbit0 = 0);
 // Segmented shrink for steps with few delta rows per adapter: one CTA cluster per (target, slot) streams the
 // adapter's down rows once (K split over the cluster, DSMEM reduction in rank order), mma.sync over the
 // slot's active rows; writes the same [3][M][n_slots*R] layout (zeros elsewhere). R in {8, 16, 32, 64}.
 int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                          const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
-                         __nv_bfloat16* s, cudaStream_t st);
+                         __nv_bfloat16* s, cudaStream_t st, int n_planes = 3, int tbit0 = 0);
+bool lora_shrink_seg_fits(int K);  // the segmented kernel's K slice fits a <= 8-CTA cluster
 constexpr int kSegMaxRows = 128;  // the executor's switch: at most this many delta rows per adapter slot
 int rope_bf16(__nv_bfloat16* qkv, int ld, const int32_t* positions, int M, int H, int Hkv, int D,
               const float* cos_t, const float* sin_t, cudaStream_t st);
@@ -76,10 +79,12 @@ int64_t attn_bf16_workspace_bound(int H, int D);
 
 // tcgen05 GEMM: C = epi(A[M,K] @ Bt[N,K]^T (+ S_t[M,Ks] @ Ut[N,Ks]^T lora part)), bf16 in, fp32 accumulate.
 struct GemmLora {
-  const __nv_bfloat16* s = nullptr;    // [3][M][Ks] shrink output (K-major), nullptr = no LoRA
-  const __nv_bfloat16* up_t = nullptr; // [N][Ks]
+  const __nv_bfloat16* s = nullptr;    // [s_planes][M][Ks] shrink output (K-major), nullptr = no LoRA
+  const __nv_bfloat16* up_t = nullptr; // [N][Ks] (select mode) or [N][planes * Ks] (concat mode)
   int ks = 0;                          // n_slots * rank
-  int n_q = 0, n_kv = 0;               // column ranges of the q|k|v targets
+  int n_q = 0, n_kv = 0;               // select mode: column ranges of the q|k|v targets (planes 0 | 1 | 2)
+  int planes = 0;                      // > 1: concat mode, every tile adds all planes (SwiGLU gate|up tiles)
+  int s_planes = 3;                    // planes allocated in s
   const uint32_t* tile_slot_mask = nullptr;  // [ceil(M/128)] bitmask of slots present (taking the delta)
   int rank = 0;
   // kEpiRope: rotate-half RoPE in fp32 on the accumulator of columns < rope_cols (q and k heads), one rounding
@@ -96,6 +101,8 @@ struct GemmLora {
   const uint8_t* sel_targets = nullptr;
   int sel_sr = 0;
   int sel_rank = 0;
+  int sel_planes = 3;  // N = sel_planes * sel_sr
+  int sel_tbit0 = 0;   // target bit of plane 0 in sel_targets (q 0, k 1, v 2, o 3, gate 4, up 5, down 6)
   // fp32-store epilogue of a weight-streaming launch: per row, atomicMax of (orderable logit << 32 | ~col),
   // i.e. the greedy token with ties to the lowest id (model.py:190-195), fused into the lm_head
   unsigned long long* argmax = nullptr;
@@ -151,7 +158,7 @@ int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv,
 // where row m takes slot (off / rank)'s delta on target t, else 0.
 int lora_select_finalize_bf16(const float* partials, int nparts, int M, int SR, int rank, const int32_t* row_slot,
                               const uint8_t* row_apply, const uint8_t* slot_targets, __nv_bfloat16* s,
-                              cudaStream_t st);
+                              cudaStream_t st, int n_planes = 3, int tbit0 = 0);
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st);
 
 }  // namespace alora

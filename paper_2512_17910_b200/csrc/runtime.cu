@@ -75,6 +75,8 @@ using GraphKey = std::tuple<int, int, int, int, int, int, int>;
 struct Model {
   AloraModelDesc d;
   std::vector<const void*> w_qkv_t, w_o_t, w_in_t, w_out_t, lora_down, lora_up_t;
+  // O / MLP adapter targets (empty = untargeted)
+  std::vector<const void*> lora_o_down, lora_o_up_t, lora_in_down, lora_in_up_t, lora_out_down, lora_out_up_t;
   std::vector<const float*> attn_norm, mlp_norm;
   int32_t last_launches = 0;
   Profiler prof;
@@ -182,22 +184,28 @@ int validate(const AloraModelDesc* d) {
 // lora_select_finalize_bf16 (one extra small launch, counted in *extra_launches).
 int shrink(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
            const __nv_bfloat16* down, int n_slots, int R, const uint8_t* targets, __nv_bfloat16* s, cudaStream_t st,
-           const GemmWs* gw, float* part = nullptr, int64_t part_bytes = 0, int* extra_launches = nullptr) {
+           const GemmWs* gw, float* part = nullptr, int64_t part_bytes = 0, int* extra_launches = nullptr,
+           int n_planes = 3, int tbit0 = 0) {
   const int SR = n_slots * R;
-  if (SR % 64 != 0) return lora_shrink_bf16(h, M, K, row_slot, row_apply, down, n_slots, R, targets, s, st);
+  if (SR % 64 != 0)
+    return lora_shrink_bf16(h, M, K, row_slot, row_apply, down, n_slots, R, targets, s, st, n_planes, tbit0);
   GemmLora g;
   g.sel_row_slot = row_slot;
   g.sel_row_apply = row_apply;
   g.sel_targets = targets;
   g.sel_sr = SR;
   g.sel_rank = R;
+  g.sel_planes = n_planes;
+  g.sel_tbit0 = tbit0;
   GemmDefer df;
   df.partial = part;
   df.capacity = part_bytes;
-  const int rc = gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, 3 * SR, K, &g, st, gw, 8, part ? &df : nullptr);
+  const int rc =
+      gemm_bf16(kEpiLoraSelect, h, K, down, K, s, SR, M, n_planes * SR, K, &g, st, gw, 8, part ? &df : nullptr);
   if (rc != ALORA_OK || !df.deferred) return rc;
   if (extra_launches) ++*extra_launches;
-  return lora_select_finalize_bf16(part, df.splits_out, M, SR, R, row_slot, row_apply, targets, s, st);
+  return lora_select_finalize_bf16(part, df.splits_out, M, SR, R, row_slot, row_apply, targets, s, st, n_planes,
+                                   tbit0);
 }
 
 int forward_f32(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
@@ -286,6 +294,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const int rk = d.lora_rank;
   const bool seg_shrink = lora && s.lora_rows_max <= kSegMaxRows && d.d_model % 128 == 0 &&
                           (rk == 8 || rk == 16 || rk == 32 || rk == 64);
+  const bool lora_o = lora && !mdl.lora_o_down.empty(), lora_in = lora && !mdl.lora_in_down.empty();
+  const bool lora_out = lora && !mdl.lora_out_down.empty();
+  const int in_planes = llama ? 2 : 1;
   Launcher run{mdl, st};
   const bool tp = d.tp_size > 1;
   float* tpd = reinterpret_cast<float*>(base + w.tpd);
@@ -293,18 +304,19 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   // split-K partials are left for the next RMSNorm. Tensor parallel: this rank's partial product is
   // materialised in tpd (split-K summed in order), all-reduced by the caller's hook, then applied by the
   // RMSNorm as a single pending partial (row-parallel linear layer + all-reduce).
-  auto residual_gemm = [&](const __nv_bfloat16* A, int K, const void* W, int ldw) -> int {
+  auto residual_gemm = [&](const __nv_bfloat16* A, int K, const void* W, int ldw,
+                           const GemmLora* gla = nullptr) -> int {
     GemmDefer df;
     df.partial = part;
     df.capacity = w.part_bytes;
     if (!tp) {
-      const int rc = gemm_bf16(kEpiAdd, A, K, static_cast<const __nv_bfloat16*>(W), ldw, x, dm, M, dm, K, nullptr,
+      const int rc = gemm_bf16(kEpiAdd, A, K, static_cast<const __nv_bfloat16*>(W), ldw, x, dm, M, dm, K, gla,
                                st, gw, 8, &df);
       pend = df.deferred ? df.splits_out : 0;
       pend_buf = part;
       return rc;
     }
-    int rc = gemm_bf16(kEpiStore | 16, A, K, static_cast<const __nv_bfloat16*>(W), ldw, tpd, dm, M, dm, K, nullptr,
+    int rc = gemm_bf16(kEpiStore | 16, A, K, static_cast<const __nv_bfloat16*>(W), ldw, tpd, dm, M, dm, K, gla,
                        st, gw, 8, nullptr);
     pend = 1;
     pend_buf = tpd;
@@ -384,18 +396,54 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
                     static_cast<const __nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, H, Hkv, D, attn, Nq,
                     aws, w.attn_ws_bytes, st, d.total_blocks));
     }
-    RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true), 2.0 * m_ * dm_ * Nq_,
-        residual_gemm(attn, Nq, mdl.w_o_t[l], Nq));
+    // O / MLP adapter targets (extension): the masked shrink of the projection's input into the shrink
+    // workspace (its q|k|v planes were consumed by gemm_qkv), then the expand as extra K of the GEMM
+    auto target_shrink = [&](const __nv_bfloat16* in, int K, const void* down, int planes, int tbit0) -> int {
+      if (seg_shrink && lora_shrink_seg_fits(K))
+        return lora_shrink_seg_bf16(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down),
+                                    d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0);
+      return shrink(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down), d.n_slots, rk,
+                    d.slot_targets, sws, st, gw, part, w.part_bytes, &run.n, planes, tbit0);
+    };
+    auto target_lora = [&](const void* up_t, int N, int planes) {
+      GemmLora g;
+      g.s = sws;
+      g.up_t = static_cast<const __nv_bfloat16*>(up_t);
+      g.ks = d.n_slots * rk;
+      g.rank = rk;
+      g.tile_slot_mask = masks;
+      g.planes = planes > 1 ? planes : 0;
+      g.s_planes = planes;
+      g.n_q = N;  // select mode: every column reads plane 0
+      g.n_kv = 0;
+      return g;
+    };
+    const double shrink_bytes_o = m_ * Nq_ * 2 + (double)ks_ * Nq_ * 2 + m_ * ks_ * 2;
+    if (lora_o)
+      RUN("lora_shrink", shrink_bytes_o, 2.0 * m_ * ks_ * Nq_,
+          target_shrink(attn, Nq, mdl.lora_o_down[l], 1, 3));
+    const GemmLora glo = lora_o ? target_lora(mdl.lora_o_up_t[l], dm, 1) : GemmLora{};
+    RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true) + (lora_o ? 2.0 * dm_ * ks_ : 0.0), 2.0 * m_ * dm_ * Nq_,
+        residual_gemm(attn, Nq, mdl.w_o_t[l], Nq, lora_o ? &glo : nullptr));
     if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
     RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
         residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
     pend = 0;
     const double n_in = llama ? 2 * F_ : F_;
-    RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2, 2.0 * m_ * n_in * dm_,
+    if (lora_in)
+      RUN("lora_shrink", m_ * dm_ * 2 + in_planes * ks_ * dm_ * 2 + in_planes * m_ * ks_ * 2,
+          2.0 * in_planes * m_ * ks_ * dm_, target_shrink(h, dm, mdl.lora_in_down[l], in_planes, 4 + (llama ? 0 : 1)));
+    const GemmLora gli = lora_in ? target_lora(mdl.lora_in_up_t[l], llama ? 2 * F : F, in_planes) : GemmLora{};
+    RUN("gemm_mlp_in", 2.0 * (m_ * dm_ + n_in * dm_) + m_ * F_ * 2 + (lora_in ? 2.0 * n_in * in_planes * ks_ : 0.0),
+        2.0 * m_ * n_in * dm_,
         gemm_bf16(llama ? kEpiSwiglu : kEpiRelu, h, dm, static_cast<const __nv_bfloat16*>(mdl.w_in_t[l]), dm, act, F,
-                  M, llama ? 2 * F : F, dm, nullptr, st, gw));
-    RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true), 2.0 * m_ * dm_ * F_,
-        residual_gemm(act, F, mdl.w_out_t[l], F));
+                  M, llama ? 2 * F : F, dm, lora_in ? &gli : nullptr, st, gw));
+    if (lora_out)
+      RUN("lora_shrink", m_ * F_ * 2 + ks_ * F_ * 2 + m_ * ks_ * 2, 2.0 * m_ * ks_ * F_,
+          target_shrink(act, F, mdl.lora_out_down[l], 1, 6));
+    const GemmLora glw = lora_out ? target_lora(mdl.lora_out_up_t[l], dm, 1) : GemmLora{};
+    RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true) + (lora_out ? 2.0 * dm_ * ks_ : 0.0), 2.0 * m_ * dm_ * F_,
+        residual_gemm(act, F, mdl.w_out_t[l], F, lora_out ? &glw : nullptr));
     if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
   }
   // greedy argmax fused into the lm_head epilogue (weight-streaming path: S <= 256 spans, vocab % 32 == 0)
@@ -577,6 +625,15 @@ int alora_model_create(const AloraModelDesc* desc, void** out_handle) {
   copy_ptrs(desc->w_out_t, m->w_out_t);
   copy_ptrs(desc->lora_down, m->lora_down);
   copy_ptrs(desc->lora_up_t, m->lora_up_t);
+  auto copy_opt = [&](const void* const* src, std::vector<const void*>& dst) {
+    if (src && desc->n_slots > 0) copy_ptrs(src, dst);
+  };
+  copy_opt(desc->lora_o_down, m->lora_o_down);
+  copy_opt(desc->lora_o_up_t, m->lora_o_up_t);
+  copy_opt(desc->lora_in_down, m->lora_in_down);
+  copy_opt(desc->lora_in_up_t, m->lora_in_up_t);
+  copy_opt(desc->lora_out_down, m->lora_out_down);
+  copy_opt(desc->lora_out_up_t, m->lora_out_up_t);
   m->attn_norm.assign(L, nullptr);
   m->mlp_norm.assign(L, nullptr);
   for (int i = 0; i < L; ++i) {
@@ -586,6 +643,20 @@ int alora_model_create(const AloraModelDesc* desc, void** out_handle) {
   // host arrays are not retained
   m->d.w_qkv_t = m->d.w_o_t = m->d.w_in_t = m->d.w_out_t = m->d.lora_down = m->d.lora_up_t = nullptr;
   m->d.attn_norm = m->d.mlp_norm = nullptr;
+  m->d.lora_o_down = m->d.lora_o_up_t = m->d.lora_in_down = m->d.lora_in_up_t = nullptr;
+  m->d.lora_out_down = m->d.lora_out_up_t = nullptr;
+  auto pair_ok = [&](const std::vector<const void*>& a, const std::vector<const void*>& b) {
+    if (a.empty() != b.empty()) return false;
+    for (size_t i = 0; i < a.size(); ++i)
+      if (!a[i] || !b[i]) return false;
+    return true;
+  };
+  const bool extra_targets = !m->lora_o_down.empty() || !m->lora_in_down.empty() || !m->lora_out_down.empty();
+  if (!pair_ok(m->lora_o_down, m->lora_o_up_t) || !pair_ok(m->lora_in_down, m->lora_in_up_t) ||
+      !pair_ok(m->lora_out_down, m->lora_out_up_t) || (extra_targets && desc->dtype != ALORA_BF16)) {
+    delete m;
+    return ALORA_EINVAL;
+  }
   for (int i = 0; i < L; ++i)
     if (!m->w_qkv_t[i] || !m->w_o_t[i] || !m->w_in_t[i] || !m->w_out_t[i] ||
         (desc->n_slots > 0 && (!m->lora_down[i] || !m->lora_up_t[i]))) {

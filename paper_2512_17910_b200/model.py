@@ -20,7 +20,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native
-from .adapters import MODE_ACTIVATED, LoraAdapter
+from .adapters import MODE_ACTIVATED, TARGET_BITS, LoraAdapter, target_shapes
 from .weights import BaseWeights, LayerWeights, generate_weights, position_table, rope_tables
 
 __all__ = ["ModelConfig", "LayerWeights", "BaseWeights", "generate_weights", "SeqInput", "Model",
@@ -250,31 +250,71 @@ class Model:
                 n += 1
         if n > 32 and cfg.dtype == "bf16":
             raise ValueError("the bf16 tier supports at most 32 adapters per model")
-        widths = {"q": cfg.q_width, "k": cfg.kv_width, "v": cfg.kv_width}
+        shapes = target_shapes(d, cfg.q_width, cfg.kv_width, cfg.ffn)
         offs = {"q": 0, "k": cfg.q_width, "v": cfg.q_width + cfg.kv_width}
         nqkv = cfg.q_width + 2 * cfg.kv_width
+        llama = cfg.arch == "llama"
+        used = {t for _, a in self._adapters.values() for t in a.targets}
+        if used - set("qkv") and cfg.dtype != "bf16":
+            raise ValueError("O / MLP adapter targets are served by the bf16 tier (dtype='bf16')")
+        if "gate" in used and not llama:
+            raise ValueError("the reference architecture's MLP has no gate projection")
+        # planes of the MLP-in adapter bank: llama gate|up (interleaved SwiGLU weight), ref: up only
+        in_names = ("gate", "up") if llama else ("up",)
+        nin = 2 * cfg.ffn if llama else cfg.ffn
         targets = np.zeros(n, dtype=np.uint8)
-        downs, ups = [], []
+        bank = {k: [] for k in ("down", "up_t", "o_down", "o_up_t", "in_down", "in_up_t", "out_down", "out_up_t")}
+
+        def factors(a, tname, li):
+            dn, upm = np.asarray(a.down[tname]), np.asarray(a.up[tname])
+            if dn.ndim == 3:
+                dn, upm = dn[li], upm[li]
+            n_in, n_out = shapes[tname]
+            if dn.shape != (n_in, a.rank) or upm.shape != (a.rank, n_out):
+                raise ValueError(f"adapter {a.adapter_id} factor shapes do not match the model")
+            return dn, upm
+
         for li in range(L):
             down = np.zeros((3, n, rank, d), dtype=np.float32)
             up_t = np.zeros((nqkv, n * rank), dtype=np.float32)
+            o_down = np.zeros((1, n, rank, cfg.q_width), np.float32) if "o" in used else None
+            o_up = np.zeros((d, n * rank), np.float32) if "o" in used else None
+            has_in = bool(used & set(in_names))
+            in_down = np.zeros((len(in_names), n, rank, d), np.float32) if has_in else None
+            in_up = np.zeros((nin, len(in_names) * n * rank), np.float32) if has_in else None
+            out_down = np.zeros((1, n, rank, cfg.ffn), np.float32) if "down" in used else None
+            out_up = np.zeros((d, n * rank), np.float32) if "down" in used else None
             for slot, a in self._adapters.values():
-                for ti, tname in enumerate("qkv"):
-                    if tname not in a.targets:
-                        continue
-                    targets[slot] |= 1 << ti
-                    dn = np.asarray(a.down[tname])
-                    upm = np.asarray(a.up[tname])
-                    if dn.ndim == 3:
-                        dn, upm = dn[li], upm[li]
-                    if dn.shape != (d, a.rank) or upm.shape != (a.rank, widths[tname]):
-                        raise ValueError(f"adapter {a.adapter_id} factor shapes do not match the model")
-                    down[ti, slot, :a.rank, :] = dn.T
-                    up_t[offs[tname]:offs[tname] + widths[tname], slot * rank:slot * rank + a.rank] = upm.T
-            downs.append(self._dev(down))
-            ups.append(self._dev(up_t))
-        self._bank = {"down": downs, "up_t": ups, "rank": rank, "n": n,
-                      "targets": self._dev(targets, self._torch.uint8)}
+                cols = slice(slot * rank, slot * rank + a.rank)
+                for tname in a.targets:
+                    targets[slot] |= 1 << TARGET_BITS[tname]
+                    dn, upm = factors(a, tname, li)
+                    if tname in offs:
+                        down[TARGET_BITS[tname], slot, :a.rank, :] = dn.T
+                        up_t[offs[tname]:offs[tname] + upm.shape[1], cols] = upm.T
+                    elif tname == "o":
+                        o_down[0, slot, :a.rank] = dn.T
+                        o_up[:, cols] = upm.T
+                    elif tname == "down":
+                        out_down[0, slot, :a.rank] = dn.T
+                        out_up[:, cols] = upm.T
+                    else:  # gate / up: plane p, rows as the (interleaved) w_in_t rows
+                        p = in_names.index(tname)
+                        in_down[p, slot, :a.rank] = dn.T
+                        pc = slice(p * n * rank + slot * rank, p * n * rank + slot * rank + a.rank)
+                        if llama:
+                            F = cfg.ffn
+                            rows = (np.arange(F) // GLU_BLOCK) * 2 * GLU_BLOCK + np.arange(F) % GLU_BLOCK
+                            in_up[rows + (GLU_BLOCK if tname == "up" else 0), pc] = upm.T
+                        else:
+                            in_up[:, pc] = upm.T
+            bank["down"].append(self._dev(down))
+            bank["up_t"].append(self._dev(up_t))
+            for key, arr in (("o_down", o_down), ("o_up_t", o_up), ("in_down", in_down), ("in_up_t", in_up),
+                             ("out_down", out_down), ("out_up_t", out_up)):
+                if arr is not None:
+                    bank[key].append(self._dev(arr))
+        self._bank = dict(bank, rank=rank, n=n, targets=self._dev(targets, self._torch.uint8))
         self._bank_version += 1
 
     # ---------------------------------------------------------- workspace ---
@@ -323,6 +363,9 @@ class Model:
         if bank is not None:
             D.lora_down, D.lora_up_t = self._ptr_array(bank["down"]), self._ptr_array(bank["up_t"])
             D.slot_targets = bank["targets"].data_ptr()
+            for key in ("o_down", "o_up_t", "in_down", "in_up_t", "out_down", "out_up_t"):
+                if bank[key]:
+                    setattr(D, "lora_" + key, self._ptr_array(bank[key]))
         D.kv_pool = kv.data_ptr()
         D.total_blocks, D.block_size = kv.shape[0], kv.shape[3]
         D.workspace, D.workspace_bytes = self._ws.data_ptr(), self._ws.numel()

@@ -597,3 +597,36 @@ def test_attention_plan_covers_every_key_once(case):
         assert int(out[5]) < sum(s + n for s, n in zip(starts, lens)) // 3  # distinct keys: prefixes counted once
     if case == "mixed":
         assert int(out[2]) == 4  # the two spans on the shared blocks form one set
+
+
+def test_extension_targets_shapes_and_validation():
+    """O / MLP adapter targets (extension of adapters.py:26): factor shapes per projection, unknown names rejected."""
+    import paper_2512_17910_b200 as P
+    ad = P.generate_adapter("x", 64, 4, targets=("o", "gate", "up", "down"), mode="standard", q_width=32,
+                            kv_width=16, ffn_width=96)
+    assert ad.down["o"].shape == (32, 4) and ad.up["o"].shape == (4, 64)
+    assert ad.down["gate"].shape == (64, 4) and ad.up["up"].shape == (4, 96)
+    assert ad.down["down"].shape == (96, 4) and ad.up["down"].shape == (4, 64)
+    # the q/k/v factors are unchanged by the extension (same Philox streams as the reference)
+    a1 = P.generate_adapter("y", 64, 4, targets=("q", "v"), mode="standard")
+    a2 = P.generate_adapter("y", 64, 4, targets=("q", "v", "o"), mode="standard")
+    np.testing.assert_array_equal(a1.down["q"], a2.down["q"])
+    with pytest.raises(ValueError):
+        P.generate_adapter("z", 64, 4, targets=("w_gate",), mode="standard")
+
+
+def test_oracle_extension_targets_formula():
+    """oracle._adapted at fp64acc is the reference's masked formula (model.py:141-145) at another projection."""
+    import oracle as O
+    from oracle.model_oracle import _adapted
+    cfg = O.OracleConfig(n_layers=1, n_heads=2, head_dim=8, d_model=16, vocab_size=32)
+    ad = O.oracle_adapter("o", cfg, 4, targets=("o",), mode="standard")
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((5, 16)).astype(np.float32)
+    w = rng.standard_normal((16, 16)).astype(np.float32)
+    mask = np.array([True, False, True, False, False])
+    got = _adapted(x, w, "o", ad, mask, False).astype(np.float32)
+    base = O.mm(x, w)
+    adapted = base + O.mm(O.mm(x, ad.down["o"]), ad.up["o"])
+    np.testing.assert_array_equal(got, np.where(mask[:, None], base, adapted))
+    np.testing.assert_array_equal(_adapted(x, w, "up", ad, None, False).astype(np.float32), base)
