@@ -289,6 +289,15 @@ typedef struct AloraModelDesc {
   const void* const* lora_in_up_t;   /* [L] -> [rows of w_in_t, P*n_slots*rank], plane p in columns p*n_slots*rank.. */
   const void* const* lora_out_down;  /* [L] -> [1, n_slots, rank, F] */
   const void* const* lora_out_up_t;  /* [L] -> [d, n_slots*rank] */
+  /* fused tensor-parallel all-reduce (tp_size > 1 and tp_peers != NULL; replaces the tp_allreduce hook):
+   * tp_peers[r] = rank r's symmetric buffer of alora_tp_buffer_bytes(max_tokens, d_model) bytes, zeroed
+   * before first use, mapped into this process (CUDA IPC: alora_ipc_get_handle / alora_ipc_open, or the
+   * same device pointers when the ranks are threads on one GPU: tp_colocated = 1). The O-projection and
+   * MLP-down write their fp32 partials into this rank's buffer and one kernel per rank sums every rank's
+   * partial in rank order, adds the residual and applies the next RMSNorm (graph-capturable). */
+  int32_t tp_rank;
+  void* const* tp_peers;
+  int32_t tp_colocated;
 } AloraModelDesc;
 
 /* One engine step: all spans packed back to back (varlen). Device arrays. */
@@ -317,6 +326,25 @@ typedef struct AloraStepDesc {
   int32_t lora_rows_max;
 } AloraStepDesc;
 
+/* Tensor-parallel peer buffers: bytes of one rank's symmetric buffer, device allocation (zeroed, a whole
+ * cudaMalloc allocation so that its IPC handle covers it), and the CUDA IPC handle exchange (64-byte
+ * handles; alora_ipc_open maps a peer's buffer with lazy peer access over NVLink). */
+int64_t alora_tp_buffer_bytes(int32_t max_tokens, int32_t d_model);
+/* Byte offset of partial slot `slot` (0 | 1) in a rank's buffer: [max_tokens, d_model] fp32 rows. */
+int64_t alora_tp_partial_offset(int32_t max_tokens, int32_t d_model, int32_t slot);
+int alora_device_alloc(int64_t bytes, void** out);
+int alora_device_free(void* p);
+int alora_ipc_get_handle(void* dev_ptr, uint8_t* out64);
+int alora_ipc_open(const uint8_t* handle64, void** out_ptr);
+int alora_ipc_close(void* ptr);
+/* The fused all-reduce + residual + RMSNorm on its own (what alora_model_forward launches after the
+ * row-parallel O-projection / MLP-down): x[M, d] += sum over ranks (rank order) of the partial in slot
+ * `slot` of every peer buffer; h = bf16(rmsnorm(x) * w) unless h is NULL. Every rank must make the same
+ * sequence of calls. */
+int alora_tp_allreduce_norm(void* const* peers, int32_t n_ranks, int32_t rank, int32_t colocated,
+                            int32_t max_tokens, int32_t slot, int32_t M, int32_t d, float* x, const float* w,
+                            float eps, void* h, void* stream);
+
 int64_t alora_model_workspace_bytes(const AloraModelDesc* desc);
 int alora_model_create(const AloraModelDesc* desc, void** out_handle);
 int alora_model_destroy(void* handle);
@@ -330,6 +358,10 @@ int alora_model_forward(void* handle, const AloraStepDesc* step, void* stream);
  * padded block-table width and context bound fall in the same bucket. Falls back to alora_model_forward
  * while profiling. */
 int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream);
+/* Capture (if not cached yet) the graph alora_model_forward_graph would replay for this step, without
+ * launching it: tensor-parallel ranks sharing one GPU capture before any rank starts spinning in the fused
+ * all-reduce (graph instantiation may wait for the device). */
+int alora_model_graph_prepare(void* handle, const AloraStepDesc* step, void* stream);
 /* Count of kernel launches issued by the last alora_model_forward. */
 int32_t alora_model_last_launches(void* handle);
 

@@ -60,6 +60,7 @@ class AloraModelDesc(ctypes.Structure):
         ("lora_o_down", ctypes.POINTER(c_void_p)), ("lora_o_up_t", ctypes.POINTER(c_void_p)),
         ("lora_in_down", ctypes.POINTER(c_void_p)), ("lora_in_up_t", ctypes.POINTER(c_void_p)),
         ("lora_out_down", ctypes.POINTER(c_void_p)), ("lora_out_up_t", ctypes.POINTER(c_void_p)),
+        ("tp_rank", c_i32), ("tp_peers", ctypes.POINTER(c_void_p)), ("tp_colocated", c_i32),
     ]
 
 
@@ -144,11 +145,21 @@ EXPORTS = {
                             c_i32, c_i32, c_i32, c_void_p, c_i64, c_void_p),
     "alora_gemm_workspace_bytes": _sig("alora_gemm_workspace_bytes", c_i64),
     "alora_argmax": _sig("alora_argmax", c_i32, c_void_p, c_i32, c_i32, c_void_p, c_void_p),
+    "alora_tp_buffer_bytes": _sig("alora_tp_buffer_bytes", c_i64, c_i32, c_i32),
+    "alora_tp_partial_offset": _sig("alora_tp_partial_offset", c_i64, c_i32, c_i32, c_i32),
+    "alora_device_alloc": _sig("alora_device_alloc", c_i32, c_i64, c_void_p),
+    "alora_device_free": _sig("alora_device_free", c_i32, c_void_p),
+    "alora_ipc_get_handle": _sig("alora_ipc_get_handle", c_i32, c_void_p, c_void_p),
+    "alora_ipc_open": _sig("alora_ipc_open", c_i32, c_void_p, c_void_p),
+    "alora_ipc_close": _sig("alora_ipc_close", c_i32, c_void_p),
+    "alora_tp_allreduce_norm": _sig("alora_tp_allreduce_norm", c_i32, c_void_p, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                    c_i32, c_i32, c_void_p, c_void_p, c_f32, c_void_p, c_void_p),
     "alora_model_workspace_bytes": _sig("alora_model_workspace_bytes", c_i64, ctypes.POINTER(AloraModelDesc)),
     "alora_model_create": _sig("alora_model_create", c_i32, ctypes.POINTER(AloraModelDesc),
                                ctypes.POINTER(c_void_p)),
     "alora_model_destroy": _sig("alora_model_destroy", c_i32, c_void_p),
     "alora_model_forward": _sig("alora_model_forward", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc), c_void_p),
+    "alora_model_graph_prepare": _sig("alora_model_graph_prepare", c_i32, c_void_p, c_void_p, c_void_p),
     "alora_model_forward_graph": _sig("alora_model_forward_graph", c_i32, c_void_p, ctypes.POINTER(AloraStepDesc),
                                       c_void_p),
     "alora_model_last_launches": _sig("alora_model_last_launches", c_i32, c_void_p),

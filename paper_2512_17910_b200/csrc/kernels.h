@@ -159,6 +159,12 @@ int qkv_finalize_bf16(const float* partials, int nparts, int M, int Nq, int Nkv,
 int lora_select_finalize_bf16(const float* partials, int nparts, int M, int SR, int rank, const int32_t* row_slot,
                               const uint8_t* row_apply, const uint8_t* slot_targets, __nv_bfloat16* s,
                               cudaStream_t st, int n_planes = 3, int tbit0 = 0);
+// Fused TP all-reduce + residual + RMSNorm over peer buffers (tp_allreduce.cu).
+void configure_tp();
+int64_t tp_buffer_bytes(int max_tokens, int d);
+float* tp_partial_slot(void* own, int max_tokens, int d, int slot);
+int tp_allreduce_norm(void* const* peers, int n, int rank, int colocated, int max_tokens, int slot, int M, int d,
+                      float* x, const float* w, float eps, __nv_bfloat16* h, cudaStream_t st);
 int lora_tile_masks(const int32_t* row_slot, const uint8_t* row_apply, int M, uint32_t* masks, cudaStream_t st);
 
 }  // namespace alora

@@ -29,6 +29,7 @@ void configure_kernels() {
     configure_kv_ops();
     configure_attention();
     configure_gemm();
+    configure_tp();
   });
 }
 }  // namespace alora
@@ -68,6 +69,7 @@ struct GraphEntry {
   AloraStepDesc step{};
   int32_t launches = 0;
   uint64_t last_use = 0;
+  bool uploaded = false;
 };
 // n_tokens, n_seqs, max_blocks, max_q, max_ctx, attention items, attention partitions (the grids a capture bakes in)
 using GraphKey = std::tuple<int, int, int, int, int, int, int>;
@@ -78,6 +80,7 @@ struct Model {
   // O / MLP adapter targets (empty = untargeted)
   std::vector<const void*> lora_o_down, lora_o_up_t, lora_in_down, lora_in_up_t, lora_out_down, lora_out_up_t;
   std::vector<const float*> attn_norm, mlp_norm;
+  std::vector<void*> tp_peers;  // fused TP all-reduce: every rank's symmetric buffer (empty = hook path)
   int32_t last_launches = 0;
   Profiler prof;
   std::map<GraphKey, GraphEntry> graphs;
@@ -157,7 +160,8 @@ Ws plan_ws(const AloraModelDesc& d) {
   w.part_bytes = d.dtype == ALORA_BF16 ? 8LL * std::min<int64_t>(T, 256) * std::max<int64_t>(nq + 2 * nkv, d.d_model) * 4 : 0;
   w.part = take(w.part_bytes);
   w.amax = take(S * 8);  // packed greedy argmax per span (fused into the lm_head epilogue)
-  w.tpd = take(d.tp_size > 1 ? T * d.d_model * 4 : 0);  // TP: this rank's residual delta, all-reduced in place
+  // TP through the hook: this rank's residual delta, all-reduced in place (the fused path uses the peer buffers)
+  w.tpd = take(d.tp_size > 1 && d.tp_peers == nullptr ? T * d.d_model * 4 : 0);
   w.total = off;
   return w;
 }
@@ -174,7 +178,10 @@ int validate(const AloraModelDesc* d) {
     return ALORA_EINVAL;
   if (d->n_slots < 0 || d->lora_rank < 0 || (d->n_slots > 0 && d->lora_rank < 1)) return ALORA_EINVAL;
   if (d->dtype == ALORA_BF16 && d->n_slots > 32) return ALORA_EINVAL;  // tile slot masks are 32-bit
-  if (d->tp_size > 1 && (d->dtype != ALORA_BF16 || d->tp_allreduce == nullptr)) return ALORA_EINVAL;
+  if (d->tp_size > 1 && (d->dtype != ALORA_BF16 || (d->tp_allreduce == nullptr && d->tp_peers == nullptr)))
+    return ALORA_EINVAL;
+  if (d->tp_size > 1 && d->tp_peers != nullptr && (d->tp_size > 8 || d->tp_rank < 0 || d->tp_rank >= d->tp_size))
+    return ALORA_EINVAL;
   return ALORA_OK;
 }
 
@@ -299,7 +306,10 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const int in_planes = llama ? 2 : 1;
   Launcher run{mdl, st};
   const bool tp = d.tp_size > 1;
+  const bool tp_fused = tp && !mdl.tp_peers.empty();
   float* tpd = reinterpret_cast<float*>(base + w.tpd);
+  int ar_i = 0;          // fused all-reduces issued so far in this forward (partial slot = parity)
+  bool h_ready = false;  // the fused all-reduce already produced the next RMSNorm's output in h
   // Residual-producing GEMM (O-projection, MLP-down). Unsharded: x += A.W^T fused in the epilogue, or the
   // split-K partials are left for the next RMSNorm. Tensor parallel: this rank's partial product is
   // materialised in tpd (split-K summed in order), all-reduced by the caller's hook, then applied by the
@@ -315,6 +325,12 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       pend = df.deferred ? df.splits_out : 0;
       pend_buf = part;
       return rc;
+    }
+    if (tp_fused) {  // this rank's partial -> its symmetric buffer slot, reduced by tp_allreduce_norm
+      float* slot = tp_partial_slot(mdl.tp_peers[d.tp_rank], d.max_tokens, dm, ar_i);
+      pend = 0;
+      return gemm_bf16(kEpiStore | 16, A, K, static_cast<const __nv_bfloat16*>(W), ldw, slot, dm, M, dm, K, gla,
+                       st, gw, 8, nullptr);
     }
     int rc = gemm_bf16(kEpiStore | 16, A, K, static_cast<const __nv_bfloat16*>(W), ldw, tpd, dm, M, dm, K, gla,
                        st, gw, 8, nullptr);
@@ -336,9 +352,20 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   RUN("embed", m_ * dm_ * 6, 0, embed_bf16(s.tokens, s.positions, static_cast<const __nv_bfloat16*>(d.embed),
                                            llama ? nullptr : d.pos_table, M, dm, x, st, s.next_ids));
   if (lora) RUN("lora_masks", m_ * 5, 0, lora_tile_masks(s.row_slot, s.row_apply, M, masks, st));
+  // fused TP: sum of every rank's partial (rank order) + residual + the next RMSNorm (norm_w) in one kernel
+  auto tp_reduce = [&](const float* norm_w, bool norm) -> int {
+    const int rc = tp_allreduce_norm(mdl.tp_peers.data(), d.tp_size, d.tp_rank, d.tp_colocated, d.max_tokens, ar_i,
+                                     M, dm, x, norm_w, d.rms_eps, norm ? h : nullptr, st);
+    ++ar_i;
+    h_ready = norm;
+    return rc;
+  };
+  const double tp_bytes = m_ * dm_ * 4.0 * (d.tp_size + 2) + m_ * dm_ * 2;
   for (int l = 0; l < d.n_layers; ++l) {
-    RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
-        residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    if (!h_ready)
+      RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+          residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
+    h_ready = false;
     pend = 0;
     GemmLora gl;
     if (lora && seg_shrink) {
@@ -425,9 +452,12 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     const GemmLora glo = lora_o ? target_lora(mdl.lora_o_up_t[l], dm, 1) : GemmLora{};
     RUN("gemm_o", gemm_bytes(m_, dm_, Nq_, 4, true) + (lora_o ? 2.0 * dm_ * ks_ : 0.0), 2.0 * m_ * dm_ * Nq_,
         residual_gemm(attn, Nq, mdl.w_o_t[l], Nq, lora_o ? &glo : nullptr));
-    if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
-    RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
-        residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    if (tp_fused) RUN("tp_allreduce", tp_bytes, 0, tp_reduce(mdl.mlp_norm[l], true));
+    else if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
+    if (!h_ready)
+      RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+          residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
+    h_ready = false;
     pend = 0;
     const double n_in = llama ? 2 * F_ : F_;
     if (lora_in)
@@ -444,7 +474,12 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     const GemmLora glw = lora_out ? target_lora(mdl.lora_out_up_t[l], dm, 1) : GemmLora{};
     RUN("gemm_mlp_out", gemm_bytes(m_, dm_, F_, 4, true) + (lora_out ? 2.0 * dm_ * ks_ : 0.0), 2.0 * m_ * dm_ * F_,
         residual_gemm(act, F, mdl.w_out_t[l], F, lora_out ? &glw : nullptr));
-    if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
+    if (tp_fused) {
+      const bool last = l + 1 == d.n_layers;  // the final norm runs on the last rows only (below)
+      RUN("tp_allreduce", tp_bytes, 0, tp_reduce(last ? nullptr : mdl.attn_norm[l + 1], !last));
+    } else if (tp) {
+      RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
+    }
   }
   // greedy argmax fused into the lm_head epilogue (weight-streaming path: S <= 256 spans, vocab % 32 == 0)
   auto* amax = reinterpret_cast<unsigned long long*>(base + w.amax);
@@ -668,6 +703,15 @@ int alora_model_create(const AloraModelDesc* desc, void** out_handle) {
     delete m;
     return ALORA_EINVAL;
   }
+  if (desc->tp_size > 1 && desc->tp_peers) {
+    m->tp_peers.assign(desc->tp_peers, desc->tp_peers + desc->tp_size);
+    for (void* p : m->tp_peers)
+      if (!p) {
+        delete m;
+        return ALORA_EINVAL;
+      }
+  }
+  m->d.tp_peers = nullptr;
   *out_handle = m;
   return ALORA_OK;
 }
@@ -693,13 +737,9 @@ static bool same_step_buffers(const AloraStepDesc& a, const AloraStepDesc& b) {
          a.row_seq == b.row_seq && a.attn_plan == b.attn_plan && a.attn_segs == b.attn_segs && a.attn_sets == b.attn_sets;
 }
 
-int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream) {
-  if (!handle || !step) return ALORA_EINVAL;
-  Model& m = *static_cast<Model*>(handle);
-  if (m.d.dtype != ALORA_BF16 || m.prof.on) return alora_model_forward(handle, step, stream);
-  if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
-    return ALORA_EINVAL;
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
+// The captured forward for this step shape (capturing on first sight); nullptr + rc on failure.
+static GraphEntry* graph_for(Model& m, const AloraStepDesc* step, cudaStream_t st, int* rc_out) {
+  *rc_out = ALORA_OK;
   const GraphKey key{step->n_tokens, step->n_seqs, step->max_blocks, step->max_q, step->max_ctx,
                      step->attn_plan ? step->attn_items : -1,
                      (step->attn_plan ? step->attn_max_parts : -1) * 2 + (step->lora_rows_max <= kSegMaxRows ? 1 : 0)};
@@ -718,25 +758,65 @@ int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* str
       m.graphs.erase(lru);
     }
     cudaGraph_t g = nullptr;
-    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return ALORA_ECUDA;
+    if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+      *rc_out = ALORA_ECUDA;
+      return nullptr;
+    }
     const int rc = forward_bf16(m, *step, st);
     const cudaError_t ce = cudaStreamEndCapture(st, &g);
     if (rc != ALORA_OK) {
       if (g) cudaGraphDestroy(g);
-      return rc;
+      *rc_out = rc;
+      return nullptr;
     }
-    if (ce != cudaSuccess || g == nullptr) return ALORA_ECUDA;
+    if (ce != cudaSuccess || g == nullptr) {
+      *rc_out = ALORA_ECUDA;
+      return nullptr;
+    }
     GraphEntry e;
     const cudaError_t ie = cudaGraphInstantiate(&e.exec, g, 0);
     cudaGraphDestroy(g);
-    if (ie != cudaSuccess) return ALORA_ECUDA;
+    if (ie != cudaSuccess) {
+      *rc_out = ALORA_ECUDA;
+      return nullptr;
+    }
     e.step = *step;
     e.launches = m.last_launches;
     it = m.graphs.emplace(key, e).first;
   }
-  it->second.last_use = ++m.graph_clock;
-  m.last_launches = it->second.launches;
-  return cudaGraphLaunch(it->second.exec, st) == cudaSuccess ? ALORA_OK : ALORA_ECUDA;
+  return &it->second;
+}
+
+int alora_model_forward_graph(void* handle, const AloraStepDesc* step, void* stream) {
+  if (!handle || !step) return ALORA_EINVAL;
+  Model& m = *static_cast<Model*>(handle);
+  if (m.d.dtype != ALORA_BF16 || m.prof.on) return alora_model_forward(handle, step, stream);
+  if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
+    return ALORA_EINVAL;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc;
+  GraphEntry* e = graph_for(m, step, st, &rc);
+  if (!e) return rc;
+  e->last_use = ++m.graph_clock;
+  m.last_launches = e->launches;
+  return cudaGraphLaunch(e->exec, st) == cudaSuccess ? ALORA_OK : ALORA_ECUDA;
+}
+
+int alora_model_graph_prepare(void* handle, const AloraStepDesc* step, void* stream) {
+  if (!handle || !step) return ALORA_EINVAL;
+  Model& m = *static_cast<Model*>(handle);
+  if (m.d.dtype != ALORA_BF16 || m.prof.on) return ALORA_OK;
+  if (step->n_tokens < 1 || step->n_tokens > m.d.max_tokens || step->n_seqs < 1 || step->n_seqs > m.d.max_seqs)
+    return ALORA_EINVAL;
+  int rc;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  GraphEntry* e = graph_for(m, step, st, &rc);
+  if (!e) return rc;
+  if (!e->uploaded) {  // the first launch would upload the executable graph: do it here, off the critical path
+    if (cudaGraphUpload(e->exec, st) != cudaSuccess || cudaStreamSynchronize(st) != cudaSuccess) return ALORA_ECUDA;
+    e->uploaded = true;
+  }
+  return ALORA_OK;
 }
 
 int32_t alora_model_last_launches(void* handle) {

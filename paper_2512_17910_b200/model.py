@@ -350,6 +350,9 @@ class Model:
         tp = getattr(self, "_tp", None)  # (size, allreduce hook address): set by tp.TPModel
         if tp is not None:
             D.tp_size, D.tp_allreduce = tp
+        tpf = getattr(self, "_tp_fused", None)  # (rank, peer buffer array, colocated): fused all-reduce
+        if tpf is not None:
+            D.tp_rank, D.tp_peers, D.tp_colocated = tpf
         if probe:
             return D
         D.embed, D.unembed_t = self.embed.data_ptr(), self.unembed_t.data_ptr()

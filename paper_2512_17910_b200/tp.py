@@ -18,11 +18,20 @@ native executor on a smaller "model":
     tables and block hashes are identical on every rank because every rank
     runs the same deterministic scheduler on the same requests.
 
-Groups: `TorchDistGroup` all-reduces with torch.distributed (NCCL on B200s,
-one process per GPU); `ThreadGroup` runs the ranks as threads of one process
-(each on its own CUDA stream) and reduces on the device -- the single-GPU
-harness the GPU tests use to check the sharded forward against the unsharded
-one.
+The all-reduce. By default (`fused=True`) it is the executor's own kernel
+(csrc/tp_allreduce.cu): every rank maps every other rank's symmetric buffer
+(alora_tp_buffer_bytes), the row-parallel GEMM writes its fp32 partial into its
+own buffer, and one kernel per rank sums all ranks' partials in rank order over
+peer memory (NVLink / NVSwitch), adds the residual and applies the next RMSNorm
+-- no host round trip, so the whole TP forward is CUDA-graph capturable.
+`fused=False` keeps the host hook (group.all_reduce through torch.distributed).
+
+Groups: `TorchDistGroup` is one process per GPU: its peer buffers are exchanged
+as CUDA IPC handles over the torch.distributed group (NCCL on B200s), and its
+hook path all-reduces with NCCL. `ThreadGroup` runs the ranks as threads of one
+process (each on its own CUDA stream, peer buffers are plain device memory of
+the one GPU) -- the single-GPU harness the GPU tests use to check the sharded
+forward against the unsharded one.
 """
 
 import ctypes
@@ -102,6 +111,8 @@ def _tensor_at(ptr: int, count: int):
 class TorchDistGroup:
     """One process per GPU: in-place sum all-reduce over a torch.distributed process group (NCCL)."""
 
+    colocated = False
+
     def __init__(self, group=None):
         import torch.distributed as dist
 
@@ -109,9 +120,44 @@ class TorchDistGroup:
         self.group = group
         self.size = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
+        self._own = None
+        self._opened = []
 
     def all_reduce(self, t) -> None:
         self._dist.all_reduce(t, op=self._dist.ReduceOp.SUM, group=self.group)
+
+    def peer_buffers(self, nbytes: int) -> list:
+        """Allocate this rank's symmetric buffer and map every peer's (CUDA IPC handles exchanged over the
+        group); returns the device pointer of each rank's buffer in this process, in rank order."""
+        lib = _native.lib
+        own = ctypes.c_void_p()
+        _native.check(lib.alora_device_alloc(int(nbytes), ctypes.byref(own)), "alora_device_alloc")
+        self._own = own.value
+        handle = (ctypes.c_uint8 * 64)()
+        _native.check(lib.alora_ipc_get_handle(self._own, handle), "alora_ipc_get_handle")
+        handles = [None] * self.size
+        self._dist.all_gather_object(handles, (self.rank, bytes(handle)), group=self.group)
+        ptrs = [0] * self.size
+        for r, h in handles:
+            if r == self.rank:
+                ptrs[r] = self._own
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_uint8 * 64).from_buffer_copy(h)
+            _native.check(lib.alora_ipc_open(buf, ctypes.byref(p)), "alora_ipc_open")
+            self._opened.append(p.value)
+            ptrs[r] = p.value
+        self._dist.barrier(group=self.group)
+        return ptrs
+
+    def close(self) -> None:
+        for p in self._opened:
+            _native.lib.alora_ipc_close(p)
+        self._opened = []
+        if self._own:
+            self._dist.barrier(group=self.group)  # no peer still maps it
+            _native.lib.alora_device_free(self._own)
+            self._own = None
 
 
 class ThreadGroup:
@@ -122,14 +168,36 @@ class ThreadGroup:
         self.size = size
         self._barrier = threading.Barrier(size)
         self._slots = [None] * size
+        self._buffers = None
+        self._lock = threading.Lock()
 
     def rank_view(self, rank: int):
         return _ThreadRank(self, rank)
 
+    def peer_buffers(self, nbytes: int) -> list:
+        import torch
+
+        with self._lock:
+            if self._buffers is None or self._buffers[0].numel() < nbytes:
+                self._buffers = [torch.zeros(int(nbytes), dtype=torch.uint8, device="cuda") for _ in range(self.size)]
+                torch.cuda.synchronize()
+            return [b.data_ptr() for b in self._buffers]
+
 
 class _ThreadRank:
+    colocated = True  # every rank on the same GPU
+
     def __init__(self, parent: ThreadGroup, rank: int):
         self.parent, self.rank, self.size = parent, rank, parent.size
+
+    def peer_buffers(self, nbytes: int) -> list:
+        return self.parent.peer_buffers(nbytes)
+
+    def launch_barrier(self) -> None:
+        """Every rank has finished its host-side step preparation before any rank enqueues the forward: a
+        rank spinning in the fused all-reduce must not meet a peer still inside a device-synchronising
+        CUDA call (an allocation or pageable copy while staging), which would wait for the spinner."""
+        self.parent._barrier.wait()
 
     def all_reduce(self, t) -> None:
         import torch
@@ -156,7 +224,7 @@ class TPModel(Model):
     """
 
     def __init__(self, config: ModelConfig, group, weights: BaseWeights | None = None, init: str = "philox",
-                 **kw):
+                 fused: bool = True, **kw):
         self.full_config = config
         self.tp_group = group
         scfg = shard_config(config, group.size)
@@ -176,11 +244,35 @@ class TPModel(Model):
                 return _native.ALORA_ECUDA
 
         self._tp_cb = _native.ALLREDUCE_FN(_cb)  # kept alive for the handle's lifetime
-        self._tp = (group.size, ctypes.cast(self._tp_cb, ctypes.c_void_p).value) if group.size > 1 else None
-        # the all-reduce hook is a host callback (stream syncs / host barriers): not capturable in a CUDA graph
-        kw.setdefault("graphs", group.size <= 1)
+        fused = fused and group.size > 1 and hasattr(group, "peer_buffers")
+        self._tp_fused = None
+        if fused:
+            # the peer-buffer layout is sized for a fixed step capacity: the workspace never grows past it
+            self._tp_max_tokens = int(kw.get("max_tokens", 2048))
+            nbytes = int(_native.lib.alora_tp_buffer_bytes(self._tp_max_tokens, config.d_model))
+            peers = group.peer_buffers(nbytes)
+            arr = (ctypes.c_void_p * group.size)(*peers)
+            self._tp_peer_arr = arr
+            self._tp_fused = (group.rank, ctypes.cast(arr, ctypes.POINTER(ctypes.c_void_p)), int(group.colocated))
+            self._tp = (group.size, None)
+            import os
+            if os.environ.get("ALORA_TP_GRAPHS", "1") == "0":  # debug / A-B: eager decode steps
+                kw["graphs"] = False
+        else:
+            self._tp = (group.size, ctypes.cast(self._tp_cb, ctypes.c_void_p).value) if group.size > 1 else None
+            # the all-reduce hook is a host callback (stream syncs / host barriers): not capturable in a graph
+            kw.setdefault("graphs", group.size <= 1)
         super().__init__(scfg, weights=weights, init=init, **kw)
         self.pool_kv_width = scfg.kv_width
+
+    def _grow_workspace(self, tokens: int):
+        if self._tp_fused is not None:
+            if tokens > self._tp_max_tokens:
+                raise ValueError(f"step of {tokens} rows exceeds the TP model's max_tokens {self._tp_max_tokens}")
+            if self._ws is not None:
+                return
+            tokens = self._tp_max_tokens
+        super()._grow_workspace(tokens)
 
     def _slot_for(self, adapter: LoraAdapter | None) -> int:
         if adapter is None:
@@ -193,6 +285,14 @@ class TPModel(Model):
 
     def launch(self, st) -> None:
         self._tp_error = None
+        if self._tp_fused is not None and getattr(self.tp_group, "colocated", False):
+            if self._staged_graphable and not getattr(self, "_profiling", False):  # capture before the barrier
+                gs = self._graph_stream
+                gs.wait_stream(self._torch.cuda.current_stream())
+                _native.check(_native.lib.alora_model_graph_prepare(self._handle, ctypes.byref(st),
+                                                                    ctypes.c_void_p(gs.cuda_stream)),
+                              "alora_model_graph_prepare")
+            self.tp_group.launch_barrier()
         try:
             super().launch(st)
         finally:

@@ -9,6 +9,12 @@ import json
 import os
 import sys
 
+# Tensor-parallel tests run several ranks as threads of one process on one GPU, each with its own streams,
+# spinning in the fused all-reduce until every peer arrives. With the default 8 hardware work queues, 8 ranks'
+# 16 streams share queues and a rank's kernels can sit behind a peer's spinning kernel (a false dependency
+# that deadlocks until the barrier timeout). Must be set before the CUDA context exists.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 import numpy as np
 import pytest
 

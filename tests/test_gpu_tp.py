@@ -1,9 +1,13 @@
-"""Tensor-parallel native forward on one B200: two TPModel ranks (threads, own CUDA streams) vs unsharded.
+"""Tensor-parallel native forward on one B200: TPModel ranks (threads, own CUDA streams) vs unsharded.
 
-The ranks run the sm_100a executor on their shards (half the q/kv heads, half the FFN) and meet in
-alora_model_forward's tp_allreduce hook after the row-parallel O-projection and MLP-down
-(tp.ThreadGroup: a device-side sum in rank order). Logits, greedy ids and each rank's slice of the
-paged KV cache must match the unsharded bf16 model within the bf16 tolerance of SURVEY.md §8(c).
+The ranks run the sm_100a executor on their shards (1/T of the q/kv heads and of the FFN) and meet after
+the row-parallel O-projection and MLP-down (reference model.py:269-271, sharded as SURVEY.md §8(e)):
+either in the fused kernel (default: every rank's GEMM writes its fp32 partial into its symmetric buffer,
+one kernel per rank sums all partials in rank order, adds the residual and applies the next RMSNorm --
+here the "peer" buffers are device memory of the one GPU) or through the host hook (tp.ThreadGroup: a
+device-side sum in rank order). Logits, greedy ids and each rank's slice of the paged KV cache must match
+the unsharded model / the oracle within the bf16 tolerance of SURVEY.md §8(c); the fused and hook paths
+sum in the same order, so they agree bitwise.
 """
 
 import threading
@@ -31,7 +35,29 @@ def _spans(cfg, adapter):
     return pre, suf
 
 
-def test_tp2_threaded_ranks_match_unsharded_model():
+def _run_ranks(ranks, fn, timeout=300):
+    out, errs = [None] * len(ranks), []
+
+    def run(r):
+        try:
+            with torch.cuda.stream(torch.cuda.Stream()):
+                out[r] = fn(r)
+                torch.cuda.current_stream().synchronize()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(len(ranks))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=timeout)
+    assert not errs, errs
+    assert all(o is not None for o in out)
+    return out
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "hook"])
+def test_tp2_threaded_ranks_match_unsharded_model(fused):
     cfg = P.ModelConfig(**CFG)
     ad = P.generate_adapter("adapter0", cfg.d_model, 8, seed=1, invocation_tokens=(500, 501, 502),
                             kv_width=cfg.kv_width, q_width=cfg.q_width)
@@ -42,7 +68,7 @@ def test_tp2_threaded_ranks_match_unsharded_model():
     want = full.forward_step([suf], pool.kv)["r0"]
 
     group = P.ThreadGroup(2)
-    ranks = [P.TPModel(cfg, group.rank_view(r)) for r in range(2)]
+    ranks = [P.TPModel(cfg, group.rank_view(r), fused=fused) for r in range(2)]
     pools = [P.BlockPool(8, 16, cfg.n_layers, cfg.d_model, kv_width=m.pool_kv_width, dtype="bf16") for m in ranks]
     out, errs = [None, None], []
 
@@ -74,3 +100,172 @@ def test_tp2_threaded_ranks_match_unsharded_model():
         ref = full_kv[..., r * w:(r + 1) * w]
         rel = np.linalg.norm(got - ref) / np.linalg.norm(ref)
         assert rel < 1e-2, (r, rel)
+
+
+def test_tp2_fused_equals_hook_bitwise_with_decode_graphs():
+    """The fused kernel and the host-hook all-reduce sum the same partials in the same order: identical logits
+    and KV, through a prefill, a masked suffix and 3 decode steps (fused: decode steps replay CUDA graphs
+    that contain the all-reduce kernel)."""
+    cfg = P.ModelConfig(**CFG)
+    ad = P.generate_adapter("adapter0", cfg.d_model, 8, seed=1, invocation_tokens=(500, 501, 502),
+                            kv_width=cfg.kv_width, q_width=cfg.q_width)
+    pre, suf = _spans(cfg, ad)
+    n = suf.start_pos + len(suf.tokens)
+    res = {}
+    for fused in (True, False):
+        group = P.ThreadGroup(2)
+        ranks = [P.TPModel(cfg, group.rank_view(r), fused=fused) for r in range(2)]
+        pools = [P.BlockPool(8, 16, cfg.n_layers, cfg.d_model, kv_width=m.pool_kv_width, dtype="bf16")
+                 for m in ranks]
+
+        def fn(r):
+            m, kv = ranks[r], pools[r].kv
+            m.forward_step([pre], kv)
+            logits = [m.forward_step([suf], kv)["r0"]]
+            for step in range(3):
+                tok = np.array([int(np.argmax(logits[-1]))])
+                logits.append(m.forward_step([P.SeqInput("r0", tok, n + step, list(range(4)), ad,
+                                                         np.array([False]))], kv)["r0"])
+            return np.stack(logits), kv.float().cpu().numpy()
+
+        res[fused] = _run_ranks(ranks, fn)
+    for r in range(2):
+        np.testing.assert_array_equal(res[True][r][0], res[False][r][0])
+        np.testing.assert_array_equal(res[True][r][1], res[False][r][1])
+
+
+@pytest.mark.parametrize("fused", [True, False], ids=["fused", "hook"])
+def test_tp8_llama70b_shard_geometry_vs_oracle(fused):
+    """Llama-3-70B at TP=8, the per-rank shard of C5 (H 8, Hkv 1, d 8192, FFN 3584, head_dim 128), 2 layers,
+    8 ranks as threads of one B200 with the fused all-reduce + RMSNorm, against the unsharded oracle (bf16
+    numerics): a base prefix, 4 aLoRA adapters' masked suffixes over it, then 2 decode steps."""
+    import oracle as O
+    from test_gpu_bench_geometry import _weights
+    dims = dict(arch="llama", n_heads=64, n_kv_heads=8, head_dim=128, d_model=8192, ffn_dim=28672,
+                vocab_size=32768)
+    T, L = 8, 2
+    pw, ow = _weights(dims, L, seed=3)
+    cfg = P.ModelConfig(**dims, n_layers=L, max_seq_len=1024, dtype="bf16")
+    ocfg = O.OracleConfig(**dims, n_layers=L, max_seq_len=1024, numerics="bf16")
+    om = O.OracleModel(ocfg, ow).to_f64()
+    V = dims["vocab_size"]
+    pads, oads = [], []
+    for k in range(4):
+        inv = P.invocation_for(V, k)
+        pads.append(P.generate_adapter(f"adapter{k}", cfg.d_model, 32, seed=k, invocation_tokens=inv,
+                                       kv_width=cfg.kv_width, q_width=cfg.q_width))
+        oads.append(O.oracle_adapter(f"adapter{k}", ocfg, 32, seed=k, invocation_tokens=inv))
+    rng = np.random.default_rng(0)
+    conv = rng.integers(0, V - 32, 45)
+    B = 16
+    reqs = []  # every adapter evaluates the same conversation: shared prefix blocks 0, 1, own tail blocks
+    for k in range(4):
+        toks = np.concatenate([conv, [V - 1], P.invocation_for(V, k), rng.integers(0, V - 32, 2)])
+        reqs.append((f"a{k}", toks, [0, 1] + [2 + 2 * k, 3 + 2 * k], k, 46))
+    group = P.ThreadGroup(T)
+    ranks = [P.TPModel(cfg, group.rank_view(r), weights=pw, max_tokens=256, fused=fused) for r in range(T)]
+    del pw
+    pools = [P.BlockPool(16, B, L, cfg.d_model, kv_width=m.pool_kv_width, dtype="bf16") for m in ranks]
+    okv = np.zeros((16, L, 2, B, ocfg.kv_width), np.float32)
+    steps = [[(None, conv[:48 - 16], 0)]]  # base prefix: 32 tokens = blocks 0, 1
+    steps.append([(k, reqs[k][1][32:], 32) for k in range(4)])  # suffixes (18 tokens each)
+    res = {"dlogit": [], "decided": 0, "agree": 0}
+
+    def spans(step, nxt):
+        o_s, p_s = [], []
+        for item in step:
+            k, toks, start = item
+            if k is None:
+                o_s.append(O.OracleSpan("base", toks, start, [0, 1]))
+                p_s.append(P.SeqInput("base", toks, start, [0, 1]))
+                continue
+            rid, _, table, ki, inv_start = reqs[k]
+            mask = np.arange(start, start + len(toks)) < inv_start
+            o_s.append(O.OracleSpan(rid, toks, start, table, oads[ki], mask))
+            p_s.append(P.SeqInput(rid, toks, start, table, pads[ki], mask))
+        return o_s, p_s
+
+    nxt = {}
+    n_full = len(reqs[0][1])
+    for si in range(4):
+        if si < 2:
+            step = steps[si]
+        else:  # decode: teacher-forced with the oracle's greedy token
+            step = [(k, np.array([nxt[f"a{k}"]]), n_full + si - 2) for k in range(4)]
+        o_s, p_s = spans(step, nxt)
+        print(f"[tp8] step {si}: {sum(len(x.tokens) for x in p_s)} rows", flush=True)
+        got = _run_ranks(ranks, lambda r: ranks[r].forward_step(p_s, pools[r].kv), timeout=600)
+        want = om.forward_step(o_s, okv, batch_head=True)
+        for r in range(1, T):
+            for rid in want:
+                np.testing.assert_array_equal(got[r][rid], got[0][rid])  # replicated outputs agree bitwise
+        for rid in want:
+            res["dlogit"].append(float(np.max(np.abs(got[0][rid] - want[rid]))))
+            top2 = np.partition(want[rid], -2)[-2:]
+            if top2[1] - top2[0] > 2 * 5e-2:
+                res["decided"] += 1
+                res["agree"] += int(np.argmax(got[0][rid])) == int(np.argmax(want[rid]))
+        nxt = {rid: int(np.argmax(v)) for rid, v in want.items()}
+    # each rank's pool holds its kv head (kv_width 128) of the full [.., 8 * 128]
+    w = ranks[0].pool_kv_width
+    rels = []
+    for r in range(T):
+        got_kv = pools[r].kv.float().cpu().numpy()
+        ref = okv[..., r * w:(r + 1) * w]
+        rels.append(float(np.linalg.norm(got_kv - ref) / np.linalg.norm(ref)))
+    print(f"[parity] TP=8 70B shard: max |dlogit| {max(res['dlogit']):.3g}, KV rel-L2 {max(rels):.3g}, greedy "
+          f"{res['agree']}/{res['decided']} decided")
+    assert max(res["dlogit"]) <= 5e-2 and max(rels) <= 1e-2
+    assert res["agree"] == res["decided"]
+
+
+@pytest.mark.parametrize("n,M,d", [(2, 8, 512), (2, 300, 4096), (8, 4, 8192), (8, 32, 8192), (8, 77, 8192),
+                                   (4, 200, 2048)])
+def test_tp_allreduce_norm_kernel(n, M, d):
+    """alora_tp_allreduce_norm alone, n ranks as threads on one GPU: x += sum of the n partials (rank order),
+    h = bf16(rmsnorm(x) * w), identical on every rank; one-shot and two-shot sizes; 3 calls (both slots)."""
+    import ctypes
+    from paper_2512_17910_b200 import _native
+    lib = _native.lib
+    T = 512
+    nbytes = lib.alora_tp_buffer_bytes(T, d)
+    group = P.ThreadGroup(n)
+    peers = group.peer_buffers(nbytes)
+    arr = (ctypes.c_void_p * n)(*peers)
+    g = torch.Generator(device="cuda").manual_seed(n * 1000 + M)
+    x0 = torch.randn(M, d, device="cuda", generator=g)
+    w = (1 + 0.1 * torch.randn(d, device="cuda", generator=g)).float()
+    parts = [[torch.randn(M, d, device="cuda", generator=g) for _ in range(n)] for _ in range(3)]
+    xs = [x0.clone() for _ in range(n)]
+    hs = [torch.empty(M, d, dtype=torch.bfloat16, device="cuda") for _ in range(n)]
+    torch.cuda.synchronize()
+
+    def fn(r):
+        for call in range(3):
+            slot = call & 1
+            off = lib.alora_tp_partial_offset(T, d, slot)
+            dst = _tensor(peers[r] + off, M * d).view(M, d)
+            dst.copy_(parts[call][r])
+            rc = lib.alora_tp_allreduce_norm(arr, n, r, 1, T, slot, M, d, ctypes.c_void_p(xs[r].data_ptr()),
+                                             ctypes.c_void_p(w.data_ptr()), 1e-5, ctypes.c_void_p(hs[r].data_ptr()),
+                                             ctypes.c_void_p(torch.cuda.current_stream().cuda_stream))
+            assert rc == 0
+        return True
+
+    _run_ranks(list(range(n)), fn, timeout=120)
+    want = x0.clone()
+    for call in range(3):
+        s = parts[call][0].clone()
+        for r in range(1, n):
+            s += parts[call][r]
+        want += s
+    hw = (want * torch.rsqrt(want.pow(2).mean(-1, keepdim=True) + 1e-5) * w).to(torch.bfloat16)
+    for r in range(n):
+        assert torch.equal(xs[r], xs[0]) and torch.equal(hs[r], hs[0])
+    assert torch.allclose(xs[0], want, atol=1e-4, rtol=1e-5)
+    assert (hs[0].float() - hw.float()).abs().max().item() < 5e-2
+
+
+def _tensor(ptr, count):
+    from paper_2512_17910_b200.tp import _tensor_at
+    return _tensor_at(ptr, count)
