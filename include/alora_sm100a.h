@@ -298,6 +298,12 @@ typedef struct AloraModelDesc {
   int32_t tp_rank;
   void* const* tp_peers;
   int32_t tp_colocated;
+  /* batch-invariant numerics (bf16 tier): every row of every step goes through the same kernels with the
+   * same reduction order -- one weight-streaming GEMM kernel and K range (no M-dependent split-K or
+   * swap-AB decode GEMM), the segmented (or per-row) LoRA shrink, one tcgen05 attention kernel with a single
+   * KV partition per row -- so a token's KV and logits are bitwise independent of batching, chunking and
+   * decode vs prefill (the reference's property, model.py:95-98; tests/test_model.py:167-202). Slower. */
+  int32_t batch_invariant;
 } AloraModelDesc;
 
 /* One engine step: all spans packed back to back (varlen). Device arrays. */

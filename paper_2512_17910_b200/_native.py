@@ -61,6 +61,7 @@ class AloraModelDesc(ctypes.Structure):
         ("lora_in_down", ctypes.POINTER(c_void_p)), ("lora_in_up_t", ctypes.POINTER(c_void_p)),
         ("lora_out_down", ctypes.POINTER(c_void_p)), ("lora_out_up_t", ctypes.POINTER(c_void_p)),
         ("tp_rank", c_i32), ("tp_peers", ctypes.POINTER(c_void_p)), ("tp_colocated", c_i32),
+        ("batch_invariant", c_i32),
     ]
 
 

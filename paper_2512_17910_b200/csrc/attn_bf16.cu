@@ -1841,7 +1841,8 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
   static const bool no_dec = getenv("ALORA_ATTN_NO_DECODE") != nullptr;  // A/B switch
   const int Gq = H / Hkv;
   const int64_t kv_rows_all = (int64_t)total_blocks * n_layers * 2 * B;
-  const bool decode = !no_dec && max_q == 1 && (Gq == 1 || Gq == 2 || Gq == 4 || Gq == 8) && total_blocks > 0 &&
+  const bool decode = !no_dec && !g_batch_invariant && max_q == 1 && (Gq == 1 || Gq == 2 || Gq == 4 || Gq == 8) &&
+                      total_blocks > 0 &&
                       B <= kDecKeys && kDecKeys % B == 0 && kv_rows_all < (1ll << 31);
   if (decode) {
     plan_decode(n_seqs, max_ctx, Hkv, D, a.part_size, a.n_parts);
@@ -1854,6 +1855,10 @@ int attn_bf16(const __nv_bfloat16* q, int64_t ld_q, int M, int n_seqs, const int
     }
   } else {
     plan(n_seqs, max_q, max_ctx, H, Hkv, D, a.part_size, a.n_parts, a.n_qtiles);
+    if (g_batch_invariant) {  // one partition: a row's key tiles and softmax order never depend on the step
+      a.n_parts = 1;
+      a.part_size = (max_ctx + kKT - 1) / kKT * kKT;
+    }
   }
   if (a.n_parts > 1) {
     const int64_t need = (int64_t)a.n_parts * M * H * (D + 2) * 4 + (int64_t)kMaxCounters * 4;

@@ -1322,6 +1322,32 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (M == 0 || N == 0) return ALORA_OK;
   if (M < 0 || N < 0 || K < 1 || lda % 8 || ldb % 8 || ldc % 8) return ALORA_EINVAL;
   const int base_epi = epi & 15;
+  if (g_batch_invariant && M > 2 * kBM) {
+    // batch-invariant mode: every row goes through the same weight-streaming kernel with one K range, so
+    // rows larger steps are cut into 256-row launches (row offsets into A, C, the shrink planes, the tile
+    // slot masks and the positions)
+    if (base_epi == kEpiLoraSelect) return ALORA_EINVAL;
+    const int esz = (base_epi == kEpiAdd || (epi & 16)) ? 4 : 2;
+    for (int r0 = 0; r0 < M; r0 += 2 * kBM) {
+      const int mc = std::min(2 * kBM, M - r0);
+      GemmLora lc;
+      if (lora) {
+        lc = *lora;
+        if (lc.s) {
+          lc.s_rows = lora->s_rows > 0 ? lora->s_rows : M;
+          lc.s = lora->s + (int64_t)r0 * lora->ks;
+        }
+        if (lc.tile_slot_mask) lc.tile_slot_mask = lora->tile_slot_mask + r0 / kBM;
+        if (lc.positions) lc.positions = lora->positions + r0;
+        if (lc.argmax) lc.argmax = lora->argmax + r0;
+      }
+      void* cc = static_cast<char*>(Cout) + (int64_t)r0 * ldc * esz;
+      const int rc = gemm_bf16(epi, A + (int64_t)r0 * lda, lda, Bt, ldb, cc, ldc, mc, N, K, lora ? &lc : nullptr, st,
+                               ws, max_splits, nullptr);
+      if (rc != ALORA_OK) return rc;
+    }
+    return ALORA_OK;
+  }
   if (N % 32 != 0) return ALORA_EINVAL;
   if (base_epi == kEpiSwiglu && N % 128 != 0) return ALORA_EINVAL;
   // Tile width: large M keeps 128 (256 for SwiGLU); small M (weight streaming, <= 2 row tiles) picks the
@@ -1386,7 +1412,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (lora != nullptr && lora->s != nullptr && lora->ks > 0) {
     if (lora->ks % 8 || (lora->n_q % BN) || (lora->n_kv % BN) || lora->rank < 1) return ALORA_EINVAL;
     if (lora->s_planes < 1 || lora->planes > lora->s_planes) return ALORA_EINVAL;
-    if (!make_tmap_3d(&ts, lora->s, lora->s_planes, M, lora->ks, kBM, kBK)) return ALORA_ECUDA;
+    if (!make_tmap_3d(&ts, lora->s, lora->s_planes, M, lora->ks, kBM, kBK, lora->s_rows)) return ALORA_ECUDA;
     if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks * up_planes, lora->ks * up_planes, BN, kBK)) return ALORA_ECUDA;
     args.ks = lora->ks;
     args.rank = lora->rank;
@@ -1396,7 +1422,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     args.tile_slot_mask = lora->tile_slot_mask;
   }
   static const bool no_dec = getenv("ALORA_GEMM_NO_DEC") != nullptr;  // A/B switch off the swap-AB decode GEMM
-  if (M <= 32 && !no_dec && N % kBM == 0 && K % kBK == 0) {
+  if (M <= 32 && !no_dec && !g_batch_invariant && N % kBM == 0 && K % kBK == 0) {
     const bool defer_ok = defer != nullptr && defer->partial != nullptr;
     int mode = -1;
     if (base_epi == kEpiAdd && !(epi & 16)) mode = defer_ok ? kDecPartial : kDecAdd;
@@ -1433,7 +1459,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
       if (lora != nullptr && lora->s != nullptr && lora->ks > 0) {
         if (lora->ks % 8 || (lora->n_q % kBM) || (lora->n_kv % kBM) || lora->rank < 1) return ALORA_EINVAL;
         if (!make_tmap_2d(&tu, lora->up_t, N, lora->ks * up_planes, lora->ks * up_planes, kBM, kBK)) return ALORA_ECUDA;
-        if (!make_tmap_3d(&tsm, lora->s, lora->s_planes, M, lora->ks, MN, kBK)) return ALORA_ECUDA;
+        if (!make_tmap_3d(&tsm, lora->s, lora->s_planes, M, lora->ks, MN, kBK, lora->s_rows)) return ALORA_ECUDA;
         da.ks = lora->ks;
         da.rank = lora->rank;
         da.n_q = lora->n_q;
@@ -1448,7 +1474,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (M <= 2 * kBM && !no_ws) {
     // weight streaming: one CTA per (N tile, K split) covering every token row
     const int mt = (M + kBM - 1) / kBM;
-    const bool can_defer = defer != nullptr && defer->partial != nullptr && !(epi & 16) &&
+    const bool can_defer = !g_batch_invariant && defer != nullptr && defer->partial != nullptr && !(epi & 16) &&
                            (base_epi == kEpiAdd || base_epi == kEpiRope || base_epi == kEpiLoraSelect);
     const int64_t defer_cap = can_defer ? defer->capacity : 0;
     WsChoice best;
@@ -1475,6 +1501,7 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
     static const int force_s = getenv("ALORA_WS_S") ? atoi(getenv("ALORA_WS_S")) : 0;
     if (force_bn > 0 && fits(force_bn) && mt * force_bn <= 512) best.bn = force_bn;
     if (force_s > 0 && (force_s == 1 || can_defer)) best.splits = force_s;
+    if (g_batch_invariant) best.splits = 1;  // one K range: the row's sum order never depends on the step
     if (best.bn > 0) {
       if (base_epi == kEpiRope && (lora->rope_cols % best.bn || best.bn % lora->head_dim)) return ALORA_EINVAL;
       CUtensorMap tb2, tu2 = tu;

@@ -14,6 +14,11 @@ void configure_kv_ops();
 void configure_attention();
 void configure_gemm();
 
+// Batch-invariant mode (AloraModelDesc.batch_invariant; set by the executor for the duration of a forward on
+// its thread): GEMMs use one kernel and one K range for every row, attention one kernel and one partition
+// per row, so a token's KV and logits do not depend on the step it was computed in.
+inline thread_local bool g_batch_invariant = false;
+
 enum Epi : int { kEpiStore = 0, kEpiAdd = 1, kEpiRelu = 2, kEpiSwiglu = 3, kEpiRope = 4, kEpiLoraSelect = 5 };
 
 // ---- fp32 storage / fp64 accumulation (parity tier), parity_f64.cu
@@ -85,6 +90,7 @@ struct GemmLora {
   int n_q = 0, n_kv = 0;               // select mode: column ranges of the q|k|v targets (planes 0 | 1 | 2)
   int planes = 0;                      // > 1: concat mode, every tile adds all planes (SwiGLU gate|up tiles)
   int s_planes = 3;                    // planes allocated in s
+  int s_rows = 0;                      // rows between planes of s (0 = M)
   const uint32_t* tile_slot_mask = nullptr;  // [ceil(M/128)] bitmask of slots present (taking the delta)
   int rank = 0;
   // kEpiRope: rotate-half RoPE in fp32 on the accumulator of columns < rope_cols (q and k heads), one rounding

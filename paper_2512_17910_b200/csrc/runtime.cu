@@ -299,8 +299,16 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const bool llama = d.arch == ALORA_ARCH_LLAMA;
   const bool lora = d.n_slots > 0;
   const int rk = d.lora_rank;
-  const bool seg_shrink = lora && s.lora_rows_max <= kSegMaxRows && d.d_model % 128 == 0 &&
-                          (rk == 8 || rk == 16 || rk == 32 || rk == 64);
+  // batch-invariant mode pins every per-row choice to the model, never to the step: the segmented shrink for
+  // any row count (else the per-row SIMT shrink), one GEMM kernel and K range, one attention partition
+  struct InvariantScope {
+    bool prev;
+    explicit InvariantScope(bool on) : prev(g_batch_invariant) { g_batch_invariant = on; }
+    ~InvariantScope() { g_batch_invariant = prev; }
+  } inv_scope(d.batch_invariant != 0);
+  const bool inv = d.batch_invariant != 0;
+  const bool seg_ok = lora && d.d_model % 128 == 0 && (rk == 8 || rk == 16 || rk == 32 || rk == 64);
+  const bool seg_shrink = seg_ok && (s.lora_rows_max <= kSegMaxRows || inv);
   const bool lora_o = lora && !mdl.lora_o_down.empty(), lora_in = lora && !mdl.lora_in_down.empty();
   const bool lora_out = lora && !mdl.lora_out_down.empty();
   const int in_planes = llama ? 2 : 1;
@@ -375,6 +383,10 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
           2.0 * 3 * d.n_slots * act * d.lora_rank * dm_,
           lora_shrink_seg_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
                                d.n_slots, d.lora_rank, d.slot_targets, sws, st));
+    } else if (lora && inv) {
+      RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
+          lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
+                           d.n_slots, d.lora_rank, d.slot_targets, sws, st));
     } else if (lora) {
       RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
           shrink(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]), d.n_slots,
@@ -411,7 +423,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
           kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                    d.block_size, st));
     }
-    if (s.attn_plan != nullptr) {  // shared-prefix plan: each group's prefix KV streamed once for all its rows
+    if (s.attn_plan != nullptr && !inv) {  // shared-prefix plan: each group's prefix KV streamed once for all its rows
       RUN("attention", s.attn_kv_tokens * 2.0 * Nkv * 2 + 2.0 * m_ * Nq_ * 2, 4.0 * H * D * s.attn_qk_pairs,
           attn_grouped(qkv, Nqkv, M, S, s.positions, s.row_seq, s.block_table, s.max_blocks, s.attn_plan,
                        s.attn_items, s.attn_segs, s.attn_sets, s.attn_max_parts, true,
@@ -429,6 +441,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       if (seg_shrink && lora_shrink_seg_fits(K))
         return lora_shrink_seg_bf16(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down),
                                     d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0);
+      if (inv)
+        return lora_shrink_bf16(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down),
+                                d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0);
       return shrink(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down), d.n_slots, rk,
                     d.slot_targets, sws, st, gw, part, w.part_bytes, &run.n, planes, tbit0);
     };

@@ -37,13 +37,13 @@ inline bool make_tmap_2d(CUtensorMap* m, const void* base, uint64_t rows, uint64
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 3-D bf16 tensor [d2, rows, cols] (contiguous planes), box [1, box_rows, box_cols].
+// 3-D bf16 tensor [d2, rows, cols], box [1, box_rows, box_cols]; planes are plane_rows (default rows) apart.
 inline bool make_tmap_3d(CUtensorMap* m, const void* base, uint64_t planes, uint64_t rows, uint64_t cols,
-                         uint32_t box_rows, uint32_t box_cols) {
+                         uint32_t box_rows, uint32_t box_cols, uint64_t plane_rows = 0) {
   EncodeTiledFn fn = encode_tiled_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {cols, rows, planes};
-  cuuint64_t strides[2] = {cols * 2, rows * cols * 2};
+  cuuint64_t strides[2] = {cols * 2, (plane_rows ? plane_rows : rows) * cols * 2};
   cuuint32_t box[3] = {box_cols, box_rows, 1};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, estr,

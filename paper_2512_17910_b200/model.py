@@ -119,7 +119,8 @@ class Model:
     GRAPH_BLOCK_BUCKET = 32  # decode steps pad the block table to a multiple of this many blocks
 
     def __init__(self, config: ModelConfig | None = None, weights: BaseWeights | None = None, init: str = "philox",
-                 max_tokens: int = 2048, max_seqs: int = 256, graphs: bool = True, shared_prefix: bool = True):
+                 max_tokens: int = 2048, max_seqs: int = 256, graphs: bool = True, shared_prefix: bool = True,
+                 batch_invariant: bool = False):
         torch = _native.require_cuda()
         self._torch = torch
         # decode steps (one row per span, bf16) replay a captured CUDA graph of the whole forward
@@ -128,7 +129,11 @@ class Model:
         # shared-prefix attention: spans holding the same leading blocks (adapters on one conversation) read
         # that prefix once (alora_plan_attention + the grouped kernel); ALORA_SHARED_PREFIX=0 disables it (A/B)
         import os
-        self._shared_prefix = (bool(shared_prefix) and c0.dtype == "bf16" and c0.head_dim in (64, 128)
+        # batch_invariant (bf16): a token's KV / logits are bitwise independent of the step that computed it
+        # (alora_sm100a.h AloraModelDesc.batch_invariant); the fp32 tier is invariant by construction
+        self.batch_invariant = bool(batch_invariant) and c0.dtype == "bf16"
+        self._shared_prefix = (bool(shared_prefix) and not self.batch_invariant and c0.dtype == "bf16"
+                               and c0.head_dim in (64, 128)
                                and os.environ.get("ALORA_SHARED_PREFIX", "1") != "0")
         self._attn_partial_cap = int(_native.lib.alora_attn_partial_capacity(c0.n_heads, c0.head_dim)) \
             if c0.dtype == "bf16" else 0
@@ -344,6 +349,7 @@ class Model:
         D.head_dim, D.ffn_dim, D.vocab, D.max_seq_len = cfg.head_dim, cfg.ffn, cfg.vocab_size, cfg.max_seq_len
         D.rms_eps, D.rope_theta = cfg.rms_eps, cfg.rope_theta
         D.max_tokens, D.max_seqs = self._ws_tokens, self._max_seqs
+        D.batch_invariant = int(self.batch_invariant)
         bank = self._bank
         D.n_slots = 0 if bank is None else bank["n"]
         D.lora_rank = 0 if bank is None else bank["rank"]

@@ -65,7 +65,8 @@ def pipeline_shape(spec: PipelineSpec):
 def build_engine(spec: PipelineSpec, model: ModelConfig | None = None, pool_blocks: int = 512, block_size: int = 4,
                  token_budget: int = 64, virtual_clock: bool = True, rank: int = 8,
                  max_batch_requests: int | None = None, prefix_caching: bool = True, chunked_prefill: bool = True,
-                 engine_model=None, pool_storage: str = "cuda", pipelined_decode: bool = False) -> Engine:
+                 engine_model=None, pool_storage: str = "cuda", pipelined_decode: bool = False,
+                 batch_invariant: bool = False) -> Engine:
     """One registered adapter per eval slot: adapter{k} with invocation_for(V, k) (bench.py:175-213)."""
     model = model or ModelConfig()
     _, _, n_eval = pipeline_shape(spec)
@@ -80,7 +81,7 @@ def build_engine(spec: PipelineSpec, model: ModelConfig | None = None, pool_bloc
                        comparison_mode=spec.mode, prefix_caching=prefix_caching)
     return Engine(cfg, clock=VirtualClock() if virtual_clock else WallClock(), model=engine_model,
                   pool_storage=pool_storage, max_tokens=max(token_budget, max_batch_requests),
-                  pipelined_decode=pipelined_decode)
+                  pipelined_decode=pipelined_decode, batch_invariant=batch_invariant)
 
 
 def _rid(prefix, idx, stage):
