@@ -483,7 +483,19 @@ __global__ void __launch_bounds__(kThreads, 1)
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   // LoRA extra K of a tile: the m tile's slot mask decides which K blocks are present
-  auto tile_of = [&](int t, int& m_tile, int& n0) { m_tile = t / n_n; n0 = (t % n_n) * BN; };
+  // Tile order: groups of up to kGroupM M tiles, M-fastest inside a group. The 148 CTAs in flight then cover
+  // ~148 / group N tiles with every M tile of the group, so each weight tile is fetched from HBM once and
+  // served to the group's CTAs from L2 (N-fastest order re-read the weights from HBM once per M tile: 5.8x
+  // the weight bytes for the C3 MLP-in GEMM at M = 1024, which made it HBM-bound); the group's activation
+  // rows (<= 2048 x K bf16) stay L2-resident across its N tiles.
+  constexpr int kGroupM = 16;
+  auto tile_of = [&](int t, int& m_tile, int& n0) {
+    const int gm = min(n_m, kGroupM);
+    const int g = t / (gm * n_n), r = t - g * gm * n_n;
+    const int gs = min(gm, n_m - g * gm);
+    m_tile = g * gm + r % gs;
+    n0 = (r / gs) * BN;
+  };
 
   // Producer and MMA loops run warp-converged with one elected lane per operation (see gemm_ws_kernel: a lone
   // lane looping while its siblings wait let ptxas clobber the MMA's uniform TMEM operand).
