@@ -68,7 +68,19 @@ __device__ __forceinline__ uint32_t smem_addr(const void* p) { return static_cas
 __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(valid ? 16 : 0));
 }
+__device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t x, uint32_t y, uint32_t z, uint32_t w) {
+  asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(x), "r"(y), "r"(z), "r"(w) : "memory");
+}
+// shared-window address form: no generic->shared conversion per copy
+__device__ __forceinline__ void cp_async16_s(uint32_t dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+// arrive on an mbarrier once every cp.async this thread issued so far has completed (no pending-count increment:
+// the barrier's expected count includes this arrival)
+__device__ __forceinline__ void cp_async_mbar_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
 
@@ -94,6 +106,44 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+// 2^x on the FMA pipe, for part of the softmax exponentials (the MUFU's 16 ex2 / clk / SM bound the softmax):
+// x = j + f, j = rint(x) through the 1.5 * 2^23 magic add, 2^f on [-0.5, 0.5] by a degree-3 near-minimax
+// polynomial (max rel error 1.0e-4, below bf16's half ulp of 2^-9), 2^j added into the exponent field.
+// x <= -127 (masked keys are -inf) gives +0, as ex2.approx.ftz does.
+__device__ __forceinline__ float poly_exp2(float x) {
+  const float xc = fmaxf(x, -127.f);
+  const float t = xc + 12582912.f;
+  const float f = xc - (t - 12582912.f);
+  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221098f), f, 0.6932829f), f, 1.f);
+  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+  return x > -127.f ? r : 0.f;
+}
+// pairs of scores per 32 whose exponentials run on poly_exp2 (every kPolyEvery-th pair; 0 = none)
+#ifndef ALORA_POLY_EVERY
+#define ALORA_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = ALORA_POLY_EVERY;
+
+// paired fp32 arithmetic (sm_100 FFMA2 / FADD2 on a 64-bit register pair)
+__device__ __forceinline__ uint64_t f2_pack(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
@@ -915,23 +965,39 @@ struct SegCursor {
 // serve tile X (TMEM lane quadrant = warp % 4).
 template <int PW, int MT>
 constexpr int kGrpThreads = (4 * MT + (PW > 0 ? PW : 1) + 1) * 32;
-// S buffers per tile: the TMEM (512 columns) holds MT O tiles of D columns plus MT x NB S buffers of 64
+// TMEM (512 columns; 256 for D=64 with one query tile, two CTAs per SM) per query tile x: O (D fp32 columns),
+// Q (D/2 columns of bf16 pairs: the A operand of S = Q K^T comes from TMEM, which keeps the smem for the K/V
+// ring) and NB S buffers of 64 columns
 template <int D, int MT>
-constexpr int kGrpNB = MT == 2 ? 2 : (D == 128 ? 4 : 3);
+constexpr int kGrpNB = MT == 2 ? (D == 128 ? 1 : 2) : (D == 128 ? 3 : 2);
 template <int D, int MT>
-constexpr int kGrpTmem = (MT * D + MT * kGrpNB<D, MT> * 64) <= 256 ? 256 : 512;
+constexpr int kGrpTmemUsed = MT * (D + D / 2 + kGrpNB<D, MT> * 64);
 template <int D, int MT>
-constexpr int kGrpNS = MT == 2 ? (D == 128 ? 5 : 8) : kNS<D>;  // K/V ring stages
+constexpr int kGrpTmem = kGrpTmemUsed<D, MT> <= 256 ? 256 : 512;
+// P buffers per query tile (bf16 [128 rows][64 keys] in smem, the A operand of O += P V)
+#ifndef ALORA_GRP_NP
+#define ALORA_GRP_NP 1
+#endif
+template <int D, int MT>
+constexpr int kGrpNP = (D == 64 && MT == 2) ? 2 : ALORA_GRP_NP;
+// K/V ring stages: what the 227 KB of smem leaves after the P buffers (D=64 with one query tile keeps two CTAs
+// per SM)
+template <int D, int MT>
+constexpr int kGrpNS = D == 128 ? (kGrpNP<D, MT> == 1 ? 6 : 5) : (MT == 2 ? 9 : 4);
 template <int D, int MT>
 struct SmemG {
-  static constexpr int kQBytes = MT * kQT * D * 2;
   static constexpr int kKVBytes = kKT * D * 2;
-  static constexpr int kQ = 0;
-  static constexpr int kK = kQ + kQBytes;
+  static constexpr int kPBytes = kQT * kKT * 2;
+  static constexpr int kP = 0;
+  static constexpr int kK = kP + MT * kGrpNP<D, MT> * kPBytes;
   static constexpr int kV = kK + kGrpNS<D, MT> * kKVBytes;
   static constexpr int kBar = kV + kGrpNS<D, MT> * kKVBytes;
   static constexpr int kTotal = kBar + 512 + 1024;
 };
+static_assert(SmemG<128, 2>::kTotal <= 232448 && SmemG<64, 2>::kTotal <= 232448 &&
+              SmemG<128, 1>::kTotal <= 232448 && 2 * SmemG<64, 1>::kTotal <= 232448, "attn_grp smem");
+static_assert(kGrpTmemUsed<128, 2> <= 512 && kGrpTmemUsed<64, 2> <= 512 && kGrpTmemUsed<128, 1> <= 512 &&
+              kGrpTmemUsed<64, 1> <= 256, "attn_grp tmem");
 
 template <int D, int PW, int MT>
 __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 : 1)
@@ -939,6 +1005,8 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   using L = SmemG<D, MT>;
   constexpr int NB = kGrpNB<D, MT>;
   constexpr int NS = kGrpNS<D, MT>;
+  constexpr int NP = kGrpNP<D, MT>;
+  static_assert(NS > NB, "the S look-ahead needs its K tiles in the ring");
   constexpr int kSoftWarps = 4 * MT;
   constexpr int kMmaWarp = kSoftWarps + (PW > 0 ? PW : 1);
   constexpr int kTmemCols = kGrpTmem<D, MT>;
@@ -947,10 +1015,12 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + L::kBar);
   uint64_t* kv_full = bars;
   uint64_t* kv_empty = kv_full + NS;
-  uint64_t* s_full = kv_empty + NS;     // [MT][NB]
-  uint64_t* p_full = s_full + MT * NB;  // [MT][NB]
-  uint64_t* s_free = p_full + MT * NB;  // [MT][NB]: PV of the P in that S buffer completed (one phase per use)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + MT * NB);
+  uint64_t* s_full = kv_empty + NS;     // [MT][NB] S MMA committed
+  uint64_t* s_free = s_full + MT * NB;  // [MT][NB] the softmax has read S into registers (one phase per use)
+  uint64_t* p_full = s_free + MT * NB;  // [MT][NP] P stored to smem (and proxy-fenced)
+  uint64_t* p_free = p_full + MT * NP;  // [MT][NP] the PV reading that P completed (one phase per use)
+  uint64_t* q_full = p_free + MT * NP;  // [MT] Q rows stored to TMEM
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + MT);
 
   const int* it = a.items + (int64_t)blockIdx.x * 8;
   const int set = it[0], mtile = it[1], seg_b = it[2], seg_e = it[3], p_index = it[4], cached = it[5];
@@ -963,18 +1033,23 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   for (int x = 0; x < MT; ++x) rows_t[x] = max(0, min(kQT, n_tok * G - (mtile * MT + x) * kQT));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) ATTN_TRACE(0);
-  constexpr int CH = D / 8;
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       sm100::mbar_init(&kv_full[i], PW > 0 ? 32 : 1);  // cp.async: every lane of the loading warp arrives
       sm100::mbar_init(&kv_empty[i], 1);
     }
-    for (int x = 0; x < MT; ++x)
+    for (int x = 0; x < MT; ++x) {
+      const int live_threads = 32 * max(1, (rows_t[x] + 31) / 32);
       for (int i = 0; i < NB; ++i) {
         sm100::mbar_init(&s_full[x * NB + i], 1);
-        sm100::mbar_init(&s_free[x * NB + i], 1);
-        sm100::mbar_init(&p_full[x * NB + i], 32 * max(1, (rows_t[x] + 31) / 32));
+        sm100::mbar_init(&s_free[x * NB + i], live_threads);
       }
+      for (int i = 0; i < NP; ++i) {
+        sm100::mbar_init(&p_full[x * NP + i], live_threads);
+        sm100::mbar_init(&p_free[x * NP + i], 1);
+      }
+      sm100::mbar_init(&q_full[x], live_threads);
+    }
     sm100::fence_barrier_init();
   }
   if (warp == kMmaWarp) sm100::tmem_alloc<kTmemCols>(tmem_slot);
@@ -982,9 +1057,10 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // O of tile x at x*D, then the S buffers: tile x buffer i at MT*D + (x*NB + i)*64
+  // O of tile x at x*D, its Q at MT*D + x*D/2, then the S buffers: tile x buffer i at MT*3D/2 + (x*NB + i)*64
   auto tOx = [&](int x) { return tmem + (uint32_t)(x * D); };
-  auto tSx = [&](int x, int i) { return tmem + (uint32_t)(MT * D + (x * NB + i) * 64); };
+  auto tQx = [&](int x) { return tmem + (uint32_t)(MT * D + x * (D / 2)); };
+  auto tSx = [&](int x, int i) { return tmem + (uint32_t)(MT * D + MT * (D / 2) + (x * NB + i) * 64); };
 
   if (PW > 0 && warp >= kSoftWarps && warp < kSoftWarps + PW) {
     // ------------------------------------------------------------------ cp.async producer warps
@@ -996,10 +1072,14 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     bool waited = false;
     const int kvw = a.Hkv * D;
     const int per_tile = kKT / a.B;
-    const int chunks_pp = a.B * 8;  // 16-byte chunks of one page row block (B rows x 64 dims)
-    int prev_st = -1;
+    const int r0 = lane >> 3, c0 = lane & 7;
+    const int64_t g_lane = ((int64_t)r0 * kvw + c0 * 8) * 2;  // bytes
+    const int64_t row4 = (int64_t)4 * kvw * 2, vstep = (int64_t)a.B * kvw * 2;
+    const uint32_t s_lane0 = (uint32_t)(r0 * 128 + ((c0 ^ r0) << 4));
+    const uint32_t s_lane1 = (uint32_t)((r0 + 4) * 128 + ((c0 ^ (r0 + 4)) << 4));
+    constexpr uint32_t kVOff = L::kV - L::kK;  // V stage st sits at a fixed distance from K stage st
     for (int t = 0; t < n_tiles; ++t, cur.next()) {
-      if (t % PW != pw) continue;
+      if (t % (PW > 0 ? PW : 1) != pw) continue;
       const int st = t % NS;
       const int k0 = cur.k0();
       if (!waited && !(k0 + kKT <= cached || (cur.filter < 0 && cur.hi <= cached))) {
@@ -1018,38 +1098,33 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         w0 = b0;
         win = bt[min(w0 + lane, last_blk)];
       }
-      uint8_t* dk = sm + L::kK + st * L::kKVBytes;
-      uint8_t* dv = sm + L::kV + st * L::kKVBytes;
+      // lane = (row r0 = lane / 8 of each 4-row group, 16-byte chunk c = lane % 8): every address below is a
+      // per-lane base plus a per-(page, row group) step, so the loop is a run of cp.async with few address ops
+      // (the generic per-chunk address arithmetic made this warp issue-bound at ~30 GB/s per SM)
+      const uint32_t sk = smem_addr(sm + L::kK + st * L::kKVBytes);
       for (int j = 0; j < per_tile; ++j) {
         const int idx = min(b0 + j, last_blk);  // past the end: a valid duplicate, masked by the softmax
         const int64_t blk = __shfl_sync(0xffffffffu, win, idx - w0);
-        const __nv_bfloat16* kp = a.kv + ((blk * a.n_layers + a.layer) * 2) * a.B * (int64_t)kvw + kvh * D;
-        const __nv_bfloat16* vp = kp + (int64_t)a.B * kvw;
+        const char* kp = reinterpret_cast<const char*>(
+                             a.kv + ((blk * a.n_layers + a.layer) * 2) * a.B * (int64_t)kvw + kvh * D) + g_lane;
+        const uint32_t sj = sk + (uint32_t)(j * a.B * 128);
+#pragma unroll 4
+        for (int i = 0; i < a.B / 4; ++i) {
+          const char* kg = kp + (int64_t)i * row4;
+          const uint32_t so = sj + (uint32_t)((i >> 1) * 1024) + ((i & 1) ? s_lane1 : s_lane0);
 #pragma unroll
-        for (int sub = 0; sub < D / 64; ++sub) {
-          for (int q = lane; q < chunks_pp; q += 32) {
-            const int rp = q >> 3, c = q & 7;
-            const int r = j * a.B + rp;
-            const uint32_t off = sw_off(r, sub * 8 + c, kKT);
-            cp_async16(dk + off, kp + (int64_t)rp * kvw + sub * 64 + c * 8, true);
-            cp_async16(dv + off, vp + (int64_t)rp * kvw + sub * 64 + c * 8, true);
+          for (int sub = 0; sub < D / 64; ++sub) {
+            cp_async16_s(so + sub * kKT * 128, kg + sub * 128);
+            cp_async16_s(so + sub * kKT * 128 + kVOff, kg + vstep + sub * 128);
           }
         }
       }
-      cp_async_commit();
-      // two tiles in flight per warp: publish the PREVIOUS one once its data landed (this one keeps loading)
-      if (prev_st >= 0) {
-        cp_async_wait<1>();
-        sm100::fence_proxy_async_smem();  // these generic-proxy writes are read by tcgen05.mma (async proxy)
-        sm100::mbar_arrive(&kv_full[prev_st]);
-      }
-      prev_st = st;
+      // each lane's arrive fires when its copies (and all its earlier ones) have landed, so the warp never
+      // blocks on its own loads: every free ring stage can be in flight. The MMA warp issues the proxy fence
+      // after its wait (generic-proxy smem writes read by tcgen05.mma).
+      cp_async_mbar_arrive_noinc(&kv_full[st]);
     }
-    if (prev_st >= 0) {
-      cp_async_wait<0>();
-      sm100::fence_proxy_async_smem();
-      sm100::mbar_arrive(&kv_full[prev_st]);
-    }
+    cp_async_wait<0>();
     if (!waited) pdl_wait();
   } else if (PW == 0 && warp == kSoftWarps) {
     // ------------------------------------------------------------------ TMA producer warp
@@ -1110,68 +1185,54 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     // ------------------------------------------------------------------ MMA issuer (static schedule)
     pdl_wait();  // q comes from the kernels before
     pdl_trigger();
-    // Q: the 32 lanes gather the MT x 128 GQA-packed rows of the set with cp.async into the swizzled layout
-    // (tile x at kQ + x * 128 rows)
-    for (int p = lane; p < MT * kQT; p += 32) {
-      const int x = p / kQT, pl = p % kQT;
-      const bool valid = pl < rows_t[x];
-      const int pr = (mtile * MT + x) * kQT + pl;
-      const int row = valid ? a.set_tok[tok_off + pr / G] : 0;
-      const __nv_bfloat16* src = a.q + (int64_t)row * a.ld_q + (kvh * G + (valid ? pr % G : 0)) * D;
-      uint8_t* qx = sm + L::kQ + x * kQT * D * 2;
-#pragma unroll
-      for (int c = 0; c < CH; ++c) cp_async16(qx + sw_off(pl, c, kQT), valid ? src + c * 8 : a.q, valid);
-    }
-    cp_async_commit();
-    cp_async_wait<0>();
-    sm100::fence_proxy_async_smem();
-    __syncwarp();
     constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
     constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
     if (lane == 0) ATTN_TRACE(1);
     sm100::tc_fence_after();
-    // S of tile ts for query tile x; its buffer was last read (P) by PV_x(ts - NB), which must have COMPLETED
+    // S of tile ts for query tile x (A = Q from TMEM), into the buffer the softmax of tile ts - NB has read
     auto issue_s = [&](int ts) {
       const int st = ts % NS;
       sm100::mbar_wait(&kv_full[st], (ts / NS) & 1);
+      if (PW > 0) sm100::fence_proxy_async_smem();  // cp.async (generic proxy) data -> tcgen05.mma operands
 #pragma unroll
       for (int x = 0; x < MT; ++x) {
         if (rows_t[x] == 0) continue;
+        if (ts == 0) sm100::mbar_wait(&q_full[x], 0);
         if (ts >= NB) sm100::mbar_wait(&s_free[x * NB + ts % NB], ((ts / NB) - 1) & 1);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
-          const uint8_t* qb = sm + L::kQ + x * kQT * D * 2;
           const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
 #pragma unroll
           for (int ks = 0; ks < D / 16; ++ks) {
-            const uint64_t da = sm100::umma_desc_sw128(qb + (ks >> 2) * kQT * 128 + (ks & 3) * 32);
             const uint64_t db = sm100::umma_desc_sw128(kb + (ks >> 2) * kKT * 128 + (ks & 3) * 32);
-            if (!(a.exp & 64)) sm100::mma_bf16_ss(tSx(x, ts % NB), da, db, idesc_s, ks > 0 ? 1u : 0u);
+            if (!(a.exp & 64)) sm100::mma_bf16_ts(tSx(x, ts % NB), tQx(x) + ks * 8, db, idesc_s, ks > 0 ? 1u : 0u);
           }
           sm100::mma_commit(&s_full[x * NB + ts % NB]);
         }
         __syncwarp();
       }
     };
-    // S runs NB-1 tiles ahead: S_{tp+NB-1} is issued at the top of iteration tp (its buffer was freed by
-    // PV_{tp-1}, issued one iteration earlier), then the PVs of tile tp as each query tile's P lands
-    for (int ts = 0; ts < min(n_tiles, NB - 1); ++ts) issue_s(ts);
+    // S runs NB tiles ahead of the PVs: S_{tp+NB} reuses the buffer the softmax released as soon as it had read
+    // S_tp into registers (P goes to smem, not back into TMEM), so it is issued before PV_tp waits for P_tp and
+    // the tensor pipe always holds the next tiles' S while the softmax works
+    for (int ts = 0; ts < min(n_tiles, NB); ++ts) issue_s(ts);
     for (int tp = 0; tp < n_tiles; ++tp) {
-      if (tp + NB - 1 < n_tiles) issue_s(tp + NB - 1);
+      if (tp + NB < n_tiles) issue_s(tp + NB);
 #pragma unroll
       for (int x = 0; x < MT; ++x) {
         if (rows_t[x] == 0) continue;
-        sm100::mbar_wait(&p_full[x * NB + tp % NB], (tp / NB) & 1);
+        sm100::mbar_wait(&p_full[x * NP + tp % NP], (tp / NP) & 1);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
-          const uint32_t tp_a = tSx(x, tp % NB);
+          const uint8_t* pb = sm + L::kP + (x * NP + tp % NP) * L::kPBytes;
           const uint8_t* vb = sm + L::kV + (tp % NS) * L::kKVBytes;
 #pragma unroll
           for (int kk = 0; kk < kKT / 16; ++kk) {
+            const uint64_t da = sm100::umma_desc_sw128(pb + kk * 32);
             const uint64_t db = sm100::umma_desc_sw128_mn(vb + kk * 16 * 128, kKT * 128);
-            if (!(a.exp & 64)) sm100::mma_bf16_ts(tOx(x), tp_a + kk * 8, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
+            if (!(a.exp & 64)) sm100::mma_bf16_ss(tOx(x), da, db, idesc_o, (tp > 0 || kk > 0) ? 1u : 0u);
           }
-          sm100::mma_commit(&s_free[x * NB + tp % NB]);
+          sm100::mma_commit(&p_free[x * NP + tp % NP]);
         }
         __syncwarp();
       }
@@ -1191,12 +1252,29 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     const int span = live ? a.row_seq[row] : -2;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
     uint64_t* s_full_x = s_full + xt * NB;
-    uint64_t* p_full_x = p_full + xt * NB;
     uint64_t* s_free_x = s_free + xt * NB;
-    uint32_t tS[NB];
-#pragma unroll
-    for (int i = 0; i < NB; ++i) tS[i] = tSx(xt, i);
+    uint64_t* p_full_x = p_full + xt * NP;
+    uint64_t* p_free_x = p_free + xt * NP;
+    const uint32_t tS0 = tSx(xt, 0) + lane_base;  // S buffer i at tS0 + 64 i
     const uint32_t tO = tOx(xt);
+    // this thread's P row (K-major SW128: 16-byte chunk c of row r at chunk c ^ (r & 7))
+    const uint32_t p_row = smem_addr(sm + L::kP + xt * NP * L::kPBytes) + (uint32_t)(r * 128);
+    {  // this row's Q (D bf16 = D/2 columns of pairs, the layout of a TMEM A operand) into TMEM lane r
+      const uint4* src = reinterpret_cast<const uint4*>(a.q + (int64_t)row * a.ld_q + head * D);
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 32) {
+        uint32_t qv[32];
+#pragma unroll
+        for (int v = 0; v < 8; ++v) {
+          const uint4 w = live ? __ldg(src + c / 4 + v) : make_uint4(0u, 0u, 0u, 0u);
+          qv[4 * v] = w.x; qv[4 * v + 1] = w.y; qv[4 * v + 2] = w.z; qv[4 * v + 3] = w.w;
+        }
+        sm100::tmem_st_32x32b_x32(tQx(xt) + lane_base + c, qv);
+      }
+      sm100::tmem_st_wait();
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&q_full[xt]);
+    }
     const float sc = a.scale_log2;
     const float thr = kRescaleLog2 / sc;
     float m_run = -INFINITY, l_run = 0.f;
@@ -1213,22 +1291,25 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       sm100::mbar_wait(&s_full_x[t % NB], (t / NB) & 1);
       sm100::tc_fence_after();
       if (t == 0 && tid == 0) ATTN_TRACE(2);
-      if (a.exp & 16) {  // timing experiment: no softmax work at all
-        sm100::tc_fence_before();
-        sm100::mbar_arrive(&p_full_x[t % NB]);
-        continue;
-      }
       float sv[kKT];
       {
         uint32_t r0[32], r1[32];
-        sm100::tmem_ld_32x32b_x32(tS[t % NB] + lane_base, r0);
-        sm100::tmem_ld_32x32b_x32(tS[t % NB] + lane_base + 32, r1);
+        const uint32_t ts = tS0 + (uint32_t)((t % NB) * 64);
+        sm100::tmem_ld_32x32b_x32(ts, r0);
+        sm100::tmem_ld_32x32b_x32(ts + 32, r1);
         sm100::tmem_ld_wait();
 #pragma unroll
         for (int j = 0; j < 32; ++j) {
           sv[j] = __uint_as_float(r0[j]);
           sv[j + 32] = __uint_as_float(r1[j]);
         }
+      }
+      sm100::tc_fence_before();
+      sm100::mbar_arrive(&s_free_x[t % NB]);  // S_{t+NB} may overwrite the buffer
+      if (a.exp & 16) {  // timing experiment: no softmax work at all
+        if (t >= NP) sm100::mbar_wait(&p_free_x[t % NP], ((t / NP) - 1) & 1);
+        sm100::mbar_arrive(&p_full_x[t % NP]);
+        continue;
       }
       if (__any_sync(0xffffffffu, k0 + kKT - 1 > lim)) {
 #pragma unroll
@@ -1248,7 +1329,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
       if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
         const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
-        sm100::mbar_wait(&s_free_x[(t - 1) % NB], ((t - 1) / NB) & 1);  // O holds PV_{t-1}
+        sm100::mbar_wait(&p_free_x[(t - 1) % NP], ((t - 1) / NP) & 1);  // O holds PV_{t-1}
         sm100::tc_fence_after();
 #pragma unroll
         for (int c = 0; c < D; c += 32) {
@@ -1264,26 +1345,39 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       }
       if (grow) m_run = m_new;
       const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
-      float rs4[4] = {0.f, 0.f, 0.f, 0.f};
+      // paired fp32 (FFMA2 / FADD2): half the FMA-pipe instructions of the scale and the row sum
+      const uint64_t sc2 = f2_pack(sc, sc), nb2 = f2_pack(nb, nb);
+      uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
+      uint32_t pk[32];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float p0 = fast_exp2(fmaf(sv[h * 32 + 2 * j], sc, nb));
-          const float p1 = (a.exp & 128) ? p0 : fast_exp2(fmaf(sv[h * 32 + 2 * j + 1], sc, nb));
-          rs4[j & 3] += p0 + p1;
-          pk[j] = pack_bf16(p0, p1);
-        }
-        if (!(a.exp & 256)) sm100::tmem_st_32x32b_x16(tS[t % NB] + lane_base + h * 16, pk);
+      for (int j = 0; j < 32; ++j) {
+        float x0, x1;
+        f2_unpack(ffma2(f2_pack(sv[2 * j], sv[2 * j + 1]), sc2, nb2), x0, x1);
+        // every kPolyEvery-th pair on the FMA pipe (A/B; the MUFU runs 16 ex2 / clk / SM)
+        const bool poly = kPolyEvery > 0 && (j % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1;
+        const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
+        const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+        acc2[j & 3] = fadd2(acc2[j & 3], f2_pack(p0, p1));
+        pk[j] = pack_bf16(p0, p1);
       }
-      sm100::tmem_st_wait();
-      l_run += (rs4[0] + rs4[1]) + (rs4[2] + rs4[3]);
-      sm100::tc_fence_before();
-      sm100::mbar_arrive(&p_full_x[t % NB]);
+      {
+        const uint64_t s2 = fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3]));
+        float l0, l1;
+        f2_unpack(s2, l0, l1);
+        l_run += l0 + l1;
+      }
+      if (t >= NP) sm100::mbar_wait(&p_free_x[t % NP], ((t / NP) - 1) & 1);  // PV_{t-NP} read this buffer
+      {
+        const uint32_t pb = p_row + (uint32_t)((t % NP) * L::kPBytes);
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          st_shared_v4(pb + (uint32_t)((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      sm100::fence_proxy_async_smem();  // generic-proxy P stores -> tcgen05.mma operand reads
+      sm100::mbar_arrive(&p_full_x[t % NP]);
     }
     if (tid == 0) ATTN_TRACE(3);
-    sm100::mbar_wait(&s_free_x[(n_tiles - 1) % NB], ((n_tiles - 1) / NB) & 1);
+    sm100::mbar_wait(&p_free_x[(n_tiles - 1) % NP], ((n_tiles - 1) / NP) & 1);  // O holds the last PV
     sm100::tc_fence_after();
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
@@ -1372,8 +1466,9 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
   // cp.async producer warps: 2 with two query tiles per CTA, 4 with one at D=128; D=64 with one query tile runs
   // two CTAs per SM (register bound) with the TMA producer. ALORA_ATTN_TMA=1 forces the TMA producer (A/B).
   static const bool force_tma = getenv("ALORA_ATTN_TMA") != nullptr;
-  constexpr int PW = MT == 2 ? 2 : (D == 128 ? 4 : 0);
-  const bool use_pw = PW > 0 && !force_tma && a.B >= 4;
+  // cp.async producer warps with two query tiles per CTA; one query tile (A/B only) uses the TMA producer
+  constexpr int PW = MT == 2 ? 2 : 0;
+  const bool use_pw = PW > 0 && !force_tma && a.B % 8 == 0;  // producer lanes assume 8-row swizzle groups per page
   auto kern = use_pw ? tc::attn_grp_kernel<D, PW, MT> : tc::attn_grp_kernel<D, 0, MT>;
   const int threads = use_pw ? tc::kGrpThreads<PW, MT> : tc::kGrpThreads<0, MT>;
   static bool configured = false;
