@@ -106,23 +106,6 @@ __device__ __forceinline__ float fast_exp2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe, for part of the softmax exponentials (the MUFU's 16 ex2 / clk / SM bound the softmax):
-// x = j + f, j = rint(x) through the 1.5 * 2^23 magic add, 2^f on [-0.5, 0.5] by a degree-3 near-minimax
-// polynomial (max rel error 1.0e-4, below bf16's half ulp of 2^-9), 2^j added into the exponent field.
-// x <= -127 (masked keys are -inf) gives +0, as ex2.approx.ftz does.
-__device__ __forceinline__ float poly_exp2(float x) {
-  const float xc = fmaxf(x, -127.f);
-  const float t = xc + 12582912.f;
-  const float f = xc - (t - 12582912.f);
-  const float p = fmaf(fmaf(fmaf(0.05500893f, f, 0.24221098f), f, 0.6932829f), f, 1.f);
-  const float r = __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-  return x > -127.f ? r : 0.f;
-}
-// pairs of scores per 32 whose exponentials run on poly_exp2 (every kPolyEvery-th pair; 0 = none)
-#ifndef ALORA_POLY_EVERY
-#define ALORA_POLY_EVERY 0
-#endif
-constexpr int kPolyEvery = ALORA_POLY_EVERY;
 
 // paired fp32 arithmetic (sm_100 FFMA2 / FADD2 on a 64-bit register pair)
 __device__ __forceinline__ uint64_t f2_pack(float a, float b) {
@@ -920,6 +903,7 @@ struct GrpArgs {
   int M;
   unsigned long long* trace;
   int exp;
+  long long* tl;  // ALORA_ATTN_TL=1: clock64 timeline of CTA (0, 0): [4 events][2 query tiles][256 tiles]
 };
 
 // walks an item's segments tile by tile (64 keys per tile)
@@ -955,16 +939,19 @@ struct SegCursor {
 };
 
 // Producer: PW = 0 -> one warp issuing TMA page boxes [B keys x 64 dims]; PW > 0 -> PW warps loading whole
-// tiles with cp.async (16-byte chunks written straight into the SW128 layout), warp w owning tiles w, w+PW, ...
-// and publishing each after its own data landed (wait_group 0 + proxy fence + arrive). Per-box TMA processing
-// (~70 ns per 2 KB page box under ncu) capped a CTA's K/V supply at ~30 GB/s; PW warps of cp.async keep PW
-// tiles in flight at the LSU's issue rate.
+// tiles with cp.async (16-byte chunks written straight into the SW128 layout from per-lane precomputed offsets),
+// warp w owning tiles w, w+PW, ..., each lane arriving on the tile's barrier when its copies land
+// (cp.async.mbarrier.arrive), so every free ring stage is in flight. Per-box TMA processing (~70 ns per 2 KB page
+// box) capped a CTA's K/V supply at ~30 GB/s; the first cp.async version (generic per-chunk address arithmetic,
+// wait_group publishing) was issue-bound at about the same rate.
 // MT = M-tiles per CTA. With MT = 2 (the default) a CTA runs two 128-row query tiles of a set against every
-// K/V tile it loads: a CTA's K/V ingest (~45 GB/s per SM, the same whether L2 hit or not) is what bounded the
-// one-tile kernel, so sharing each loaded tile between 256 rows halves the per-row cost. Softmax warps 4X..4X+3
-// serve tile X (TMEM lane quadrant = warp % 4).
+// K/V tile it loads, halving the per-row K/V ingest. Softmax warps 4X..4X+3 serve tile X (TMEM lane quadrant =
+// warp % 4). Q sits in TMEM (the A operand of S = Q K^T), P goes to smem (the A operand of O += P V), so an S
+// buffer is free again as soon as the softmax has read it: S_{t+NB} does not wait for PV_t, and two issuer warps
+// (S and PV) keep either MMA from queueing behind the other's wait.
+// Warps: 4 x MT softmax, PW producers, the S-MMA issuer, the PV-MMA issuer.
 template <int PW, int MT>
-constexpr int kGrpThreads = (4 * MT + (PW > 0 ? PW : 1) + 1) * 32;
+constexpr int kGrpThreads = (4 * MT + (PW > 0 ? PW : 1) + 2) * 32;
 // TMEM (512 columns; 256 for D=64 with one query tile, two CTAs per SM) per query tile x: O (D fp32 columns),
 // Q (D/2 columns of bf16 pairs: the A operand of S = Q K^T comes from TMEM, which keeps the smem for the K/V
 // ring) and NB S buffers of 64 columns
@@ -974,12 +961,10 @@ template <int D, int MT>
 constexpr int kGrpTmemUsed = MT * (D + D / 2 + kGrpNB<D, MT> * 64);
 template <int D, int MT>
 constexpr int kGrpTmem = kGrpTmemUsed<D, MT> <= 256 ? 256 : 512;
-// P buffers per query tile (bf16 [128 rows][64 keys] in smem, the A operand of O += P V)
-#ifndef ALORA_GRP_NP
-#define ALORA_GRP_NP 1
-#endif
+// P buffers per query tile (bf16 [128 rows][64 keys] in smem, the A operand of O += P V); at D=128 one buffer
+// (the softmax of tile t+1 rarely waits for PV_t) buys the sixth K/V stage
 template <int D, int MT>
-constexpr int kGrpNP = (D == 64 && MT == 2) ? 2 : ALORA_GRP_NP;
+constexpr int kGrpNP = (D == 64 && MT == 2) ? 2 : 1;
 // K/V ring stages: what the 227 KB of smem leaves after the P buffers (D=64 with one query tile keeps two CTAs
 // per SM)
 template <int D, int MT>
@@ -1008,7 +993,8 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   constexpr int NP = kGrpNP<D, MT>;
   static_assert(NS > NB, "the S look-ahead needs its K tiles in the ring");
   constexpr int kSoftWarps = 4 * MT;
-  constexpr int kMmaWarp = kSoftWarps + (PW > 0 ? PW : 1);
+  constexpr int kMmaWarp = kSoftWarps + (PW > 0 ? PW : 1);  // S = Q K^T issuer (and TMEM owner)
+  constexpr int kPvWarp = kMmaWarp + 1;                       // O += P V issuer
   constexpr int kTmemCols = kGrpTmem<D, MT>;
   extern __shared__ uint8_t smem_raw_grp[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw_grp) + 1023) & ~uintptr_t(1023));
@@ -1033,6 +1019,9 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   for (int x = 0; x < MT; ++x) rows_t[x] = max(0, min(kQT, n_tok * G - (mtile * MT + x) * kQT));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) ATTN_TRACE(0);
+  long long* tl = (a.tl && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) ? a.tl : nullptr;
+#define GRP_TL(ev, x, t) \
+  if (tl && (t) < 256) tl[((ev) * 2 + (x)) * 256 + (t)] = clock64()
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) {
       sm100::mbar_init(&kv_full[i], PW > 0 ? 32 : 1);  // cp.async: every lane of the loading warp arrives
@@ -1182,11 +1171,12 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       cur.next();
     }
   } else if (warp == kMmaWarp) {
-    // ------------------------------------------------------------------ MMA issuer (static schedule)
-    pdl_wait();  // q comes from the kernels before
+    // ------------------------------------------------------------------ S-MMA issuer
+    // Two issuer warps: S_{t+NB} needs only the softmax's read of S_t and the K tile, PV_t only P_t, so neither
+    // waits behind the other (one in-order issuer left the PV ~800 cycles behind its P and S_{t+1} behind it)
+    pdl_wait();
     pdl_trigger();
     constexpr uint32_t idesc_s = sm100::idesc_bf16_f32(kQT, kKT);
-    constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
     if (lane == 0) ATTN_TRACE(1);
     sm100::tc_fence_after();
     // S of tile ts for query tile x (A = Q from TMEM), into the buffer the softmax of tile ts - NB has read
@@ -1200,6 +1190,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         if (ts == 0) sm100::mbar_wait(&q_full[x], 0);
         if (ts >= NB) sm100::mbar_wait(&s_free[x * NB + ts % NB], ((ts / NB) - 1) & 1);
         sm100::tc_fence_after();
+        GRP_TL(2, x, ts);
         if (sm100::elect_one()) {
           const uint8_t* kb = sm + L::kK + st * L::kKVBytes;
 #pragma unroll
@@ -1212,17 +1203,20 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         __syncwarp();
       }
     };
-    // S runs NB tiles ahead of the PVs: S_{tp+NB} reuses the buffer the softmax released as soon as it had read
-    // S_tp into registers (P goes to smem, not back into TMEM), so it is issued before PV_tp waits for P_tp and
-    // the tensor pipe always holds the next tiles' S while the softmax works
-    for (int ts = 0; ts < min(n_tiles, NB); ++ts) issue_s(ts);
+    // S_{ts} reuses the buffer the softmax released as soon as it had read S_{ts-NB} into registers (P goes to
+    // smem, not back into TMEM)
+    for (int ts = 0; ts < n_tiles; ++ts) issue_s(ts);
+  } else if (warp == kPvWarp) {
+    // ------------------------------------------------------------------ PV-MMA issuer
+    constexpr uint32_t idesc_o = sm100::idesc_bf16_f32_bmn(kQT, D);
+    sm100::tc_fence_after();
     for (int tp = 0; tp < n_tiles; ++tp) {
-      if (tp + NB < n_tiles) issue_s(tp + NB);
 #pragma unroll
       for (int x = 0; x < MT; ++x) {
         if (rows_t[x] == 0) continue;
         sm100::mbar_wait(&p_full[x * NP + tp % NP], (tp / NP) & 1);
         sm100::tc_fence_after();
+        GRP_TL(3, x, tp);
         if (sm100::elect_one()) {
           const uint8_t* pb = sm + L::kP + (x * NP + tp % NP) * L::kPBytes;
           const uint8_t* vb = sm + L::kV + (tp % NS) * L::kKVBytes;
@@ -1236,7 +1230,8 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         }
         __syncwarp();
       }
-      if (sm100::elect_one()) sm100::mma_commit(&kv_empty[tp % NS]);  // every PV of tile tp read its V
+      // every PV of tile tp read its V; S_tp (issued by the other warp) completed before the softmax published P_tp
+      if (sm100::elect_one()) sm100::mma_commit(&kv_empty[tp % NS]);
       __syncwarp();
     }
   } else if (warp < kSoftWarps && (warp & 3) < (rows_t[warp >> 2] + 31) / 32) {
@@ -1251,10 +1246,9 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     const int pos = live ? a.positions[row] : -1;
     const int span = live ? a.row_seq[row] : -2;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    uint64_t* s_full_x = s_full + xt * NB;
-    uint64_t* s_free_x = s_free + xt * NB;
-    uint64_t* p_full_x = p_full + xt * NP;
-    uint64_t* p_free_x = p_free + xt * NP;
+    // this tile's barriers as 32-bit shared addresses (buffer i at + 8 i)
+    const uint32_t s_full_x = smem_addr(s_full + xt * NB), s_free_x = smem_addr(s_free + xt * NB);
+    const uint32_t p_full_x = smem_addr(p_full + xt * NP), p_free_x = smem_addr(p_free + xt * NP);
     const uint32_t tS0 = tSx(xt, 0) + lane_base;  // S buffer i at tS0 + 64 i
     const uint32_t tO = tOx(xt);
     // this thread's P row (K-major SW128: 16-byte chunk c of row r at chunk c ^ (r & 7))
@@ -1288,29 +1282,23 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       }
       const int k0 = cur.k0();
       cur.next();
-      sm100::mbar_wait(&s_full_x[t % NB], (t / NB) & 1);
+      sm100::mbar_wait_a(s_full_x + 8 * (t % NB), (t / NB) & 1);
       sm100::tc_fence_after();
-      if (t == 0 && tid == 0) ATTN_TRACE(2);
+      if ((warp & 3) == 0) GRP_TL(0, xt, t);
       float sv[kKT];
       {
-        uint32_t r0[32], r1[32];
         const uint32_t ts = tS0 + (uint32_t)((t % NB) * 64);
-        sm100::tmem_ld_32x32b_x32(ts, r0);
-        sm100::tmem_ld_32x32b_x32(ts + 32, r1);
-        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          sv[j] = __uint_as_float(r0[j]);
-          sv[j + 32] = __uint_as_float(r1[j]);
+        for (int c = 0; c < kKT; c += 32) {
+          uint32_t rv[32];
+          sm100::tmem_ld_32x32b_x32(ts + c, rv);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sv[c + j] = __uint_as_float(rv[j]);
         }
       }
       sm100::tc_fence_before();
-      sm100::mbar_arrive(&s_free_x[t % NB]);  // S_{t+NB} may overwrite the buffer
-      if (a.exp & 16) {  // timing experiment: no softmax work at all
-        if (t >= NP) sm100::mbar_wait(&p_free_x[t % NP], ((t / NP) - 1) & 1);
-        sm100::mbar_arrive(&p_full_x[t % NP]);
-        continue;
-      }
+      sm100::mbar_arrive_a(s_free_x + 8 * (t % NB));  // S_{t+NB} may overwrite the buffer
       if (__any_sync(0xffffffffu, k0 + kKT - 1 > lim)) {
 #pragma unroll
         for (int j = 0; j < kKT; ++j)
@@ -1329,16 +1317,16 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
       if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
         const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
-        sm100::mbar_wait(&p_free_x[(t - 1) % NP], ((t - 1) / NP) & 1);  // O holds PV_{t-1}
+        sm100::mbar_wait_a(p_free_x + 8 * ((t - 1) % NP), ((t - 1) / NP) & 1);  // O holds PV_{t-1}
         sm100::tc_fence_after();
-#pragma unroll
-        for (int c = 0; c < D; c += 32) {
-          uint32_t ov[32];
-          sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+#pragma unroll 1
+        for (int c = 0; c < D; c += 16) {  // 16 columns at a time: the scores stay in registers
+          uint32_t ov[16];
+          sm100::tmem_ld_32x32b_x16(tO + lane_base + c, ov);
           sm100::tmem_ld_wait();
 #pragma unroll
-          for (int j = 0; j < 32; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
-          sm100::tmem_st_32x32b_x32(tO + lane_base + c, ov);
+          for (int j = 0; j < 16; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
+          sm100::tmem_st_32x32b_x16(tO + lane_base + c, ov);
         }
         sm100::tmem_st_wait();
         l_run *= corr;
@@ -1348,15 +1336,12 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       // paired fp32 (FFMA2 / FADD2): half the FMA-pipe instructions of the scale and the row sum
       const uint64_t sc2 = f2_pack(sc, sc), nb2 = f2_pack(nb, nb);
       uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
-      uint32_t pk[32];
+      uint32_t pk[kKT / 2];
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
+      for (int j = 0; j < kKT / 2; ++j) {
         float x0, x1;
         f2_unpack(ffma2(f2_pack(sv[2 * j], sv[2 * j + 1]), sc2, nb2), x0, x1);
-        // every kPolyEvery-th pair on the FMA pipe (A/B; the MUFU runs 16 ex2 / clk / SM)
-        const bool poly = kPolyEvery > 0 && (j % (kPolyEvery > 0 ? kPolyEvery : 1)) == kPolyEvery - 1;
-        const float p0 = poly ? poly_exp2(x0) : fast_exp2(x0);
-        const float p1 = poly ? poly_exp2(x1) : fast_exp2(x1);
+        const float p0 = fast_exp2(x0), p1 = fast_exp2(x1);
         acc2[j & 3] = fadd2(acc2[j & 3], f2_pack(p0, p1));
         pk[j] = pack_bf16(p0, p1);
       }
@@ -1366,7 +1351,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         f2_unpack(s2, l0, l1);
         l_run += l0 + l1;
       }
-      if (t >= NP) sm100::mbar_wait(&p_free_x[t % NP], ((t / NP) - 1) & 1);  // PV_{t-NP} read this buffer
+      if (t >= NP) sm100::mbar_wait_a(p_free_x + 8 * (t % NP), ((t / NP) - 1) & 1);  // PV_{t-NP} read this buffer
       {
         const uint32_t pb = p_row + (uint32_t)((t % NP) * L::kPBytes);
 #pragma unroll
@@ -1374,10 +1359,11 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
           st_shared_v4(pb + (uint32_t)((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
       sm100::fence_proxy_async_smem();  // generic-proxy P stores -> tcgen05.mma operand reads
-      sm100::mbar_arrive(&p_full_x[t % NP]);
+      sm100::mbar_arrive_a(p_full_x + 8 * (t % NP));
+      if ((warp & 3) == 0) GRP_TL(1, xt, t);
     }
     if (tid == 0) ATTN_TRACE(3);
-    sm100::mbar_wait(&p_free_x[(n_tiles - 1) % NP], ((n_tiles - 1) / NP) & 1);  // O holds the last PV
+    sm100::mbar_wait_a(p_free_x + 8 * ((n_tiles - 1) % NP), ((n_tiles - 1) / NP) & 1);  // O holds the last PV
     sm100::tc_fence_after();
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
@@ -1386,8 +1372,9 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
       sm100::tmem_ld_wait();
       if (!live) continue;
+      const int oc = c;  // O column
       if (p_index < 0) {
-        __nv_bfloat16* dst = a.out + (int64_t)row * a.ld_out + head * D + c;
+        __nv_bfloat16* dst = a.out + (int64_t)row * a.ld_out + head * D + oc;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           __align__(16) __nv_bfloat162 o2[4];
@@ -1399,13 +1386,13 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         }
       } else {
         const int64_t slot = ((int64_t)p_index * a.M + row) * a.H + head;
-        float* dst = a.ws_o + slot * D + c;
+        float* dst = a.ws_o + slot * D + oc;
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           __stcg(reinterpret_cast<float4*>(dst + q * 4),
                  make_float4(__uint_as_float(ov[q * 4]), __uint_as_float(ov[q * 4 + 1]),
                              __uint_as_float(ov[q * 4 + 2]), __uint_as_float(ov[q * 4 + 3])));
-        if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run * sc, l_run));
+        if (oc == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run * sc, l_run));
       }
     }
   }
@@ -1481,6 +1468,13 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
     configured = true;
   }
   tc::GrpArgs ta = a;
+  static const bool timeline = getenv("ALORA_ATTN_TL") != nullptr;
+  static long long* tlbuf = nullptr;
+  if (timeline) {
+    if (!tlbuf) cudaMalloc(&tlbuf, sizeof(long long) * 4 * 2 * 256);
+    cudaMemsetAsync(tlbuf, 0, sizeof(long long) * 4 * 2 * 256, st);
+    ta.tl = tlbuf;
+  }
   static const bool tracing = getenv("ALORA_ATTN_TRACE") != nullptr;
   static unsigned long long* tbuf = nullptr;
   const dim3 grid(n_items, a.Hkv);
@@ -1512,6 +1506,28 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
       fprintf(stderr, "[attn grp trace] ctas %d/%d span %.2f us (longest CTA %.2f); mean start->Q %.2f, Q->S0 %.2f, "
               "S0->last P %.2f, ->end %.2f us\n", live, n_ctas, (t1 - t0) / 1e3, longest / 1e3, ph[0] / live / 1e3,
               ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3);
+  }
+  if (timeline) {  // per-tile means over CTA (0, 0), SM cycles
+    std::vector<long long> h(4 * 2 * 256);
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h.data(), tlbuf, h.size() * 8, cudaMemcpyDeviceToHost);
+    auto at = [&](int ev, int x, int t) { return h[(ev * 2 + x) * 256 + t]; };
+    for (int x = 0; x < MT; ++x) {
+      double soft = 0, wait_s = 0, s_lat = 0, pv_lag = 0;
+      int n = 0;
+      for (int t = 2; t < 250; ++t) {
+        if (!at(0, x, t) || !at(1, x, t) || !at(2, x, t) || !at(3, x, t) || !at(1, x, t - 1)) break;
+        soft += at(1, x, t) - at(0, x, t);        // softmax: S in hand -> P published
+        wait_s += at(0, x, t) - at(1, x, t - 1);  // softmax idle before S_t
+        s_lat += at(0, x, t) - at(2, x, t);       // S_t issued -> softmax has it
+        pv_lag += at(3, x, t) - at(1, x, t);      // P_t published -> PV_t issued
+        ++n;
+      }
+      if (n)
+        fprintf(stderr, "[attn grp timeline] tile %d: %d tiles, per tile (cycles): softmax %.0f, softmax idle %.0f, "
+                "S issue->softmax %.0f, P->PV issue %.0f, period %.0f\n", x, n, soft / n, wait_s / n, s_lat / n,
+                pv_lag / n, double(at(1, x, n + 1) - at(1, x, 1)) / n);
+    }
   }
   if (merge) {
     ALORA_CUDA_CHECK(launch_pdl(tc::attn_grp_merge_kernel<D>, dim3(a.M), dim3(256), 0, st, nullptr, 0, ta));
