@@ -1384,8 +1384,23 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
       for (int bn : {32, 64, 128, 256})
         if (fits(bn)) { BN = bn; break; }
   } else {
-    for (int bn : {base_epi == kEpiSwiglu ? 256 : 128, 128, 64, 32})
-      if (fits(bn)) { BN = bn; break; }
+    // 128 x 256 tiles when they cost fewer tile rounds: a 128 x 128 tile's K-block brings 32 KB through the
+    // L2 -> SM crossbar per 256 MMA cycles, which held the M = 1024 projections near 50% of the tensor pipe
+    // (ncu); a 256-wide tile does the same work in ~1.63x the time of a 128-wide one (measured), so it wins
+    // unless it adds a round of tiles over the 148 SMs (C3: o-proj / MLP-down 256 -> 128 tiles, one round;
+    // QKV stays at 128: 384 tiles in 3 rounds vs 192 in 2 x 1.63)
+    static const int large_bn = getenv("ALORA_LARGE_BN") ? atoi(getenv("ALORA_LARGE_BN")) : 0;  // A/B override
+    auto rounds = [&](int bn) { return (double)((m_tiles_ * (N / bn) + kNumSMs - 1) / kNumSMs); };
+    if (base_epi == kEpiSwiglu) {
+      if (fits(256)) BN = 256;
+    } else if (large_bn > 0) {
+      if (fits(large_bn)) BN = large_bn;
+    } else if (fits(256) && fits(128) && rounds(256) * 1.63 < rounds(128)) {
+      BN = 256;
+    }
+    if (BN == 0)
+      for (int bn : {128, 64, 32})
+        if (fits(bn)) { BN = bn; break; }
   }
   if (BN == 0) return ALORA_EINVAL;
   GemmArgs args{};

@@ -84,6 +84,8 @@ def _case(kind, B, D, H, Hkv, seed):
     ("decode", 16, 128, 32, 8), ("decode", 16, 64, 32, 8),
     ("mixed", 16, 128, 32, 8), ("mixed", 16, 64, 16, 2),
     ("long", 16, 128, 32, 8), ("long", 16, 64, 8, 8),
+    # B = 4 runs the TMA page-box producer (the cp.async producer needs 8-row swizzle groups per page)
+    ("eval", 4, 128, 32, 8), ("mixed", 4, 64, 16, 2), ("eval", 8, 128, 32, 8),
 ])
 def test_shared_prefix_attention_vs_dense(kind, B, D, H, Hkv):
     starts, lens, tables, pool, qs, ks, vs = _case(kind, B, D, H, Hkv, seed=B + D + H)
