@@ -513,23 +513,25 @@ int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_sl
 
 // ------------------------------------------------------------------------------------------------------------
 // Segmented LoRA shrink (model.py:141, `x @ down_t` of the rows that take the delta): the aLoRA eval step has
-// only the post-invocation rows (3 of a request's ~16-20 suffix rows) and decode rows on an adapter, a few
-// dozen per adapter, so the work is the adapter's down matrix streamed once (r x K bf16 per target) against
-// those rows -- bandwidth, not tensor throughput. One cluster of KS CTAs per (target, adapter slot), each CTA
-// one K slice:
-//   before the dependency wait  its down slice [R x Kc] streams into shared memory (cp.async; it does not
-//                               depend on the previous kernel, so the read overlaps the RMSNorm before)
-//   after it                    the slot's active rows (row_slot == slot and row_apply, in row order) are
-//                               listed, their h slices staged, and 8 warps compute [rows x R] partials over
-//                               K sub-slices with mma.sync m16n8k16 (ldmatrix from XOR-swizzled smem)
-//   reduction                   warps in warp order, then the cluster's CTAs in rank order through DSMEM
-//                               (deterministic), rank 0 writes s[t][row][slot*R + j] in bf16
-//   zero fill                   every other row's entries of this (t, slot) are written 0, so the expand GEMM
-//                               (extra K of the QKV GEMM) adds exact zeros there (base rows stay bitwise, model.py:145)
-// Rows are processed 64 at a time (any count is correct; the executor takes this path when each slot has at
-// most kSegMaxRows rows and the tensor-core shrink GEMM otherwise).
+// only the post-invocation rows of each request (and decode rows) on an adapter, a few dozen to a few hundred
+// per adapter, so the work is each adapter's down matrices streamed once against its own rows -- bandwidth, not
+// tensor throughput. Work item = (adapter slot, chunk of 64 of its active rows), one cluster of KS CTAs per item,
+// CTA `rank` owning the K range [rank K/KS, (rank+1) K/KS):
+//   before the dependency wait  the chunk's active rows (row_slot == slot and row_apply, in row order) are
+//                               listed (step metadata, not written by the kernels before)
+//   after it                    K sub-slices of 128 stream through a cp.async ring: the down rows of every
+//                               targeted plane [P*R x 128] and the chunk's h rows [64 x 128]; warp w computes the
+//                               [16-row tile w%4] x [half w/4 of the P*R columns] outputs with mma.sync m16n8k16,
+//                               each warp over the whole K range in order (no intra-CTA reduction)
+//   reduction                   the KS ranks' [64 x P*R] partials through DSMEM, summed in rank order (every rank
+//                               reduces a slice of the outputs), written to s[t][row][slot*R + j] in bf16
+//   zero fill                   chunk 0 of each slot writes 0 to every other row's entries of this slot in every
+//                               plane (and to all rows of an untargeted plane), so the expand GEMM (extra K of the
+//                               projection) adds exact zeros there (base rows stay bitwise, model.py:145)
+// KS depends on K only and a row's sums never depend on its chunk or warp: the result is batch invariant.
 constexpr int kSegThreads = 256;
 constexpr int kSegRowChunk = 64;
+constexpr int kSegKB = 128;  // K sub-slice per ring stage
 
 __device__ __forceinline__ uint32_t smem_u32addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -542,48 +544,52 @@ __device__ __forceinline__ void seg_ldsm4(uint32_t (&r)[4], const void* p) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(smem_u32addr(p)));
 }
+__device__ __forceinline__ void seg_ldsm2(uint32_t (&r)[2], const void* p) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+               : "=r"(r[0]), "=r"(r[1])
+               : "r"(smem_u32addr(p)));
+}
 __device__ __forceinline__ void seg_mma(float (&c)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
-// [rows][Kc] bf16 tile, 16-byte chunk c of row r at chunk (c ^ (r & 7))
-__device__ __forceinline__ int seg_off(int row, int k, int kc) {
+// [rows][kSegKB] bf16 tile, 16-byte chunk c of row r at chunk (c ^ (r & 7))
+__device__ __forceinline__ int seg_off(int row, int k) {
   const int c = (k >> 3) ^ (row & 7);
-  return row * kc + (c << 3) + (k & 7);
+  return row * kSegKB + (c << 3) + (k & 7);
 }
 
-template <int R>
+template <int R, int P>
+struct SegCfg {
+  static constexpr int kN = P * R;                      // output columns of an item (all planes)
+  static constexpr int kNT = kN / 8;                    // n8 tiles
+  static constexpr int kNTW = (kNT + 1) / 2;            // n8 tiles per warp (two column halves)
+  static constexpr int kStage = (kN + kSegRowChunk) * kSegKB * 2;
+  static constexpr int kRed = kSegRowChunk * kN * 4;
+  static constexpr int kStages = (200 * 1024 - kRed) / kStage < 4 ? (200 * 1024 - kRed) / kStage : 4;
+  static constexpr int kSmem = kStages * kStage + kRed;
+  static_assert(kStages >= 2, "shrink ring");
+};
+
+template <int R, int P>
 __global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
     const __nv_bfloat16* __restrict__ h, int M, int K, int KS, const int32_t* __restrict__ row_slot,
     const uint8_t* __restrict__ row_apply, const __nv_bfloat16* __restrict__ down, int n_slots,
     const uint8_t* __restrict__ slot_targets, __nv_bfloat16* __restrict__ s, int tbit0) {
+  using C = SegCfg<R, P>;
   extern __shared__ __align__(128) uint8_t seg_smem[];
-  const int Kc = K / KS;
-  __nv_bfloat16* sd = reinterpret_cast<__nv_bfloat16*>(seg_smem);           // [R][Kc] down slice
-  __nv_bfloat16* sh = sd + R * Kc;                                           // [kSegRowChunk][Kc] h rows
-  float* red = reinterpret_cast<float*>(sh + kSegRowChunk * Kc);            // [kSegRowChunk][R] CTA partial
-  int* rows = reinterpret_cast<int*>(red + kSegRowChunk * R);               // active rows of this slot
+  float* red = reinterpret_cast<float*>(seg_smem + C::kStages * C::kStage);  // [64][kN] this rank's partial
+  __shared__ int rows[kSegRowChunk];
   __shared__ int warp_cnt[kSegThreads / 32];
-  const int t = blockIdx.x / n_slots, slot = blockIdx.x % n_slots;
+  const int slot = blockIdx.x % n_slots, chunk = blockIdx.x / n_slots;
   const int rank = blockIdx.y;  // == cluster rank (cluster dims (1, KS, 1))
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int k0 = rank * Kc;
+  const int Kr = K / KS, k_base = rank * Kr, n_sub = Kr / kSegKB;
   const int ldS = n_slots * R;
-  const bool targeted = (slot_targets[slot] >> (tbit0 + t)) & 1;
-  // down slice: independent of the previous kernel
-  if (targeted) {
-    const __nv_bfloat16* dsrc = down + (((int64_t)t * n_slots + slot) * R) * K + k0;
-    for (int i = tid; i < R * (Kc / 8); i += kSegThreads) {
-      const int j = i / (Kc / 8), c = i % (Kc / 8);
-      seg_cp16(sd + seg_off(j, c * 8, Kc), dsrc + (int64_t)j * K + c * 8);
-    }
-    asm volatile("cp.async.commit_group;");
-  }
-  pdl_wait();
-  pdl_trigger();
-  // active rows in row order: per-warp counts over contiguous row ranges, then a prefix over warps
+  const int tmask = (slot_targets[slot] >> tbit0) & ((1 << P) - 1);
+  // active rows of this chunk (ordinals [chunk*64, chunk*64 + 64) among the slot's rows, in row order)
   const int per_warp = (M + (kSegThreads / 32) - 1) / (kSegThreads / 32);
   const int r_lo = warp * per_warp, r_hi = min(M, r_lo + per_warp);
   int cnt = 0;
@@ -598,170 +604,186 @@ __global__ void __launch_bounds__(kSegThreads) lora_shrink_seg_kernel(
     if (w < warp) base += warp_cnt[w];
     n_act += warp_cnt[w];
   }
-  // (rows[] holds at most kSegRowChunk entries per pass; larger counts are re-listed per chunk below)
-  // zero every inactive row of this (t, slot): ranks split the rows
+  const int c0 = chunk * kSegRowChunk, nc = max(0, min(kSegRowChunk, n_act - c0));
   {
+    int ord = base;
+    for (int r = r_lo + lane; r - lane < r_hi; r += 32) {
+      const bool act = r < r_hi && row_slot[r] == slot && row_apply[r];
+      const unsigned b = __ballot_sync(0xffffffffu, act);
+      const int my = ord + __popc(b & ((1u << lane) - 1));
+      if (act && my >= c0 && my < c0 + nc) rows[my - c0] = r;
+      ord += __popc(b);
+    }
+  }
+  __syncthreads();
+  const bool work = nc > 0 && tmask != 0;  // uniform over the cluster (same slot and chunk)
+  // down sub-slices do not depend on the previous kernel; h does
+  auto load_down = [&](int sub) {
+    __nv_bfloat16* sd = reinterpret_cast<__nv_bfloat16*>(seg_smem + (sub % C::kStages) * C::kStage);
+    const int k0 = k_base + sub * kSegKB;
+    for (int i = tid; i < C::kN * (kSegKB / 8); i += kSegThreads) {
+      const int q = i / (kSegKB / 8), c = i % (kSegKB / 8);
+      const int t = q / R, j = q % R;
+      if ((tmask >> t) & 1)
+        seg_cp16(sd + seg_off(q, c * 8), down + (((int64_t)t * n_slots + slot) * R + j) * K + k0 + c * 8);
+    }
+  };
+  auto load_h = [&](int sub) {
+    __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(seg_smem + (sub % C::kStages) * C::kStage) + C::kN * kSegKB;
+    const int k0 = k_base + sub * kSegKB;
+    for (int i = tid; i < kSegRowChunk * (kSegKB / 8); i += kSegThreads) {
+      const int rr = i / (kSegKB / 8), c = i % (kSegKB / 8);
+      if (rr < nc) seg_cp16(sh + seg_off(rr, c * 8), h + (int64_t)rows[rr] * K + k0 + c * 8);
+      else *reinterpret_cast<int4*>(sh + seg_off(rr, c * 8)) = make_int4(0, 0, 0, 0);
+    }
+  };
+  if (work)
+    for (int sub = 0; sub < min(n_sub, C::kStages - 1); ++sub) load_down(sub);
+  pdl_wait();
+  pdl_trigger();
+  if (chunk == 0) {  // zero every row of this slot that takes no delta, in every plane; ranks split the rows
     const int rows_per = (M + KS - 1) / KS;
     const int z0 = rank * rows_per, z1 = min(M, z0 + rows_per);
-    for (int i = tid; i < (z1 - z0) * (R / 8); i += kSegThreads) {
-      const int r = z0 + i / (R / 8), c = (i % (R / 8)) * 8;
-      if (targeted && row_slot[r] == slot && row_apply[r]) continue;
+    for (int i = tid; i < (z1 - z0) * P * (R / 8); i += kSegThreads) {
+      const int r = z0 + i / (P * (R / 8)), t = (i / (R / 8)) % P, c = (i % (R / 8)) * 8;
+      if (((tmask >> t) & 1) && row_slot[r] == slot && row_apply[r]) continue;
       *reinterpret_cast<int4*>(s + ((int64_t)t * M + r) * ldS + slot * R + c) = make_int4(0, 0, 0, 0);
     }
   }
-  if (!targeted || n_act == 0) return;  // uniform over the cluster: every rank sees the same counts
-  asm volatile("cp.async.wait_group 0;" ::: "memory");
-  for (int c0 = 0; c0 < n_act; c0 += kSegRowChunk) {
-    const int nc = min(kSegRowChunk, n_act - c0);
-    __syncthreads();  // the previous chunk's rows / red are no longer read
-    // list the chunk's rows (active ordinal in [c0, c0 + nc))
-    {
-      int ord = base;
-      for (int r = r_lo + lane; r - lane < r_hi; r += 32) {
-        const bool act = r < r_hi && row_slot[r] == slot && row_apply[r];
-        const unsigned b = __ballot_sync(0xffffffffu, act);
-        const int my = ord + __popc(b & ((1u << lane) - 1));
-        if (act && my >= c0 && my < c0 + nc) rows[my - c0] = r;
-        ord += __popc(b);
-      }
-    }
-    __syncthreads();
-    const int n_rt = (nc + 15) / 16;
-    for (int i = tid; i < n_rt * 16 * (Kc / 8); i += kSegThreads) {
-      const int rr = i / (Kc / 8), c = i % (Kc / 8);
-      if (rr < nc) seg_cp16(sh + seg_off(rr, c * 8, Kc), h + (int64_t)rows[rr] * K + k0 + c * 8);
-      else *reinterpret_cast<int4*>(sh + seg_off(rr, c * 8, Kc)) = make_int4(0, 0, 0, 0);
+  if (!work) return;
+  for (int sub = 0; sub < C::kStages - 1; ++sub) {  // exactly kStages - 1 groups, so the wait below is exact
+    if (sub < n_sub) load_h(sub);
+    asm volatile("cp.async.commit_group;");  // group `sub` = its h (+ every down issued so far)
+  }
+  const int rt = warp & 3, nh = warp >> 2;  // 16-row tile, column half
+  const bool rows_live = rt * 16 < nc;
+  float acc[C::kNTW][4];
+#pragma unroll
+  for (int f = 0; f < C::kNTW; ++f)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[f][e] = 0.f;
+  for (int sub = 0; sub < n_sub; ++sub) {
+    const int nxt = sub + C::kStages - 1;
+    if (nxt < n_sub) {
+      __syncthreads();  // stage nxt % kStages (last used by sub - 1) is no longer read
+      load_down(nxt);
+      load_h(nxt);
     }
     asm volatile("cp.async.commit_group;");
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    asm volatile("cp.async.wait_group %0;" ::"n"(C::kStages - 1) : "memory");
     __syncthreads();
-    // warp w: k sub-slices w, w + 8, ... of 16; partial [n_rt*16][R] in registers
-    float acc[kSegRowChunk / 16][R / 8][4];
+    const __nv_bfloat16* sd = reinterpret_cast<const __nv_bfloat16*>(seg_smem + (sub % C::kStages) * C::kStage);
+    const __nv_bfloat16* sh = sd + C::kN * kSegKB;
+    if (rows_live) {
 #pragma unroll
-    for (int a = 0; a < kSegRowChunk / 16; ++a)
-#pragma unroll
-      for (int f = 0; f < R / 8; ++f)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[a][f][e] = 0.f;
-    for (int ks = warp * 16; ks < Kc; ks += 16 * (kSegThreads / 32)) {
-      uint32_t bfr[R / 8][2];
-#pragma unroll
-      for (int f = 0; f < R / 8; f += 2) {
-        uint32_t r4[4];
-        const int j = f * 8 + (lane & 7) + ((lane >> 4) << 3);
-        const int kk = ks + ((lane >> 3) & 1) * 8;
-        seg_ldsm4(r4, sd + seg_off(j, kk, Kc));
-        bfr[f][0] = r4[0];
-        bfr[f][1] = r4[1];
-        if (f + 1 < R / 8) {
-          bfr[f + 1][0] = r4[2];
-          bfr[f + 1][1] = r4[3];
-        }
-      }
-#pragma unroll
-      for (int a = 0; a < kSegRowChunk / 16; ++a) {
-        if (a >= n_rt) break;
+      for (int ks = 0; ks < kSegKB; ks += 16) {
         uint32_t afr[4];
-        const int rr = a * 16 + (lane & 15);
-        const int kk = ks + (lane >> 4) * 8;
-        seg_ldsm4(afr, sh + seg_off(rr, kk, Kc));
+        seg_ldsm4(afr, sh + seg_off(rt * 16 + (lane & 15), ks + (lane >> 4) * 8));
 #pragma unroll
-        for (int f = 0; f < R / 8; ++f) seg_mma(acc[a][f], afr, bfr[f][0], bfr[f][1]);
-      }
-    }
-    // CTA reduction in warp order: warp 0 stores, then warps 1..7 add in turn
-    for (int w = 0; w < kSegThreads / 32; ++w) {
-      if (warp == w) {
-#pragma unroll
-        for (int a = 0; a < kSegRowChunk / 16; ++a) {
-          if (a >= n_rt) break;
-#pragma unroll
-          for (int f = 0; f < R / 8; ++f) {
-            const int r0 = a * 16 + (lane >> 2), c = f * 8 + (lane & 3) * 2;
-            float* p0 = red + r0 * R + c;
-            float* p1 = red + (r0 + 8) * R + c;
-            if (w == 0) {
-              p0[0] = acc[a][f][0]; p0[1] = acc[a][f][1]; p1[0] = acc[a][f][2]; p1[1] = acc[a][f][3];
-            } else {
-              p0[0] += acc[a][f][0]; p0[1] += acc[a][f][1]; p1[0] += acc[a][f][2]; p1[1] += acc[a][f][3];
-            }
-          }
+        for (int f = 0; f < C::kNTW; ++f) {
+          const int nt = nh * C::kNTW + f;
+          if (nt >= C::kNT) break;
+          uint32_t b2[2];
+          seg_ldsm2(b2, sd + seg_off(nt * 8 + (lane & 7), ks + ((lane >> 3) & 1) * 8));
+          seg_mma(acc[f], afr, b2[0], b2[1]);
         }
       }
-      __syncthreads();
     }
-    // cluster reduction in rank order on rank 0, through DSMEM
-    if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
-    if (rank == 0) {
-      for (int i = tid; i < nc * R; i += kSegThreads) {
-        float v = red[i];
-        for (int q = 1; q < KS; ++q) {
-          uint32_t ra;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32addr(red + i)), "r"(q));
-          float x;
-          asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
-          v += x;
-        }
-        const int rr = i / R, j = i % R;
-        s[((int64_t)t * M + rows[rr]) * ldS + slot * R + j] = __float2bfloat16_rn(v);
-      }
-    }
-    if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
   }
+  // this rank's partial -> smem (each warp its own outputs)
+  if (rows_live) {
+#pragma unroll
+    for (int f = 0; f < C::kNTW; ++f) {
+      const int nt = nh * C::kNTW + f;
+      if (nt >= C::kNT) break;
+      const int r0 = rt * 16 + (lane >> 2), c = nt * 8 + (lane & 3) * 2;
+      *reinterpret_cast<float2*>(red + r0 * C::kN + c) = make_float2(acc[f][0], acc[f][1]);
+      *reinterpret_cast<float2*>(red + (r0 + 8) * C::kN + c) = make_float2(acc[f][2], acc[f][3]);
+    }
+  }
+  if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
+  else __syncthreads();
+  // rank q sums outputs [q n / KS, (q+1) n / KS) over the ranks in rank order
+  const int n_out = nc * C::kN;
+  const int o0 = rank * n_out / KS, o1 = (rank + 1) * n_out / KS;
+  for (int i = o0 + tid; i < o1; i += kSegThreads) {
+    const int rr = i / C::kN, q = i % C::kN, t = q / R, j = q % R;
+    if (!((tmask >> t) & 1)) continue;
+    float v = 0.f;
+    for (int src = 0; src < KS; ++src) {
+      float x;
+      if (KS > 1) {
+        uint32_t ra;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(smem_u32addr(red + i)), "r"(src));
+        asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(x) : "r"(ra) : "memory");
+      } else {
+        x = red[i];
+      }
+      v += x;
+    }
+    s[((int64_t)t * M + rows[rr]) * ldS + slot * R + j] = __float2bfloat16_rn(v);
+  }
+  if (KS > 1) asm volatile("barrier.cluster.arrive.release;\n\tbarrier.cluster.wait.acquire;" ::: "memory");
 }
 
-template <int R>
-size_t seg_smem_of(int kc) {
-  return (size_t)R * kc * 2 + (size_t)kSegRowChunk * kc * 2 + (size_t)kSegRowChunk * R * 4 + kSegRowChunk * 4;
-}
-// K slices of one cluster: the smallest power of two <= 8 whose slice is <= 1024 wide and fits shared memory
-template <int R>
+// cluster size: 8 CTAs over K when every rank gets whole 128-wide sub-slices (fixed by K alone: batch invariant)
 int seg_split(int K) {
-  int KS = 1;
-  while ((K / KS > 1024 || seg_smem_of<R>(K / KS) > 200 * 1024) && KS < 8) KS *= 2;
-  return (K % (KS * 16) != 0 || seg_smem_of<R>(K / KS) > 220 * 1024) ? -1 : KS;
+  for (int ks : {8, 4, 2, 1})
+    if (K % (ks * kSegKB) == 0) return ks;
+  return -1;
 }
 
-bool lora_shrink_seg_fits(int K) { return K % 128 == 0 && seg_split<64>(K) > 0; }
+bool lora_shrink_seg_fits(int K) { return seg_split(K) > 0; }
 
-template <int R>
+template <int R, int P>
 int launch_shrink_seg(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                       const __nv_bfloat16* down, int n_slots, const uint8_t* slot_targets, __nv_bfloat16* s,
-                      cudaStream_t st, int P, int tbit0) {
-  auto smem_of = [](int kc) { return seg_smem_of<R>(kc); };
-  const int KS = seg_split<R>(K);
+                      cudaStream_t st, int tbit0, int max_rows) {
+  using C = SegCfg<R, P>;
+  const int KS = seg_split(K);
   if (KS < 1) return ALORA_EINVAL;
-  const int Kc = K / KS;
-  const size_t smem = smem_of(Kc);
-  static size_t configured = 0;
-  if (smem > configured) {
-    if (cudaFuncSetAttribute(lora_shrink_seg_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  static bool configured = false;
+  if (!configured) {
+    if (cudaFuncSetAttribute(lora_shrink_seg_kernel<R, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem) !=
         cudaSuccess)
       return ALORA_ECUDA;
-    configured = smem;
+    configured = true;
   }
+  const int chunks = std::max(1, (std::min(max_rows, M) + kSegRowChunk - 1) / kSegRowChunk);
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 1;
   attr[0].val.clusterDim.y = KS;
   attr[0].val.clusterDim.z = 1;
-  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_seg_kernel<R>, dim3(P * n_slots, KS), dim3(kSegThreads), smem, st, attr,
-                              KS > 1 ? 1 : 0, h, M, K, KS, row_slot, row_apply, down, n_slots, slot_targets, s,
-                              tbit0));
+  ALORA_CUDA_CHECK(launch_pdl(lora_shrink_seg_kernel<R, P>, dim3(n_slots * chunks, KS), dim3(kSegThreads), C::kSmem,
+                              st, attr, KS > 1 ? 1 : 0, h, M, K, KS, row_slot, row_apply, down, n_slots, slot_targets,
+                              s, tbit0));
   ALORA_LAUNCH_CHECK();
   return ALORA_OK;
 }
 
+template <int R>
+int launch_shrink_seg_p(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
+                        const __nv_bfloat16* down, int n_slots, const uint8_t* slot_targets, __nv_bfloat16* s,
+                        cudaStream_t st, int P, int tbit0, int max_rows) {
+  switch (P) {
+    case 1: return launch_shrink_seg<R, 1>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, tbit0, max_rows);
+    case 2: return launch_shrink_seg<R, 2>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, tbit0, max_rows);
+    case 3: return launch_shrink_seg<R, 3>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, tbit0, max_rows);
+    default: return ALORA_EINVAL;
+  }
+}
+
 int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                          const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
-                         __nv_bfloat16* s, cudaStream_t st, int P, int tbit0) {
+                         __nv_bfloat16* s, cudaStream_t st, int P, int tbit0, int max_rows) {
   if (M == 0 || n_slots == 0) return ALORA_OK;
-  if (K % 128 != 0 || P < 1 || tbit0 < 0 || tbit0 + P > 8) return ALORA_EINVAL;
+  if (K % kSegKB != 0 || P < 1 || P > 3 || tbit0 < 0 || tbit0 + P > 8) return ALORA_EINVAL;
   switch (R) {
-    case 8: return launch_shrink_seg<8>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
-    case 16: return launch_shrink_seg<16>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
-    case 32: return launch_shrink_seg<32>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
-    case 64: return launch_shrink_seg<64>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0);
+    case 8: return launch_shrink_seg_p<8>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0, max_rows);
+    case 16: return launch_shrink_seg_p<16>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0, max_rows);
+    case 32: return launch_shrink_seg_p<32>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0, max_rows);
+    case 64: return launch_shrink_seg_p<64>(h, M, K, row_slot, row_apply, down, n_slots, slot_targets, s, st, P, tbit0, max_rows);
     default: return ALORA_EINVAL;
   }
 }

@@ -56,13 +56,14 @@ int rmsnorm_bf16(const float* x, const int32_t* rows, int n_rows, int d, const f
 int lora_shrink_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                      const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets, __nv_bfloat16* s,
                      cudaStream_t st, int n_planes = 3, int tbit0 = 0);
-// Segmented shrink for steps with few delta rows per adapter: one CTA cluster per (target, slot) streams the
-// adapter's down rows once (K split over the cluster, DSMEM reduction in rank order), mma.sync over the
-// slot's active rows; writes the same [3][M][n_slots*R] layout (zeros elsewhere). R in {8, 16, 32, 64}.
+// Segmented shrink for steps with at most a few hundred delta rows per adapter: one CTA cluster per (slot,
+// chunk of 64 of its rows) streams the adapter's down rows of every plane (K split over the cluster, DSMEM
+// reduction in rank order), mma.sync over the slot's active rows; writes the same [n_planes][M][n_slots*R]
+// layout (zeros elsewhere). R in {8, 16, 32, 64}, n_planes in {1, 2, 3}; max_rows bounds any slot's row count.
 int lora_shrink_seg_bf16(const __nv_bfloat16* h, int M, int K, const int32_t* row_slot, const uint8_t* row_apply,
                          const __nv_bfloat16* down, int n_slots, int R, const uint8_t* slot_targets,
-                         __nv_bfloat16* s, cudaStream_t st, int n_planes = 3, int tbit0 = 0);
-bool lora_shrink_seg_fits(int K);  // the segmented kernel's K slice fits a <= 8-CTA cluster
+                         __nv_bfloat16* s, cudaStream_t st, int n_planes, int tbit0, int max_rows);
+bool lora_shrink_seg_fits(int K);  // K splits into whole 128-wide slices over the cluster
 constexpr int kSegMaxRows = 128;  // the executor's switch: at most this many delta rows per adapter slot
 int rope_bf16(__nv_bfloat16* qkv, int ld, const int32_t* positions, int M, int H, int Hkv, int D,
               const float* cos_t, const float* sin_t, cudaStream_t st);

@@ -309,6 +309,9 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const bool inv = d.batch_invariant != 0;
   const bool seg_ok = lora && d.d_model % 128 == 0 && (rk == 8 || rk == 16 || rk == 32 || rk == 64);
   const bool seg_shrink = seg_ok && (s.lora_rows_max <= kSegMaxRows || inv);
+  // row chunks of the segmented shrink: a function of the step's graph key (n_tokens and this switch), never of
+  // the exact per-slot counts, so a captured decode / prefill graph stays correct on replay
+  const int seg_rows = s.lora_rows_max <= kSegMaxRows ? kSegMaxRows : M;
   const bool lora_o = lora && !mdl.lora_o_down.empty(), lora_in = lora && !mdl.lora_in_down.empty();
   const bool lora_out = lora && !mdl.lora_out_down.empty();
   const int in_planes = llama ? 2 : 1;
@@ -382,7 +385,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       RUN("lora_shrink", 3.0 * d.n_slots * d.lora_rank * dm_ * 2 + d.n_slots * act * dm_ * 2 + 3.0 * m_ * ks_ * 2,
           2.0 * 3 * d.n_slots * act * d.lora_rank * dm_,
           lora_shrink_seg_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
-                               d.n_slots, d.lora_rank, d.slot_targets, sws, st));
+                               d.n_slots, d.lora_rank, d.slot_targets, sws, st, 3, 0, seg_rows));
     } else if (lora && inv) {
       RUN("lora_shrink", m_ * dm_ * 2 + 3.0 * ks_ * dm_ * 2 + 3.0 * m_ * ks_ * 2, 2.0 * 3 * m_ * ks_ * dm_,
           lora_shrink_bf16(h, M, dm, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(mdl.lora_down[l]),
@@ -440,7 +443,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     auto target_shrink = [&](const __nv_bfloat16* in, int K, const void* down, int planes, int tbit0) -> int {
       if (seg_shrink && lora_shrink_seg_fits(K))
         return lora_shrink_seg_bf16(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down),
-                                    d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0);
+                                    d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0, seg_rows);
       if (inv)
         return lora_shrink_bf16(in, M, K, s.row_slot, s.row_apply, static_cast<const __nv_bfloat16*>(down),
                                 d.n_slots, rk, d.slot_targets, sws, st, planes, tbit0);
