@@ -53,11 +53,17 @@ LLAMA_1B = dict(arch="llama", n_layers=16, n_heads=32, n_kv_heads=8, head_dim=64
                 vocab_size=128256, seed=0)
 LLAMA_8B = dict(arch="llama", n_layers=32, n_heads=32, n_kv_heads=8, head_dim=128, d_model=4096, ffn_dim=14336,
                 vocab_size=128256, seed=0)
+LLAMA_70B = dict(arch="llama", n_layers=80, n_heads=64, n_kv_heads=8, head_dim=128, d_model=8192, ffn_dim=28672,
+                 vocab_size=128256, seed=0)
 CONFIGS = {
     # BASELINE.json configs[1]: 1B + 3 adapters, 2k context, 4 instances x 3 adapters = 12 eval requests
     "c2": dict(model=LLAMA_1B, n_adapters=3, batch=4, context=2048, name="C2: Llama-3.2-1B + 3 aLoRA adapters r=32"),
     # BASELINE.json configs[2]: 8B + 8 adapters, 8k context, 8 instances x 8 adapters = 64 eval requests / replica
     "c3": dict(model=LLAMA_8B, n_adapters=8, batch=8, context=8192, name="C3: Llama-3-8B + 8 aLoRA adapters r=32"),
+    # BASELINE.json configs[4]: 70B + 4 adapters, 16k context, tensor parallel over the ranks (TP = world size;
+    # every rank runs the same requests on its shard, fused NVLink all-reduce + residual + RMSNorm)
+    "c5": dict(model=LLAMA_70B, n_adapters=4, batch=2, context=16384, tp=True,
+               name="C5: Llama-3-70B + 4 aLoRA adapters r=32, tensor parallel"),
 }
 B = 16
 BUDGET = 8192
@@ -72,6 +78,8 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
     ap.add_argument("--gen-len", type=int, default=256, help="base-turn generated tokens (y)")
+    ap.add_argument("--layers", type=int, default=None,
+                    help="override the model depth (C5 on fewer GPUs than its shards need; reported in config)")
     ap.add_argument("--adapter-gen", type=int, default=16)
     ap.add_argument("--lora-steps", type=int, default=5, help="timed LoRA-recompute eval turns")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -88,7 +96,9 @@ def parse():
 
 
 def workload(args):
-    c = CONFIGS[args.config]
+    c = dict(CONFIGS[args.config])
+    if args.layers:
+        c["model"] = dict(c["model"], n_layers=args.layers)
     x = c["context"] - args.gen_len - 4  # conversation + base output + EOT + 3-token invocation = context
     cached = ((x + args.gen_len - 1) // B) * B  # base-aligned hits ((x+y-1)//B)*B, SURVEY.md Appendix B
     return dict(c, x=x, cached=cached, suffix=c["context"] - cached)
@@ -105,7 +115,10 @@ def config_dict(args, world):
                         "per second of the TTFT-defining forward",
             "config": args.config, "context": w["context"], "eval_requests_per_replica": n_eval,
             "forward_rows_per_replica": n_eval * w["suffix"],
-            "parallelism": f"replicas x{world} (request-parallel, instance affinity)" if world > 1 else "1 GPU",
+            "parallelism": (f"TP={world} (Megatron shards, fused peer-memory all-reduce)" if w.get("tp")
+                            else f"replicas x{world} (request-parallel, instance affinity)") if world > 1 else "1 GPU",
+            **({"depth": f"{args.layers} of {CONFIGS[args.config]['model']['n_layers']} layers (--layers)"}
+               if args.layers else {}),
             "l2": "no flush needed: every step streams the weights (>= 2.5 GB) and the cached KV, both far above "
                   "the 126 MB L2",
             "decode": "synchronous" if args.sync_decode else "pipelined (Engine pipelined_decode)",
@@ -215,7 +228,7 @@ def run_reference(args):
     if int(os.environ.get("RANK", "0")) != 0:
         return
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
-    setup = oracle_setup(args)
+    setup = oracle_setup(args, n_layers=1 if workload(args).get("tp") else 2)  # 70B widths: one timed layer
     for _ in range(args.warmup):
         cpu_sample(args, setup)
     samples = [cpu_sample(args, setup) for _ in range(args.steps)]
@@ -224,7 +237,8 @@ def run_reference(args):
     t = statistics.median(times)
     value = workload(args)["context"] / t
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong" if workload(args).get("tp") else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
             "config": config_dict(args, world), "cpu_baseline": cpu,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -319,7 +333,8 @@ def probe_ranks(args):
     if world > 1:
         dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
     w = workload(args)
-    mine = replica_instances(w["batch"] * world, world, rank)
+    tp = bool(w.get("tp")) and world > 1
+    mine = replica_instances(w["batch"], 1, 0) if tp else replica_instances(w["batch"] * world, world, rank)
     every = [None] * world
     if world > 1:
         dist.all_gather_object(every, mine)
@@ -327,7 +342,7 @@ def probe_ranks(args):
         every = [mine]
     if rank == 0:
         print(json.dumps({"probe": "ranks", "n_gpus": world, "instances_per_rank": every,
-                          "eval_requests_total": sum(len(m) for m in every) * w["n_adapters"],
+                          "eval_requests_total": (len(every[0]) if tp else sum(len(m) for m in every)) * w["n_adapters"],
                           "config": config_dict(args, world)}), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -361,18 +376,24 @@ def main():
     from paper_2512_17910_b200.replicas import replica_instances
 
     w = workload(args)
+    tp = bool(w.get("tp")) and world > 1  # C5: the ranks are one tensor-parallel model, not replicas
     mcfg = P.ModelConfig(**w["model"], max_seq_len=w["context"] + args.adapter_gen + 64, dtype="bf16")
     n_eval = w["n_adapters"]
     blocks = -(-(w["context"] + args.adapter_gen) // B)
     # the LoRA arm recomputes every eval request (its own blocks) while the base turn's blocks stay cached
     pool_blocks = (w["batch"] * (n_eval + 1) + 8) * blocks
     max_batch = n_eval * w["batch"] + 8
-    model = P.Model(mcfg, init="device", max_tokens=BUDGET, max_seqs=max_batch)
-    mine = replica_instances(w["batch"] * world, world, rank)  # this replica's pipeline instances
+    if tp:
+        model = P.TPModel(mcfg, P.TorchDistGroup(), init="device", max_tokens=BUDGET, max_seqs=max_batch)
+    else:
+        model = P.Model(mcfg, init="device", max_tokens=BUDGET, max_seqs=max_batch)
+    n_inst = w["batch"] if tp else w["batch"] * world
+    # this replica's pipeline instances (every instance on every rank under TP)
+    mine = replica_instances(n_inst, 1, 0) if tp else replica_instances(n_inst, world, rank)
 
     def make_engine(mode):
         spec = P.PipelineSpec(pipeline="multi_adapter", mode=mode, prompt_len=w["x"], gen_len=args.gen_len,
-                              adapter_gen_len=args.adapter_gen, n_adapters=n_eval, batch=w["batch"] * world)
+                              adapter_gen_len=args.adapter_gen, n_adapters=n_eval, batch=n_inst)
         cfg = P.EngineConfig(model=mcfg, scheduler=P.SchedulerConfig(token_budget=BUDGET, max_batch_requests=max_batch),
                              pool_blocks=pool_blocks, block_size=B,
                              adapters=tuple(P.AdapterSpec(adapter_id=f"adapter{k}", rank=RANK_R, seed=k,
@@ -507,9 +528,10 @@ def main():
     tokens, fwd = ra["prompt_tokens"], ra["forward_s"]
     turn_ttft_s = a["turn_ttft_ms_median"] / 1e3
     vals = torch.tensor([tokens, fwd, turn_ttft_s], dtype=torch.float64, device="cuda")
-    if world > 1:  # aggregate over replicas: tokens summed, times max
+    if world > 1:  # aggregate: replicas sum their tokens (TP ranks share them), times are the max over ranks
         tok_sum = vals[0:1].clone()
-        dist.all_reduce(tok_sum, op=dist.ReduceOp.SUM)
+        if not tp:
+            dist.all_reduce(tok_sum, op=dist.ReduceOp.SUM)
         tmax = vals[1:].clone()
         dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
         tokens_all, fwd_max, ttft_max = float(tok_sum[0]), float(tmax[0]), float(tmax[1])
@@ -554,7 +576,7 @@ def main():
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         try:
-            setup = oracle_setup(args)
+            setup = oracle_setup(args, n_layers=1 if w.get("tp") else 2)
             samples = [cpu_sample(args, setup) for _ in range(2)]
             cpu = cpu_baseline_entry(args, [s[0] for s in samples], samples[0][2])
         except Exception as e:  # the CPU leg must not sink the GPU line
@@ -563,7 +585,8 @@ def main():
     value = tokens_all / fwd_max
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": fwd_max * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": fwd_max * 1e3, "higher_is_better": True, "scaling": "strong" if tp else "weak",
+        "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (random-init weights in HBM, random conversations)",
         "config": config_dict(args, world),
         "e2e": {"value": tokens_all / ttft_max, "unit": UNIT, "h2d_bytes_per_step": ra["h2d"],

@@ -99,3 +99,21 @@ def test_bench_gpus_flag_spawns_ranks():
     assert line["n_gpus"] == 2
     assert line["instances_per_rank"] == [list(range(0, 16, 2)), list(range(1, 16, 2))]
     assert line["eval_requests_total"] == 128
+
+
+def test_bench_c5_ranks_are_one_tensor_parallel_model():
+    """--config c5: the ranks are the shards of one TP model, so every rank runs every pipeline instance (no
+    instance split) and the requests are counted once."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--probe-ranks",
+                          "--config", "c5"], capture_output=True, text=True, timeout=240, env=env, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads([ln for ln in out.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2
+    assert line["instances_per_rank"] == [[0, 1], [0, 1]]
+    assert line["eval_requests_total"] == 8
+    assert line["config"]["parallelism"].startswith("TP=2")
