@@ -903,7 +903,7 @@ struct GrpArgs {
   int M;
   unsigned long long* trace;
   int exp;
-  long long* tl;  // ALORA_ATTN_TL=1: clock64 timeline of CTA (0, 0): [4 events][2 query tiles][256 tiles]
+  long long* tl;  // ALORA_ATTN_TL=1: clock64 timeline of CTA (0, 0): [6 events][2 query tiles][256 tiles]
 };
 
 // walks an item's segments tile by tile (64 keys per tile)
@@ -963,8 +963,11 @@ template <int D, int MT>
 constexpr int kGrpTmem = kGrpTmemUsed<D, MT> <= 256 ? 256 : 512;
 // P buffers per query tile (bf16 [128 rows][64 keys] in smem, the A operand of O += P V); at D=128 one buffer
 // (the softmax of tile t+1 rarely waits for PV_t) buys the sixth K/V stage
+#ifndef ALORA_GRP_NP
+#define ALORA_GRP_NP 1
+#endif
 template <int D, int MT>
-constexpr int kGrpNP = (D == 64 && MT == 2) ? 2 : 1;
+constexpr int kGrpNP = (D == 64 && MT == 2) ? 2 : ALORA_GRP_NP;
 // K/V ring stages: what the 227 KB of smem leaves after the P buffers (D=64 with one query tile keeps two CTAs
 // per SM)
 template <int D, int MT>
@@ -1351,7 +1354,9 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         f2_unpack(s2, l0, l1);
         l_run += l0 + l1;
       }
+      if ((warp & 3) == 0) GRP_TL(4, xt, t);
       if (t >= NP) sm100::mbar_wait_a(p_free_x + 8 * (t % NP), ((t / NP) - 1) & 1);  // PV_{t-NP} read this buffer
+      if ((warp & 3) == 0) GRP_TL(5, xt, t);
       {
         const uint32_t pb = p_row + (uint32_t)((t % NP) * L::kPBytes);
 #pragma unroll
@@ -1471,8 +1476,8 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
   static const bool timeline = getenv("ALORA_ATTN_TL") != nullptr;
   static long long* tlbuf = nullptr;
   if (timeline) {
-    if (!tlbuf) cudaMalloc(&tlbuf, sizeof(long long) * 4 * 2 * 256);
-    cudaMemsetAsync(tlbuf, 0, sizeof(long long) * 4 * 2 * 256, st);
+    if (!tlbuf) cudaMalloc(&tlbuf, sizeof(long long) * 6 * 2 * 256);
+    cudaMemsetAsync(tlbuf, 0, sizeof(long long) * 6 * 2 * 256, st);
     ta.tl = tlbuf;
   }
   static const bool tracing = getenv("ALORA_ATTN_TRACE") != nullptr;
@@ -1508,12 +1513,12 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
               ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3);
   }
   if (timeline) {  // per-tile means over CTA (0, 0), SM cycles
-    std::vector<long long> h(4 * 2 * 256);
+    std::vector<long long> h(6 * 2 * 256);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), tlbuf, h.size() * 8, cudaMemcpyDeviceToHost);
     auto at = [&](int ev, int x, int t) { return h[(ev * 2 + x) * 256 + t]; };
     for (int x = 0; x < MT; ++x) {
-      double soft = 0, wait_s = 0, s_lat = 0, pv_lag = 0;
+      double soft = 0, wait_s = 0, s_lat = 0, pv_lag = 0, pwait = 0;
       int n = 0;
       for (int t = 2; t < 250; ++t) {
         if (!at(0, x, t) || !at(1, x, t) || !at(2, x, t) || !at(3, x, t) || !at(1, x, t - 1)) break;
@@ -1521,12 +1526,13 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
         wait_s += at(0, x, t) - at(1, x, t - 1);  // softmax idle before S_t
         s_lat += at(0, x, t) - at(2, x, t);       // S_t issued -> softmax has it
         pv_lag += at(3, x, t) - at(1, x, t);      // P_t published -> PV_t issued
+        pwait += at(5, x, t) - at(4, x, t);       // softmax waiting for PV_{t-NP} before writing P_t
         ++n;
       }
       if (n)
         fprintf(stderr, "[attn grp timeline] tile %d: %d tiles, per tile (cycles): softmax %.0f, softmax idle %.0f, "
-                "S issue->softmax %.0f, P->PV issue %.0f, period %.0f\n", x, n, soft / n, wait_s / n, s_lat / n,
-                pv_lag / n, double(at(1, x, n + 1) - at(1, x, 1)) / n);
+                "S issue->softmax %.0f, P->PV issue %.0f, P-buffer wait %.0f, period %.0f\n", x, n, soft / n,
+                wait_s / n, s_lat / n, pv_lag / n, pwait / n, double(at(1, x, n + 1) - at(1, x, 1)) / n);
     }
   }
   if (merge) {
