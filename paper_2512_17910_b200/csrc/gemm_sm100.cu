@@ -231,8 +231,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                      const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_u,
                      const GemmArgs args) {
   using C = Cfg<BN>;
-  // the dependency wait comes after the setup and the first stages' weight loads (weights are never written by
-  // the kernels before): they overlap the previous kernel's tail (e.g. the RMSNorm producing A)
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
@@ -250,63 +250,45 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int per = (nkb_all + S - 1) / S;
   const int kb0 = min(nkb_all, split * per), kb1 = min(nkb_all, kb0 + per);
   int target = 0, nkl = 0;
+  uint32_t mask = 0;
   if (args.ks > 0 && split == S - 1) {
     target = lora_target(args, n0);
     nkl = (args.ks + kBK - 1) / kBK;
+    mask = args.tile_slot_mask[m_tile];
   }
 
-  const int pre = min(kb1 - kb0, C::kStages);  // stages whose weight half is issued before the dependency wait
-  const uint64_t pol_w = sm100::policy_evict_first();  // weights: streamed once per forward
-  if (warp == 0) {
-    if (lane == 0) {
-      sm100::prefetch_tmap(&tm_a);
-      sm100::prefetch_tmap(&tm_b);
-      for (int s = 0; s < C::kStages; ++s) {
-        sm100::mbar_init(&full[s], 1);
-        sm100::mbar_init(&empty[s], 1);
-      }
-      sm100::mbar_init(tmem_full, 1);
-      sm100::fence_barrier_init();
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tm_a);
+    sm100::prefetch_tmap(&tm_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
     }
-    __syncwarp();
-    for (int kb = kb0; kb < kb0 + pre; ++kb) {
-      if (sm100::elect_one()) {
-        uint8_t* sa = smem + (kb - kb0) * C::kStage;
-        sm100::mbar_arrive_expect_tx(&full[kb - kb0], C::kStage);
-        sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[kb - kb0], kb * kBK, n0, pol_w);
-      }
-      __syncwarp();
-    }
+    sm100::mbar_init(tmem_full, 1);
+    sm100::fence_barrier_init();
   }
-  // TMEM is allocated only after the dependency wait: a CTA parked in the wait must not hold columns a
-  // co-resident kernel of another stream (colocated tensor-parallel ranks) needs to make progress. The next
-  // kernel is released only after the wait too: released before it, the colocated ranks' early-launched grids
-  // starved the peers the fused all-reduce spins on (its timeout trap fired).
-  pdl_wait();
-  pdl_trigger();
   if (warp == 1) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  int n_iters = kb1 - kb0;
+  n_iters += lora_blocks_present(nkl, lora_np(args), args.rank, mask);
 
   // warp-converged loops, one elected lane per operation (see gemm_ws_kernel / gemm_bf16_persist_kernel)
   if (warp == 0) {
     const uint64_t pol_act = sm100::policy_evict_last();  // activations: re-read by every N tile
-    const uint32_t mask = nkl > 0 ? args.tile_slot_mask[m_tile] : 0u;
+    const uint64_t pol_w = sm100::policy_evict_first();   // weights: streamed once per forward
     int s = 0;
     uint32_t phase = 0;
     auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
     for (int kb = kb0; kb < kb1; ++kb) {
-      const bool early = kb < kb0 + pre;  // its weight half is in flight already
-      if (!early) sm100::mbar_wait(&empty[s], phase ^ 1);
+      sm100::mbar_wait(&empty[s], phase ^ 1);
       if (sm100::elect_one()) {
         uint8_t* sa = smem + s * C::kStage;
-        if (!early) {
-          sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
-          sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
-        }
+        sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
         sm100::tma_load_2d(sa, &tm_a, &full[s], kb * kBK, m0, pol_act);
+        sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
       }
       __syncwarp();
       next();
@@ -326,8 +308,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       next();
     }
   } else if (warp == 1) {
-    const int n_iters = (kb1 - kb0) + lora_blocks_present(nkl, lora_np(args), args.rank,
-                                                         nkl > 0 ? args.tile_slot_mask[m_tile] : 0u);
     constexpr uint32_t idesc = sm100::idesc_bf16_f32(kBM, BN);
     int s = 0;
     uint32_t phase = 0;
@@ -352,8 +332,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncwarp();
   } else {
     // epilogue warps: warp w owns TMEM lanes [32*(w%4), +32) = tile rows
-    const int n_iters = (kb1 - kb0) + lora_blocks_present(nkl, lora_np(args), args.rank,
-                                                         nkl > 0 ? args.tile_slot_mask[m_tile] : 0u);
     const int quarter = warp & 3;
     const int trow_idx = quarter * 32 + lane;
     sm100::mbar_wait(tmem_full, 0);
@@ -469,6 +447,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                              const __grid_constant__ CUtensorMap tm_s, const __grid_constant__ CUtensorMap tm_u,
                              const GemmArgs args) {
   using C = PCfg<BN>;
+  pdl_wait();
+  pdl_trigger();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStage);
@@ -484,6 +464,25 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkl = args.ks > 0 ? (args.ks + kBK - 1) / kBK : 0;
   if (threadIdx.x == 0) TRACE(0);
 
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tm_a);
+    sm100::prefetch_tmap(&tm_b);
+    for (int s = 0; s < C::kStages; ++s) {
+      sm100::mbar_init(&full[s], 1);
+      sm100::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      sm100::mbar_init(&tmem_full[b], 1);
+      sm100::mbar_init(&tmem_empty[b], 4);  // one arrival per epilogue warp
+    }
+    sm100::fence_barrier_init();
+  }
+  if (warp == 1) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // LoRA extra K of a tile: the m tile's slot mask decides which K blocks are present
   // Tile order: groups of up to kGroupM M tiles, M-fastest inside a group. The 148 CTAs in flight then cover
   // ~148 / group N tiles with every M tile of the group, so each weight tile is fetched from HBM once and
   // served to the group's CTAs from L2 (N-fastest order re-read the weights from HBM once per M tile: 5.8x
@@ -498,51 +497,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     n0 = (r / gs) * BN;
   };
 
-  // setup, then the first tile's first weight stages before the dependency wait (weights are never written by
-  // the kernels before): they overlap the previous kernel's tail (e.g. the RMSNorm producing A). TMEM is
-  // allocated only after the wait: a CTA parked there must not hold columns that a co-resident kernel of
-  // another stream (colocated tensor-parallel ranks) needs to make progress.
-  const uint64_t pol_w = sm100::policy_evict_normal();  // re-read by the m tiles in flight
-  const int pre = blockIdx.x < n_tiles ? min(nkb, C::kStages) : 0;
-  if (warp == 0) {
-    if (lane == 0) {
-      sm100::prefetch_tmap(&tm_a);
-      sm100::prefetch_tmap(&tm_b);
-      for (int s = 0; s < C::kStages; ++s) {
-        sm100::mbar_init(&full[s], 1);
-        sm100::mbar_init(&empty[s], 1);
-      }
-      for (int b = 0; b < 2; ++b) {
-        sm100::mbar_init(&tmem_full[b], 1);
-        sm100::mbar_init(&tmem_empty[b], 4);  // one arrival per epilogue warp
-      }
-      sm100::fence_barrier_init();
-    }
-    __syncwarp();
-    if (pre > 0) {
-      int m_tile, n0;
-      tile_of(blockIdx.x, m_tile, n0);
-      for (int kb = 0; kb < pre; ++kb) {
-        if (sm100::elect_one()) {
-          sm100::mbar_arrive_expect_tx(&full[kb], C::kStage);
-          sm100::tma_load_2d(smem + kb * C::kStage + C::kABytes, &tm_b, &full[kb], kb * kBK, n0, pol_w);
-        }
-        __syncwarp();
-      }
-    }
-  }
-  pdl_wait();
-  pdl_trigger();  // only after the wait (see gemm_bf16_kernel)
-  if (warp == 1) sm100::tmem_alloc<C::kTmemCols>(tmem_slot);
-  sm100::tc_fence_before();
-  __syncthreads();
-  sm100::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-
   // Producer and MMA loops run warp-converged with one elected lane per operation (see gemm_ws_kernel: a lone
   // lane looping while its siblings wait let ptxas clobber the MMA's uniform TMEM operand).
   if (warp == 0) {
     const uint64_t pol_act = sm100::policy_evict_last();
+    const uint64_t pol_w = sm100::policy_evict_normal();  // re-read by the m tiles in flight
     int s = 0;
     uint32_t phase = 0;
     auto next = [&] { if (++s == C::kStages) { s = 0; phase ^= 1; } };
@@ -551,15 +510,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       tile_of(t, m_tile, n0);
       const int m0 = m_tile * kBM;
       for (int kb = 0; kb < nkb; ++kb) {
-        const bool early = t == (int)blockIdx.x && kb < pre;  // its weight half is in flight already
-        if (!early) sm100::mbar_wait(&empty[s], phase ^ 1);
+        sm100::mbar_wait(&empty[s], phase ^ 1);
         if (sm100::elect_one()) {
           uint8_t* sa = smem + s * C::kStage;
-          if (!early) {
-            sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
-            sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
-          }
+          sm100::mbar_arrive_expect_tx(&full[s], C::kStage);
           sm100::tma_load_2d(sa, &tm_a, &full[s], kb * kBK, m0, pol_act);
+          sm100::tma_load_2d(sa + C::kABytes, &tm_b, &full[s], kb * kBK, n0, pol_w);
         }
         __syncwarp();
         next();
