@@ -903,7 +903,7 @@ struct GrpArgs {
   int M;
   unsigned long long* trace;
   int exp;
-  long long* tl;  // ALORA_ATTN_TL=1: clock64 timeline of CTA (0, 0): [6 events][2 query tiles][256 tiles]
+  long long* tl;  // ALORA_ATTN_TL=1: clock64 timeline of CTA (0, 0): [9 events][2 query tiles][256 tiles]
 };
 
 // walks an item's segments tile by tile (64 keys per tile)
@@ -1291,17 +1291,19 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       float sv[kKT];
       {
         const uint32_t ts = tS0 + (uint32_t)((t % NB) * 64);
+        uint32_t rv0[32], rv1[32];  // both loads in flight before the one wait
+        sm100::tmem_ld_32x32b_x32(ts, rv0);
+        sm100::tmem_ld_32x32b_x32(ts + 32, rv1);
+        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int c = 0; c < kKT; c += 32) {
-          uint32_t rv[32];
-          sm100::tmem_ld_32x32b_x32(ts + c, rv);
-          sm100::tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 32; ++j) sv[c + j] = __uint_as_float(rv[j]);
+        for (int j = 0; j < 32; ++j) {
+          sv[j] = __uint_as_float(rv0[j]);
+          sv[32 + j] = __uint_as_float(rv1[j]);
         }
       }
       sm100::tc_fence_before();
       sm100::mbar_arrive_a(s_free_x + 8 * (t % NB));  // S_{t+NB} may overwrite the buffer
+      if ((warp & 3) == 0) GRP_TL(6, xt, t);
       if (__any_sync(0xffffffffu, k0 + kKT - 1 > lim)) {
 #pragma unroll
         for (int j = 0; j < kKT; ++j)
@@ -1338,6 +1340,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
       // paired fp32 (FFMA2 / FADD2): half the FMA-pipe instructions of the scale and the row sum
       const uint64_t sc2 = f2_pack(sc, sc), nb2 = f2_pack(nb, nb);
+      if ((warp & 3) == 0) GRP_TL(7, xt, t);
       uint64_t acc2[4] = {0ull, 0ull, 0ull, 0ull};
       uint32_t pk[kKT / 2];
 #pragma unroll
@@ -1363,6 +1366,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
         for (int c = 0; c < 8; ++c)
           st_shared_v4(pb + (uint32_t)((c ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       }
+      if ((warp & 3) == 0) GRP_TL(8, xt, t);
       sm100::fence_proxy_async_smem();  // generic-proxy P stores -> tcgen05.mma operand reads
       sm100::mbar_arrive_a(p_full_x + 8 * (t % NP));
       if ((warp & 3) == 0) GRP_TL(1, xt, t);
@@ -1476,8 +1480,8 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
   static const bool timeline = getenv("ALORA_ATTN_TL") != nullptr;
   static long long* tlbuf = nullptr;
   if (timeline) {
-    if (!tlbuf) cudaMalloc(&tlbuf, sizeof(long long) * 6 * 2 * 256);
-    cudaMemsetAsync(tlbuf, 0, sizeof(long long) * 6 * 2 * 256, st);
+    if (!tlbuf) cudaMalloc(&tlbuf, sizeof(long long) * 9 * 2 * 256);
+    cudaMemsetAsync(tlbuf, 0, sizeof(long long) * 9 * 2 * 256, st);
     ta.tl = tlbuf;
   }
   static const bool tracing = getenv("ALORA_ATTN_TRACE") != nullptr;
@@ -1513,12 +1517,13 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
               ph[1] / live / 1e3, ph[2] / live / 1e3, ph[3] / live / 1e3);
   }
   if (timeline) {  // per-tile means over CTA (0, 0), SM cycles
-    std::vector<long long> h(6 * 2 * 256);
+    std::vector<long long> h(9 * 2 * 256);
     cudaStreamSynchronize(st);
     cudaMemcpy(h.data(), tlbuf, h.size() * 8, cudaMemcpyDeviceToHost);
     auto at = [&](int ev, int x, int t) { return h[(ev * 2 + x) * 256 + t]; };
     for (int x = 0; x < MT; ++x) {
-      double soft = 0, wait_s = 0, s_lat = 0, pv_lag = 0, pwait = 0;
+      double soft = 0, wait_s = 0, s_lat = 0, pv_lag = 0, pwait = 0, ph_ld = 0, ph_max = 0, ph_exp = 0, ph_st = 0,
+             ph_fence = 0;
       int n = 0;
       for (int t = 2; t < 250; ++t) {
         if (!at(0, x, t) || !at(1, x, t) || !at(2, x, t) || !at(3, x, t) || !at(1, x, t - 1)) break;
@@ -1527,12 +1532,20 @@ int launch_grp(const tc::GrpArgs& a, int n_items, bool merge, int64_t kv_rows, c
         s_lat += at(0, x, t) - at(2, x, t);       // S_t issued -> softmax has it
         pv_lag += at(3, x, t) - at(1, x, t);      // P_t published -> PV_t issued
         pwait += at(5, x, t) - at(4, x, t);       // softmax waiting for PV_{t-NP} before writing P_t
+        ph_ld += at(6, x, t) - at(0, x, t);       // S -> registers
+        ph_max += at(7, x, t) - at(6, x, t);      // mask, row max, lazy rescale
+        ph_exp += at(4, x, t) - at(7, x, t);      // exponentials, row sum, P packing
+        ph_st += at(8, x, t) - at(5, x, t);       // P stores
+        ph_fence += at(1, x, t) - at(8, x, t);    // proxy fence + arrive
         ++n;
       }
       if (n)
         fprintf(stderr, "[attn grp timeline] tile %d: %d tiles, per tile (cycles): softmax %.0f, softmax idle %.0f, "
                 "S issue->softmax %.0f, P->PV issue %.0f, P-buffer wait %.0f, period %.0f\n", x, n, soft / n,
                 wait_s / n, s_lat / n, pv_lag / n, pwait / n, double(at(1, x, n + 1) - at(1, x, 1)) / n);
+      if (n)
+        fprintf(stderr, "[attn grp timeline] tile %d softmax phases (cycles): S->regs %.0f, max/rescale %.0f, exp %.0f, "
+                "P stores %.0f, fence+arrive %.0f\n", x, ph_ld / n, ph_max / n, ph_exp / n, ph_st / n, ph_fence / n);
     }
   }
   if (merge) {
