@@ -127,8 +127,10 @@ class Model:
         self._graphs = bool(graphs) and (config or ModelConfig()).dtype == "bf16"
         c0 = config or ModelConfig()
         # shared-prefix attention: spans holding the same leading blocks (adapters on one conversation) read
-        # that prefix once (alora_plan_attention + the grouped kernel); ALORA_SHARED_PREFIX=0 disables it (A/B)
+        # that prefix once (alora_plan_attention + the grouped kernel) when a cost estimate says it pays
+        # (_plan_attention); shared_prefix="always" takes every group, False / ALORA_SHARED_PREFIX=0 none
         import os
+        self._shared_prefix_always = shared_prefix == "always"
         # batch_invariant (bf16): a token's KV / logits are bitwise independent of the step that computed it
         # (alora_sm100a.h AloraModelDesc.batch_invariant); the fp32 tier is invariant by construction
         self.batch_invariant = bool(batch_invariant) and c0.dtype == "bf16"
@@ -535,6 +537,16 @@ class Model:
         else:
             raise RuntimeError("alora_plan_attention: plan buffer sizing failed")
         if int(out[2]) == S:  # no group formed: the per-span kernels serve the step
+            return None
+        # Grouping pays when the prefix bytes it saves outweigh its fixed cost: the per-span kernels stream
+        # every span's keys at ~5 TB/s, the grouped one runs at ~0.8 PFLOP/s plus ~25 us of per-CTA setup and
+        # partition merge (B200, measured: C3, 8 adapters x 8k, grouped 169 vs per-span 432 us per layer; C2,
+        # 3 adapters x 2k, grouped 33 vs per-span 25 us)
+        n_q = np.diff(cu).astype(np.float64)
+        ends = starts.astype(np.float64) + n_q
+        span_s = float(ends.sum()) * 2 * cfg.kv_width * 2 / 5e12
+        grp_s = 4.0 * cfg.n_heads * cfg.head_dim * float((n_q * (starts + n_q / 2)).sum()) / 0.8e15 + 25e-6
+        if span_s < grp_s and not self._shared_prefix_always:
             return None
         return out[:n]
 

@@ -203,8 +203,8 @@ def test_c2_geometry_eval_turn_and_decode_vs_oracle():
     _assert_parity(res)
     pre, dec = kinds[0], kinds[1]
     assert _has(pre, "gemm_qkv", "gemm_ws_kernel<") and _has(pre, "gemm_mlp_in", "gemm_ws_kernel<")
-    # the requests of a conversation share its prefix blocks: the shared-prefix kernel serves both steps
-    assert _has(pre, "attention", "attn_grp_kernel<64,") and _has(dec, "attention", "attn_grp_kernel<64,")
+    # 3 adapters over a 2k prefix: grouping does not pay (model.py cost estimate), the per-span kernels run
+    assert _has(pre, "attention", "attn_tc_kernel<64") and _has(dec, "attention", "attn_decode_kernel")
     assert _has(pre, "rmsnorm", "residual_rmsnorm_kernel")
     assert _has(pre, "lora_shrink", "lora_shrink_seg_kernel") and _has(dec, "lora_shrink", "lora_shrink_seg_kernel")
     assert _has(dec, "gemm_qkv", "gemm_dec_kernel") and _has(dec, "gemm_lm_head", "gemm_dec_kernel")
