@@ -17,13 +17,14 @@
 //   warps 2..5  epilogue: tcgen05.ld 32 lanes x 32 cols -> fused epilogue -> global
 // mbarrier ring: full[s] (TMA tx bytes) / empty[s] (tcgen05.commit), tmem_full.
 //
-// Weight-streaming launches (few output tiles: small M) split K across a
-// thread-block cluster of up to 8 CTAs (cluster dims 1x1xS) so that every SM
-// streams a disjoint slab of the weights exactly once. Each CTA parks its fp32
-// partial tile in its own shared memory; after a cluster barrier CTA r reduces
-// rows [r*128/S, (r+1)*128/S) over distributed shared memory, summing the S
-// partials in rank order (deterministic), and runs the epilogue for those
-// rows. No global partials, no second kernel.
+// Kernels by step shape (gemm_bf16 at the end of this file picks one):
+//   M <= 32    gemm_dec_kernel: swap-AB (128 weight rows as the MMA's M, the tokens as N = 16 / 32)
+//   M <= 256   gemm_ws_kernel: weight streaming, one CTA per (N tile, K split) covering every token row;
+//              K splits are deferred: fp32 partials are TMA-stored and summed in split order by the consuming
+//              kernel (residual RMSNorm / QKV finalize), so every SM streams a disjoint weight slab once
+//   M > 256    gemm_bf16_persist_kernel (more tiles than SMs: one CTA per SM, two TMEM accumulators, grouped
+//              tile order) or gemm_bf16_kernel (one tile per CTA; co-resident split-K through global partials
+//              and arrival counters when the tiles cannot fill half the SMs); 128 x 128 or 128 x 256 tiles
 // Epilogues: bf16 store, fp32 store, residual add (C += acc), ReLU, SwiGLU of
 // 64-interleaved gate|up blocks, rotate-half RoPE on q/k columns, and the
 // LoRA-shrink row/slot select.
