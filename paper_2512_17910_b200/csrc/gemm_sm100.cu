@@ -69,6 +69,9 @@ struct GemmArgs {
   int sel_sr, sel_rank;
   int sel_tbit0;  // target bit of plane 0 in sel_targets
   unsigned long long* argmax;  // fused greedy argmax of the fp32-store epilogue (ws kernel, S == 1)
+  __nv_bfloat16* kv_pool;      // paged KV scatter of the K / V columns (GemmLora::kv_pool)
+  const int32_t* kv_slots;
+  int kv_q, kv_w, kv_layer, kv_layers, kv_block;
   int splits;                 // K splits (blockIdx.z); grid <= SM count, cooperative launch
   float* partial;             // [splits][m_tiles*128][N] fp32 when splits > 1
   int* counters;              // 2 per output tile (arrive, depart); zero between launches
@@ -155,6 +158,18 @@ __device__ __forceinline__ int units_per_row(const GemmArgs& a, int n0) {
 }
 
 // Emit one unit for `row`; fetch(c0, v) provides the 32 fp32 accumulators of tile columns [c0, c0+32).
+// 32 bf16 output columns [col, col + 32) of `row` that fall in the K or V section also go to the row's pool slot
+__device__ __forceinline__ void kv_scatter(const GemmArgs& a, int row, int col, const float (&v)[32]) {
+  const int c = col - a.kv_q;
+  if (!a.kv_pool || c < 0 || c >= 2 * a.kv_w) return;
+  const int slot = a.kv_slots[row];
+  if (slot < 0) return;
+  const int sel = c >= a.kv_w ? 1 : 0;
+  const int64_t blk = slot / a.kv_block, off = slot % a.kv_block;
+  store_bf16x32(a.kv_pool + (((blk * a.kv_layers + a.kv_layer) * 2 + sel) * a.kv_block + off) * a.kv_w +
+                    (c - sel * a.kv_w), v, false);
+}
+
 template <int BN, typename Fetch>
 __device__ __forceinline__ void emit_unit(const GemmArgs& a, int n0, int row, int u, Fetch&& fetch) {
   const bool live = row < a.M;
@@ -180,6 +195,8 @@ __device__ __forceinline__ void emit_unit(const GemmArgs& a, int n0, int row, in
     __nv_bfloat16* d1 = static_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + n0 + hb + i * 32;
     store_bf16x32(d1, r1, false);
     store_bf16x32(d1 + half, r2, false);
+    kv_scatter(a, row, n0 + hb + i * 32, r1);
+    kv_scatter(a, row, n0 + hb + half + i * 32, r2);
     return;
   }
   if (epi == kEpiSwiglu) {
@@ -223,6 +240,7 @@ __device__ __forceinline__ void emit_unit(const GemmArgs& a, int n0, int row, in
       *reinterpret_cast<float4*>(dst + q * 4) = make_float4(v[q * 4], v[q * 4 + 1], v[q * 4 + 2], v[q * 4 + 3]);
   } else {
     store_bf16x32(static_cast<__nv_bfloat16*>(a.C) + (int64_t)row * a.ldc + col, v, epi == kEpiRelu);
+    if (epi == kEpiRope) kv_scatter(a, row, col, v);  // the V columns (past the rotated q | k heads)
   }
 }
 
@@ -1565,6 +1583,17 @@ int gemm_bf16(int epi, const __nv_bfloat16* A, int lda, const __nv_bfloat16* Bt,
   if (splits > 1) {
     args.partial = static_cast<float*>(ws->partial);
     args.counters = ws->counters;
+  }
+  if (splits == 1 && base_epi == kEpiRope && lora && lora->kv_pool && lora->kv_slots && lora->kv_w % 32 == 0 &&
+      lora->kv_q % 32 == 0 && lora->kv_block > 0 && defer) {
+    args.kv_pool = lora->kv_pool;
+    args.kv_slots = lora->kv_slots;
+    args.kv_q = lora->kv_q;
+    args.kv_w = lora->kv_w;
+    args.kv_layer = lora->kv_layer;
+    args.kv_layers = lora->kv_layers;
+    args.kv_block = lora->kv_block;
+    defer->kv_written = true;
   }
   static const bool no_persist = getenv("ALORA_GEMM_NO_PERSIST") != nullptr;  // A/B switch
   if (splits == 1 && !no_persist && tiles > kNumSMs) {  // several tiles per SM: overlap epilogues with MMAs

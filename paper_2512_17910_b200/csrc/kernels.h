@@ -113,6 +113,13 @@ struct GemmLora {
   // fp32-store epilogue of a weight-streaming launch: per row, atomicMax of (orderable logit << 32 | ~col),
   // i.e. the greedy token with ties to the lowest id (model.py:190-195), fused into the lm_head
   unsigned long long* argmax = nullptr;
+  // Paged KV scatter in the QKV epilogue (large-M tile / persistent kernels, one K split): columns
+  // [kv_q, kv_q + kv_w) (K, after RoPE) and [kv_q + kv_w, kv_q + 2 kv_w) (V) of row m also go to slot
+  // kv_slots[m] of the pool [NB, kv_layers, 2, kv_block, kv_w] at layer kv_layer (model.py:217-222); the GEMM
+  // reports it through GemmDefer::kv_written
+  __nv_bfloat16* kv_pool = nullptr;
+  const int32_t* kv_slots = nullptr;
+  int kv_q = 0, kv_w = 0, kv_layer = 0, kv_layers = 0, kv_block = 0;
 };
 // Split-K scratch: fp32 partial rows + 2 arrival counters per output tile (zeroed once, self-resetting).
 constexpr int kGemmCounters = 16384;
@@ -142,6 +149,7 @@ struct GemmDefer {
   int64_t capacity = 0;
   int splits_out = 1;
   bool deferred = false;  // partials [splits_out][M][N] were written and the epilogue is the consumer's job
+  bool kv_written = false;  // the epilogue scattered K / V into the paged pool (GemmLora::kv_pool)
 };
 // ws enables split-K of the per-tile kernel (M > 256; max_splits caps it) when the output tiles cannot fill
 // the 148 SMs.

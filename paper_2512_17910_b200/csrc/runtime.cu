@@ -410,6 +410,14 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       gl.rope_sin = d.rope_sin;
       gl.rope_cols = Nq + Nkv;
       gl.head_dim = D;
+      // large-M steps: the epilogue also scatters K / V into the paged pool (no separate kv_write pass)
+      gl.kv_pool = static_cast<__nv_bfloat16*>(d.kv_pool);
+      gl.kv_slots = s.slot_mapping;
+      gl.kv_q = Nq;
+      gl.kv_w = Nkv;
+      gl.kv_layer = l;
+      gl.kv_layers = d.n_layers;
+      gl.kv_block = d.block_size;
     }
     GemmDefer dq;
     dq.partial = part;
@@ -421,7 +429,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
       RUN("qkv_finalize", m_ * Nqkv_ * 4.0 * dq.splits_out + 2.0 * m_ * Nqkv_ + 2.0 * 2 * m_ * Nkv * 2, 0,
           qkv_finalize_bf16(part, dq.splits_out, M, Nq, Nkv, D, s.positions, d.rope_cos, d.rope_sin, qkv, Nqkv,
                             s.slot_mapping, static_cast<__nv_bfloat16*>(d.kv_pool), d.n_layers, l, d.block_size, st));
-    } else {
+    } else if (!dq.kv_written) {
       RUN("kv_write", 2.0 * 2 * m_ * Nkv * 2, 0,
           kv_write(ALORA_BF16, qkv + Nq, qkv + Nq + Nkv, Nqkv, s.slot_mapping, M, Nkv, d.kv_pool, d.n_layers, l,
                    d.block_size, st));
