@@ -1,10 +1,10 @@
 #!/bin/bash
-# Attention bottleneck experiments at the C3 eval step (4 layers): per-kernel profile with the softmax math and/or
-# the tensor-core MMAs switched off (ALORA_ATTN_EXP bits: 16 = no softmax work, 64 = no MMA; outputs are wrong,
-# only times are read), the per-CTA phase trace, and the MT=1 variant.
+# Attention bottleneck experiments at the C3 eval step (4 layers): per-kernel profile with the tensor-core MMAs
+# switched off (ALORA_ATTN_EXP=64; outputs are wrong, only times are read), the per-CTA phase trace, and the
+# one-query-tile variant.
 set -u
 L=${L:-4}
-for e in 0 16 64 80; do
+for e in 0 64; do
   echo "== ALORA_ATTN_EXP=$e"
   ALORA_ATTN_EXP=$e PROFILE=1 timeout 300 python tools/eval_step.py c3 eval 5 $L 2>&1 | grep -E "step|attention"
 done
