@@ -210,6 +210,8 @@ extern "C" int64_t alora_plan_attention(int32_t S, const int32_t* cu_q, const in
         best_p = p;
       }
     }
+    static const int force_p = getenv("ALORA_ATTN_PARTS") ? atoi(getenv("ALORA_ATTN_PARTS")) : 0;  // A/B
+    if (force_p > 0) best_p = std::min(force_p, kMaxParts);
   }
   std::vector<Item> final_items;
   std::vector<int> final_segs;
