@@ -1020,6 +1020,17 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
   int rows_t[MT];
 #pragma unroll
   for (int x = 0; x < MT; ++x) rows_t[x] = max(0, min(kQT, n_tok * G - (mtile * MT + x) * kQT));
+  // Decode-like sets (at most 32 GQA-packed rows, e.g. 8 adapters x 4 heads decoding on one conversation): one
+  // softmax warp would carry every row through all 64 keys of each tile (~1 us per tile). Instead the rows are
+  // replicated into the 4 TMEM lane quadrants of query tile 0 and quadrant q takes only keys [16q, 16q + 16) of
+  // every tile (its P row is zero elsewhere), so the 4 warps split the exponentials; the 4 copies' (m, l, O)
+  // combine in the epilogue like KV partitions.
+  const int set_rows = n_tok * G;
+  const bool rep4 = MT == 2 && set_rows <= 32;
+  if (rep4) {
+    rows_t[0] = kQT;
+    rows_t[1] = 0;
+  }
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (tid == 0) ATTN_TRACE(0);
   long long* tl = (a.tl && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0) ? a.tl : nullptr;
@@ -1242,8 +1253,10 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     pdl_wait();
     const int xt = warp >> 2;  // query tile
     const int r = (warp & 3) * 32 + lane;
-    const bool live = r < rows_t[xt];
-    const int pr = (mtile * MT + xt) * kQT + r;
+    const int copy = rep4 ? (warp & 3) : 0;  // key quarter of this row copy (rep4)
+    const int lr = rep4 ? lane : r;          // row within the tile's packed rows
+    const bool live = rep4 ? lr < set_rows : r < rows_t[xt];
+    const int pr = (mtile * MT + xt) * kQT + lr;
     const int row = live ? a.set_tok[tok_off + pr / G] : 0;
     const int head = kvh * G + pr % G;
     const int pos = live ? a.positions[row] : -1;
@@ -1278,6 +1291,27 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     SegCursor cur;
     cur.init(a.segs, seg_b, seg_e);
     int lim = -1, lim_seg = -1;
+    if (rep4) {  // this row's P columns outside its key quarter stay zero for the whole kernel
+#pragma unroll
+      for (int b2 = 0; b2 < NP; ++b2)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) st_shared_v4(p_row + (uint32_t)(b2 * L::kPBytes + (c << 4)), 0u, 0u, 0u, 0u);
+    }
+    // O *= corr once the previous PV has landed (lazy rescale: the row max grew by more than 2^8)
+    auto rescale_o = [&](int t, float corr) {
+      sm100::mbar_wait_a(p_free_x + 8 * ((t - 1) % NP), ((t - 1) / NP) & 1);  // O holds PV_{t-1}
+      sm100::tc_fence_after();
+#pragma unroll 1
+      for (int c = 0; c < D; c += 16) {  // 16 columns at a time: the scores stay in registers
+        uint32_t ov[16];
+        sm100::tmem_ld_32x32b_x16(tO + lane_base + c, ov);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int j = 0; j < 16; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
+        sm100::tmem_st_32x32b_x16(tO + lane_base + c, ov);
+      }
+      sm100::tmem_st_wait();
+    };
     for (int t = 0; t < n_tiles; ++t) {
       if (cur.j != lim_seg) {
         lim_seg = cur.j;
@@ -1288,6 +1322,52 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       sm100::mbar_wait_a(s_full_x + 8 * (t % NB), (t / NB) & 1);
       sm100::tc_fence_after();
       if ((warp & 3) == 0) GRP_TL(0, xt, t);
+      if (rep4) {  // ---- this copy's 16 keys of the tile
+        float sq[16];
+        {
+          uint32_t rv[16];
+          sm100::tmem_ld_32x32b_x16(tS0 + (uint32_t)((t % NB) * 64 + 16 * copy), rv);
+          sm100::tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < 16; ++j) sq[j] = __uint_as_float(rv[j]);
+        }
+        sm100::tc_fence_before();
+        sm100::mbar_arrive_a(s_free_x + 8 * (t % NB));
+        const int kq = k0 + 16 * copy;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (kq + j > lim) sq[j] = -INFINITY;
+        float mt = sq[0];
+#pragma unroll
+        for (int j = 1; j < 16; ++j) mt = fmaxf(mt, sq[j]);
+        const float m_new = fmaxf(m_run, mt);
+        const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
+        if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
+          const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
+          rescale_o(t, corr);
+          l_run *= corr;
+        }
+        if (grow) m_run = m_new;
+        const float nb = m_run == -INFINITY ? 0.f : -m_run * sc;
+        uint32_t pk[8];
+        float ls = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float p0 = fast_exp2(fmaf(sq[2 * j], sc, nb)), p1 = fast_exp2(fmaf(sq[2 * j + 1], sc, nb));
+          ls += p0 + p1;
+          pk[j] = pack_bf16(p0, p1);
+        }
+        l_run += ls;
+        if (t >= NP) sm100::mbar_wait_a(p_free_x + 8 * (t % NP), ((t / NP) - 1) & 1);
+        const uint32_t pb = p_row + (uint32_t)((t % NP) * L::kPBytes);
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+          st_shared_v4(pb + (uint32_t)(((2 * copy + c) ^ (r & 7)) << 4), pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                       pk[4 * c + 3]);
+        sm100::fence_proxy_async_smem();
+        sm100::mbar_arrive_a(p_full_x + 8 * (t % NP));
+        continue;
+      }
       float sv[kKT];
       {
         const uint32_t ts = tS0 + (uint32_t)((t % NB) * 64);
@@ -1322,18 +1402,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
       const bool grow = m_new > m_run + thr || (m_run == -INFINITY && m_new != -INFINITY);
       if (t > 0 && __any_sync(0xffffffffu, grow && m_run != -INFINITY)) {
         const float corr = grow && m_run != -INFINITY ? fast_exp2((m_run - m_new) * sc) : 1.f;
-        sm100::mbar_wait_a(p_free_x + 8 * ((t - 1) % NP), ((t - 1) / NP) & 1);  // O holds PV_{t-1}
-        sm100::tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < D; c += 16) {  // 16 columns at a time: the scores stay in registers
-          uint32_t ov[16];
-          sm100::tmem_ld_32x32b_x16(tO + lane_base + c, ov);
-          sm100::tmem_ld_wait();
-#pragma unroll
-          for (int j = 0; j < 16; ++j) ov[j] = __float_as_uint(__uint_as_float(ov[j]) * corr);
-          sm100::tmem_st_32x32b_x16(tO + lane_base + c, ov);
-        }
-        sm100::tmem_st_wait();
+        rescale_o(t, corr);
         l_run *= corr;
       }
       if (grow) m_run = m_new;
@@ -1374,6 +1443,62 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
     if (tid == 0) ATTN_TRACE(3);
     sm100::mbar_wait_a(p_free_x + 8 * ((n_tiles - 1) % NP), ((n_tiles - 1) / NP) & 1);  // O holds the last PV
     sm100::tc_fence_after();
+    if (rep4) {
+      // combine the 4 row copies through smem (the K/V ring is free: every MMA has completed): [copy][32][D] O,
+      // [copy][32] (m, l); copy 0's warp writes the row
+      float* xo = reinterpret_cast<float*>(sm + L::kK);
+      float* xml = xo + 4 * 32 * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 32) {
+        uint32_t ov[32];
+        sm100::tmem_ld_32x32b_x32(tO + lane_base + c, ov);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          *reinterpret_cast<float4*>(xo + ((copy * 32 + lane) * D + c + 4 * q)) =
+              make_float4(__uint_as_float(ov[4 * q]), __uint_as_float(ov[4 * q + 1]), __uint_as_float(ov[4 * q + 2]),
+                          __uint_as_float(ov[4 * q + 3]));
+      }
+      xml[(copy * 32 + lane) * 2] = m_run == -INFINITY ? -INFINITY : m_run * sc;
+      xml[(copy * 32 + lane) * 2 + 1] = l_run;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the 4 softmax warps of query tile 0
+      if (copy == 0 && live) {
+        float mc[4], wc[4], mx = -INFINITY, l = 0.f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          mc[q] = xml[(q * 32 + lane) * 2];
+          if (xml[(q * 32 + lane) * 2 + 1] > 0.f) mx = fmaxf(mx, mc[q]);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float lq = xml[(q * 32 + lane) * 2 + 1];
+          wc[q] = lq > 0.f ? fast_exp2(mc[q] - mx) : 0.f;
+          l += wc[q] * lq;
+        }
+        const float inv4 = l > 0.f ? 1.f / l : 0.f;
+        for (int c = 0; c < D; c += 8) {
+          float o8[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc += wc[q] * xo[(q * 32 + lane) * D + c + e];
+            o8[e] = acc;
+          }
+          if (p_index < 0) {
+            __align__(16) __nv_bfloat162 o2[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) o2[e] = __floats2bfloat162_rn(o8[2 * e] * inv4, o8[2 * e + 1] * inv4);
+            *reinterpret_cast<int4*>(a.out + (int64_t)row * a.ld_out + head * D + c) = *reinterpret_cast<int4*>(o2);
+          } else {
+            const int64_t slot = ((int64_t)p_index * a.M + row) * a.H + head;
+            __stcg(reinterpret_cast<float4*>(a.ws_o + slot * D + c), make_float4(o8[0], o8[1], o8[2], o8[3]));
+            __stcg(reinterpret_cast<float4*>(a.ws_o + slot * D + c + 4), make_float4(o8[4], o8[5], o8[6], o8[7]));
+            if (c == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(mx, l));
+          }
+        }
+      }
+    } else {
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
     for (int c = 0; c < D; c += 32) {
@@ -1403,6 +1528,7 @@ __global__ void __launch_bounds__(kGrpThreads<PW, MT>, (D == 64 && MT == 1) ? 2 
                              __uint_as_float(ov[q * 4 + 2]), __uint_as_float(ov[q * 4 + 3])));
         if (oc == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml + slot * 2), make_float2(m_run * sc, l_run));
       }
+    }
     }
   }
   sm100::tc_fence_before();
