@@ -55,6 +55,7 @@ struct Core {
   bool chunked, prefix_caching;
   std::vector<Req> reqs;
   std::mutex intake_mu;
+  std::vector<std::vector<int64_t>> spare_tok;  // token buffers of retired requests (<= 256), reused by submit
   std::vector<int32_t> intake;  // handles in submit (ticket) order
   std::deque<int32_t> waiting;
   std::vector<int32_t> prefilling, decoding;
@@ -227,8 +228,15 @@ int32_t alora_sched_submit(void* s, const int64_t* prompt, int64_t n, int32_t ma
   if (mode == kActivated && (inv_start < 0 || inv_start > n)) return ALORA_EINVAL;
   Core& c = *C(s);
   Req r;
+  {  // a retired request's token buffer when one is parked (no fresh pages on the submit path)
+    std::lock_guard<std::mutex> l(c.intake_mu);
+    if (!c.spare_tok.empty()) {
+      r.tok = std::move(c.spare_tok.back());
+      c.spare_tok.pop_back();
+    }
+  }
+  r.tok.reserve(static_cast<size_t>(n + max_new));  // one allocation for the prompt and every generated token
   r.tok.assign(prompt, prompt + n);
-  r.tok.reserve(static_cast<size_t>(n + max_new));
   r.prompt_len = n;
   r.max_new = max_new;
   r.mode = mode;
@@ -388,7 +396,13 @@ int alora_sched_retire(void* s, int32_t h) {
   }
   r.chain.clear();
   r.chain.shrink_to_fit();
-  std::vector<int64_t>().swap(r.tok);  // the Python Request keeps the tokens
+  {  // the Python Request keeps the tokens; the buffer is parked for the next submit
+    std::vector<int64_t> buf;
+    buf.swap(r.tok);
+    buf.clear();
+    std::lock_guard<std::mutex> l(c.intake_mu);
+    if (c.spare_tok.size() < 256) c.spare_tok.push_back(std::move(buf));
+  }
   return rc;
 }
 

@@ -230,9 +230,11 @@ def test_detect_invocation():
     with pytest.raises(ValueError):
         P.detect_invocation([1, 2], [])
     rng = np.random.default_rng(1)
-    for _ in range(200):
-        p = rng.integers(0, 3, int(rng.integers(1, 20)))
-        inv = rng.integers(0, 3, int(rng.integers(1, 4)))
+    for i in range(400):
+        # short prompts (one window) and long ones (> 512 tokens: the 256-token tail window, then the whole prompt)
+        n = int(rng.integers(1, 20)) if i % 2 else int(rng.integers(500, 1200))
+        p = rng.integers(-1, 3, n) if i % 3 == 0 else rng.integers(0, 3 if n < 20 else 6, n)
+        inv = rng.integers(0, 3, int(rng.integers(1, 4 if n < 20 else 6)))
         try:
             want = O.detect_invocation(p, inv)
         except ValueError:
