@@ -92,10 +92,6 @@ int alora_pool_views(void* pool, int32_t** ref, int32_t** fill, uint8_t** has_ha
 int32_t alora_pool_num_free(void* pool);
 /* find_cached_prefix walk (kv_cache.py:154-183): pins and returns the hit count (>= 0). */
 int64_t alora_pool_lookup(void* pool, const uint8_t* digests, int64_t n, int32_t* out_ids);
-/* Pins blocks a lookup of the same scheduler step already returned for an identical digest prefix (the shared
- * conversation prefix of several adapters' requests): the same ref-count / LRU effect as the lookup hits, without
- * the index walk. Used by the native admission core (csrc/sched_core.cpp cache_lookup). */
-int alora_pool_pin(void* pool, const int32_t* ids, int64_t n);
 /* allocate (kv_cache.py:192-218): ALORA_ENOSPC and no change when n > free blocks. */
 int alora_pool_allocate(void* pool, int64_t n, int32_t* out_ids);
 /* release of a request's blocks, tail first (kv_cache.py:258-270). */

@@ -104,7 +104,6 @@ EXPORTS = {
     "alora_pool_views": _sig("alora_pool_views", c_i32, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p),
     "alora_pool_num_free": _sig("alora_pool_num_free", c_i32, c_void_p),
     "alora_pool_lookup": _sig("alora_pool_lookup", c_i64, c_void_p, c_void_p, c_i64, c_void_p),
-    "alora_pool_pin": _sig("alora_pool_pin", c_i32, c_void_p, c_void_p, c_i64),
     "alora_pool_allocate": _sig("alora_pool_allocate", c_i32, c_void_p, c_i64, c_void_p),
     "alora_pool_release": _sig("alora_pool_release", c_i32, c_void_p, c_void_p, c_i64),
     "alora_pool_publish": _sig("alora_pool_publish", c_i32, c_void_p, c_void_p, c_void_p, c_i64),

@@ -128,19 +128,6 @@ int64_t alora_pool_lookup(void* pool, const uint8_t* digests, int64_t n, int32_t
   return hits;
 }
 
-int alora_pool_pin(void* pool, const int32_t* ids, int64_t n) {
-  if (pool == nullptr || n < 0 || (n > 0 && ids == nullptr)) return ALORA_EINVAL;
-  Pool* p = P(pool);
-  for (int64_t i = 0; i < n; ++i)
-    if (ids[i] < 0 || ids[i] >= p->nb) return ALORA_EINVAL;
-  for (int64_t i = 0; i < n; ++i) {  // a lookup hit's effect, in the same order
-    const int32_t b = ids[i];
-    if (p->ref[b] == 0) p->unlink(b);
-    ++p->ref[b];
-  }
-  return ALORA_OK;
-}
-
 int alora_pool_allocate(void* pool, int64_t n, int32_t* out_ids) {
   if (pool == nullptr || n < 0 || (n > 0 && out_ids == nullptr)) return ALORA_EINVAL;
   Pool* p = P(pool);

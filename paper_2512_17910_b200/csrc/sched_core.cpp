@@ -60,10 +60,6 @@ struct Core {
   std::deque<int32_t> waiting;
   std::vector<int32_t> prefilling, decoding;
   std::vector<int32_t> scratch;
-  // the last admission lookup of the current step (cache_lookup's shared-prefix fast path); reset per step
-  std::vector<uint8_t> last_chain;
-  std::vector<int32_t> last_ids;
-  int64_t last_hits = 0;
   // blocks [0, base_blocks) of an n_blocks sequence carry the base key "" (compute_block_keys, kv_cache.py:72-96)
   int64_t base_blocks(const Req& r, int64_t n_blocks) const {
     if (r.mode == kBase) return n_blocks;
@@ -139,26 +135,9 @@ int cache_lookup(Core& c, Req& r) {
       r.chain.resize(static_cast<size_t>(limit) * 16);
     }
     r.blocks.resize(static_cast<size_t>(limit));
-    // the previous lookup of this step (an adapter's request on the same conversation) already walked the index
-    // for the digests this chain shares with it: its pinned hits are pinned again, the walk resumes after them
-    // (allocations between the two lookups only evict unpinned blocks, so the result is the full walk's)
-    int64_t known = 0;
-    const int64_t cap = std::min<int64_t>(limit, c.last_hits);
-    while (known < cap && std::memcmp(r.chain.data() + known * 16, c.last_chain.data() + known * 16, 16) == 0) ++known;
-    if (known > 0) {
-      const int rc = alora_pool_pin(c.pool, c.last_ids.data(), known);
-      if (rc != ALORA_OK) return rc;
-      std::memcpy(r.blocks.data(), c.last_ids.data(), static_cast<size_t>(known) * sizeof(int32_t));
-    }
-    const int64_t m = limit > known ? alora_pool_lookup(c.pool, r.chain.data() + known * 16, limit - known,
-                                                         r.blocks.data() + known)
-                                    : 0;
-    if (m < 0) return static_cast<int>(m);
-    const int64_t n = known + m;
+    const int64_t n = limit ? alora_pool_lookup(c.pool, r.chain.data(), limit, r.blocks.data()) : 0;
+    if (n < 0) return static_cast<int>(n);
     r.blocks.resize(static_cast<size_t>(n));
-    c.last_chain = r.chain;
-    c.last_ids.assign(r.blocks.begin(), r.blocks.end());
-    c.last_hits = n;
     r.hit = n * c.B;
   } else {
     r.blocks.clear();
@@ -316,7 +295,6 @@ int alora_sched_step(void* s, int32_t* spans, int32_t span_cap, int32_t* failed,
     if (!emit(h, r.processed, r.processed + 1, 1)) return ALORA_EINVAL;
     budget -= 1;
   }
-  c.last_hits = 0;  // pool state may have changed since the previous step (commits, releases)
   if (c.prefix_caching) prehash(c, c.max_batch - n_spans);
   // prefills strictly FCFS: running prefills, then the waiting queue (scheduler.py:186-210)
   std::vector<int32_t> order(c.prefilling.begin(), c.prefilling.end());
