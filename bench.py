@@ -603,7 +603,12 @@ def main():
                      "frac": achieved / peak, "traffic": traffic,
                      "basis": "algorithmic bytes/flops per launch (runtime.cu tags, DESIGN.md §4) / CUDA-event "
                               "launch time on the launch stream",
-                     "peak_source": "MEASURED_PEAKS.json" if peaks else "B200_PROFILING.md fallback"},
+                     "peak_source": ("MEASURED_PEAKS.json (burst: each kernel is timed on its own, event-bracketed)"
+                                     if peaks else "B200_PROFILING.md fallback"),
+                     # the sustained tensor figure (cuBLAS back to back for 4 s under the same power cap) beside it
+                     "peak_sustained": peaks.get("bf16_tflops_sustained") if bound == "tensor" else None,
+                     "frac_sustained": (achieved / peaks["bf16_tflops_sustained"]
+                                        if bound == "tensor" and peaks.get("bf16_tflops_sustained") else None)},
         "kernels": kernels,
         "cpu_baseline": cpu,
         "clocks": ra["clocks"],
