@@ -295,8 +295,18 @@ def test_submit_validation():
         eng.submit(np.zeros((2, 3), dtype=np.int64))
     with pytest.raises(ValueError):
         eng.submit([1, 2], max_new_tokens=0)
-    with pytest.raises(ValueError):
+    with pytest.raises(ValueError, match=r"\[0, 256\), got \[1, 256\]"):
         eng.submit([1, 256])
+    with pytest.raises(ValueError, match=r"got \[-1, 5\]"):  # negative ids wrap to >= 2**63 in the range check
+        eng.submit([5, -1])
+    with pytest.raises(ValueError):
+        eng.submit(np.array([3, -(2 ** 63)], dtype=np.int64))
+    # the native core reuses retired requests' token buffers: a shorter prompt after a longer one is intact
+    a = eng.submit(list(range(1, 40)), max_new_tokens=1)
+    eng.run_until_idle()
+    b = eng.submit([7, 8, 9], max_new_tokens=1)
+    eng.run_until_idle()
+    assert list(eng.finished[a].prompt) == list(range(1, 40)) and list(eng.finished[b].prompt) == [7, 8, 9]
     with pytest.raises(ValueError):
         eng.submit([1] * 100, max_new_tokens=8093)
     with pytest.raises(ValueError):
