@@ -20,7 +20,7 @@
 // slots (ld.acquire.sys); the value is a per-block epoch counter kept on the device (the same sequence of
 // calls on every rank), so the kernel is CUDA-graph capturable. Partials alternate between two slots by call
 // parity: a rank rewrites a slot only after the barrier of the next call, which every peer enters after it
-// finished reading that slot.
+// finished reading that slot. The two-shot reduced rows alternate the same way.
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kTpThreads) tp_ar_norm_kernel(const TpArgs a, 
 }
 
 struct TpLayout {
-  int64_t part[2], redx, redh, flags, epoch, total;
+  int64_t part[2], redx[2], redh[2], flags, epoch, total;
 };
 
 TpLayout tp_layout(int64_t T, int64_t d) {
@@ -174,8 +174,10 @@ TpLayout tp_layout(int64_t T, int64_t d) {
   L.epoch = take((int64_t)kTpMaxBlocks * 4);
   L.part[0] = take(T * d * 4);
   L.part[1] = take(T * d * 4);
-  L.redx = take(T * d * 4);
-  L.redh = take(T * d * 2);
+  L.redx[0] = take(T * d * 4);
+  L.redh[0] = take(T * d * 2);
+  L.redx[1] = take(T * d * 4);
+  L.redh[1] = take(T * d * 2);
   L.total = off;
   return L;
 }
@@ -204,7 +206,10 @@ int tp_allreduce_norm(void* const* peers, int n, int rank, int colocated, int ma
   // above, where reading N full partials would cost N x the traffic of a reduce-scatter + all-gather
   a.one_shot = (int64_t)M * d * 4 * n <= (int64_t)4 << 20;
   a.part_off = L.part[slot & 1];
-  a.redx_off = L.redx; a.redh_off = L.redh; a.flags_off = L.flags; a.epoch_off = L.epoch;
+  // the reduced rows alternate by call parity too: block b of a rank rewrites them right after ITS barrier of
+  // the next call, while a peer's block b' != b (the row -> block map changes with M) may still be gathering
+  // this call's rows; two calls later every peer's kernel of this call has completed (stream order)
+  a.redx_off = L.redx[slot & 1]; a.redh_off = L.redh[slot & 1]; a.flags_off = L.flags; a.epoch_off = L.epoch;
   a.x = x; a.w = w; a.eps = eps; a.h = h;
   a.timeout_trap = 1;
   const int rows = a.one_shot ? M : (M + n - 1) / n;
