@@ -374,7 +374,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   const double tp_bytes = m_ * dm_ * 4.0 * (d.tp_size + 2) + m_ * dm_ * 2;
   for (int l = 0; l < d.n_layers; ++l) {
     if (!h_ready)
-      RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+      RUN("rmsnorm", m_ * dm_ * (pend ? 10.0 + 4.0 * pend : 6.0), 0,
           residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.attn_norm[l], d.rms_eps, h, st));
     h_ready = false;
     pend = 0;
@@ -481,7 +481,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
     if (tp_fused) RUN("tp_allreduce", tp_bytes, 0, tp_reduce(mdl.mlp_norm[l], true));
     else if (tp) RUN("tp_allreduce", m_ * dm_ * 4.0, 0, d.tp_allreduce(d.tp_ctx, tpd, (int64_t)M * dm, st));
     if (!h_ready)
-      RUN("rmsnorm", m_ * dm_ * (6 + 8.0 * pend), 0,
+      RUN("rmsnorm", m_ * dm_ * (pend ? 10.0 + 4.0 * pend : 6.0), 0,
           residual_rmsnorm_bf16(x, pend_buf, pend, M, nullptr, M, dm, mdl.mlp_norm[l], d.rms_eps, h, st));
     h_ready = false;
     pend = 0;
@@ -510,7 +510,7 @@ int forward_bf16(Model& mdl, const AloraStepDesc& s, cudaStream_t st) {
   // greedy argmax fused into the lm_head epilogue (weight-streaming path: S <= 256 spans, vocab % 32 == 0)
   auto* amax = reinterpret_cast<unsigned long long*>(base + w.amax);
   const bool fused_argmax = S <= 256 && d.vocab % 32 == 0;
-  RUN("rmsnorm", S_ * dm_ * (6 + 8.0 * pend), 0,
+  RUN("rmsnorm", S_ * dm_ * (pend ? 10.0 + 4.0 * pend : 6.0), 0,
       residual_rmsnorm_bf16(x, pend_buf, pend, M, s.last_row, S, dm, d.final_norm, d.rms_eps, hf, st,
                             fused_argmax ? amax : nullptr));
   GemmLora glm;
