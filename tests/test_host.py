@@ -30,6 +30,17 @@ def test_library_exports_every_header_symbol():
     assert "sm_100a" in P.native_version()
 
 
+def test_tp_symmetric_buffer_layout():
+    # flags + epochs, two partial slots, and two (call-parity) sets of reduced x (fp32) / h (bf16) rows
+    for T, d in ((16, 64), (300, 4096), (8192, 8192)):
+        total = _native.lib.alora_tp_buffer_bytes(T, d)
+        p0, p1 = (_native.lib.alora_tp_partial_offset(T, d, s) for s in (0, 1))
+        assert 0 < p0 < p1 and p1 - p0 >= T * d * 4
+        assert _native.lib.alora_tp_partial_offset(T, d, 2) == p0  # slots alternate by call parity
+        assert total - (p1 + T * d * 4) >= 2 * (T * d * 4 + T * d * 2)
+    assert _native.lib.alora_tp_buffer_bytes(0, 64) == _native.ALORA_EINVAL
+
+
 def test_native_hash_matches_reference_kats_and_chains():
     g = golden_json("hash_kat.json")
     for row in g["kats"]:
